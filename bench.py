@@ -1,0 +1,324 @@
+"""Benchmark: adaptive sketched-LUPP column ID (BASELINE.json configs[1]) on B200.
+
+Workload (N = 1): ``rand_lupp_adaptive(A.T, b=64, tau=1e-8, Gaussian, RngStream(0))``
+on a 20000 x 20000 fp64 fast-decay matrix (singular values 1e-16^((i-1)/(n-1))
+behind Haar bases), i.e. the column ID of A to absolute Frobenius tolerance
+1e-8.  A is synthetic (generated on the device, seed 0); one "step" is one full
+adaptive ID.  Metric: TFLOP/s of algorithmic work
+    F = 2 m n (k + b) + 2 m k^2 - (4/3) k^3
+with k the detected rank.  ms_per_step is the seconds figure.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference times the reference algorithm on the host cores (the CPU
+oracle port under oracle/, numpy/OpenBLAS with all cores) on a bounded sample
+of the same workload: the first 8 blocks of the same adaptive loop.
+
+N > 1 (torchrun): every rank runs an independent replica on its own matrix
+(seed + rank); no collective on the data path ("replicas", weak scaling).
+"""
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+FP64_DMMA_PEAK_TFLOPS = 37.1  # tools/dmma_peak.cu on this pool (profiles/r01_probe_box.log)
+FP64_PEAK_SOURCE = "measured DMMA m16n8k16 register-only peak (tools/dmma_peak.cu); MEASURED_PEAKS.json has no fp64 entry"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--n", type=int, default=20000)
+    p.add_argument("--b", type=int, default=64)
+    p.add_argument("--tau", type=float, default=1e-8)
+    p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--e2e-steps", type=int, default=2)
+    p.add_argument("--cpu-blocks", type=int, default=8)
+    p.add_argument("--no-cpu", action="store_true")
+    return p.parse_args()
+
+
+def algo_flops(m, n, k, b):
+    return 2.0 * m * n * (k + b) + 2.0 * m * k * k - (4.0 / 3.0) * k ** 3
+
+
+def gen_fast_decay_device(n, beta, seed, device):
+    """Haar-basis fast-decay matrix generated on the GPU (input generation only;
+    torch/cuSOLVER QR is not on the measured path)."""
+    import torch
+
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+
+    def haar():
+        q, r = torch.linalg.qr(torch.randn(n, n, generator=g, dtype=torch.float64, device=device))
+        s = torch.sign(torch.diagonal(r))
+        s[s == 0] = 1.0
+        return q * s
+
+    u = haar()
+    v = haar()
+    d = beta ** (torch.arange(n, dtype=torch.float64, device=device) / (n - 1))
+    a = (u * d) @ v.T
+    del u, v
+    torch.cuda.synchronize()
+    return a
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = [r.split(", ") for r in (self.out or "").strip().splitlines() if r.strip()]
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                mx = max(mx, float(r[2]))
+                for nm, val in zip(names, r[5:9]):
+                    if val.strip() == "Active":
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_sample(a_host, b, tau, seed, blocks):
+    """Reference algorithm (oracle port) on the host cores: first `blocks`
+    blocks of the adaptive loop.  Returns (seconds, rank, flops, cores)."""
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import randskel_oracle as orc
+    from threadpoolctl import threadpool_limits
+
+    cores = os.cpu_count() or 1
+    with threadpool_limits(limits=cores):
+        t0 = time.perf_counter()
+        out = orc.rand_lupp_adaptive(a_host, b, tau, seed, 0, want_w=True, max_blocks=blocks)
+        dt = time.perf_counter() - t0
+    m, n = a_host.shape
+    return dt, out["rank"], algo_flops(m, n, out["rank"], b), cores
+
+
+def reference_arm(args, rank):
+    if rank != 0:
+        return
+    import torch
+
+    dev = torch.device("cuda", 0) if torch.cuda.is_available() else None
+    n = args.n
+    if dev is not None:
+        a = gen_fast_decay_device(n, 1e-16, args.seed, dev).cpu().numpy()
+    else:  # no GPU: generate on the host (slow for large n)
+        sys.path.insert(0, os.path.join(REPO, "oracle"))
+        import randskel_oracle as orc
+        a, _ = orc.gen_fast_decay(n, n, 1e-16, args.seed)
+    at = a.T
+    for _ in range(max(0, min(args.warmup, 1))):
+        cpu_sample(at, args.b, args.tau, args.seed, args.cpu_blocks)
+    times, flops = [], []
+    for _ in range(args.steps):
+        dt, k, f, cores = cpu_sample(at, args.b, args.tau, args.seed, args.cpu_blocks)
+        times.append(dt)
+        flops.append(f)
+    ms = 1e3 * float(np.median(times))
+    val = flops[0] / (ms * 1e-3) / 1e12
+    sample = (f"first {args.cpu_blocks} blocks (rank 0 -> {k}) of the adaptive loop on the same "
+              f"{n}x{n} fast-decay matrix; numpy/OpenBLAS oracle port, median of {args.steps}")
+    line = {
+        "impl": "reference", "metric": "adaptive column-ID throughput (algorithmic TFLOP/s)",
+        "value": val, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"cfg2 adaptive column ID {n}x{n} fp64 fast-decay, b={args.b}, "
+                               f"tau={args.tau:g} (abs), bounded CPU sample", "n": n, "b": args.b},
+        "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        reference_arm(args, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    import paper_2310_09417_b200 as rs
+    from paper_2310_09417_b200 import _lib, skeleton
+
+    lib = _lib.load()
+    n, b, tau = args.n, args.b, args.tau
+    seed = args.seed + rank
+    a = gen_fast_decay_device(n, 1e-16, seed, dev)
+    spec = rs.SketchSpec("gaussian", n, b)
+
+    def step():
+        return rs.rand_lupp_adaptive(a.T, b, tau, spec, rs.RngStream(seed))
+
+    for _ in range(args.warmup):
+        res = step()
+    torch.cuda.synchronize()
+
+    # ---------------- timed region: device-resident A, device result ----------
+    timer = skeleton.PhaseTimer()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = lib.rs_launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        skeleton._PHASE_TIMER = timer
+        e0.record()
+        for _ in range(args.steps):
+            res = step()
+        e1.record()
+        torch.cuda.synchronize()
+        skeleton._PHASE_TIMER = None
+    if world > 1:
+        dist.barrier()
+    launches = lib.rs_launch_count() - launches0
+    ms = e0.elapsed_time(e1) / args.steps
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    k = res.rank
+    f = algo_flops(n, n, k, b)
+    value = world * f / (ms_max * 1e-3) / 1e12
+
+    phases = timer.totals()
+    counts = timer.launches()
+    blocks = counts.get("sketch_gemm", 0)
+    sketch_flops = blocks * 2.0 * n * n * b
+    sketch_ms = phases.get("sketch_gemm", float("nan"))
+    achieved = sketch_flops / (sketch_ms * 1e-3) / 1e12 if sketch_ms else float("nan")
+    roofline = {
+        "bound": "tensor", "kernel": "dgemm_kernel (sketch Y = A^T Omega_t, DMMA fp64)",
+        "achieved": achieved, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+        "frac": achieved / FP64_DMMA_PEAK_TFLOPS, "traffic": None,
+        "peak_source": FP64_PEAK_SOURCE,
+        "per_launch_flops": 2.0 * n * n * b,
+        "launches": blocks,
+        "avg_launch_ms": sketch_ms / max(blocks, 1),
+        "share_of_step": sketch_ms / (ms * args.steps),
+    }
+    phase_ms = {kk: v / args.steps for kk, v in phases.items()}
+
+    # ---------------- e2e: host numpy in, host numpy out -----------------------
+    a_host_t = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+    a_host_t.copy_(a)
+    a_host = a_host_t.numpy()
+    torch.cuda.synchronize()
+    e2e_ms = []
+    for _ in range(args.e2e_steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res_h = rs.rand_lupp_adaptive(a_host.T, b, tau, spec, rs.RngStream(seed))
+        torch.cuda.synchronize()
+        e2e_ms.append(1e3 * (time.perf_counter() - t0))
+    e2e_t = torch.tensor([float(np.median(e2e_ms))], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_ms_max = float(e2e_t.item())
+    nblk = len(res_h.trace) + 1
+    h2d = n * n * 8 + nblk * n * b * 8
+    d2h = n * res_h.rank * 8 + res_h.rank * 8 + nblk * 12
+    e2e = {"value": world * algo_flops(n, n, res_h.rank, b) / (e2e_ms_max * 1e-3) / 1e12,
+           "unit": "TFLOP/s", "ms_per_step": e2e_ms_max,
+           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+           "path": "rand_lupp_adaptive(numpy pinned A.T) -> numpy W, row_idx"}
+
+    # ---------------- CPU baseline (rank 0, N = 1 only) -----------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        dt, kc, fc, cores = cpu_sample(a_host.T, b, tau, seed, args.cpu_blocks)
+        cpu = {"value": fc / dt / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": "port",
+               "sample": f"first {args.cpu_blocks} blocks (rank 0 -> {kc}) of the same adaptive "
+                         f"loop on the same matrix; oracle/randskel_oracle.py (numpy/OpenBLAS), "
+                         f"{dt:.2f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": "adaptive column-ID throughput (algorithmic TFLOP/s)",
+            "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {
+                "workload": f"cfg2: rand_lupp_adaptive(A.T, b={b}, tau={tau:g} abs) on a {n}x{n} "
+                            f"fp64 fast-decay matrix (beta=1e-16, Haar bases), seed {args.seed}",
+                "n": n, "b": b, "tau": tau, "rank": k, "status": res.status,
+                "blocks": len(res.trace) + 1, "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                "l2": "inputs (A: %.1f GB) larger than L2 between steps" % (n * n * 8 / 1e9),
+            },
+            "seconds_per_step": ms_max / 1e3,
+            "phase_ms_per_step": phase_ms,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

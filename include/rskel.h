@@ -1,0 +1,127 @@
+/*
+ * rskel.h — C ABI of the B200 randomized-skeleton (sketched LUPP ID/CUR) library
+ * `librskel.so` (package paper_2310_09417_b200).
+ *
+ * The reference (`randskel`, /root/reference/pkg/src/randskel) is a pure
+ * Python package with no FFI; its "operator API" is the Python namespace.  The
+ * entry points below are the native operations that namespace's hot path
+ * reaches through numpy/OpenBLAS/LAPACK, one C function per reference call
+ * site (cited per function).  The Python host layer
+ * (paper_2310_09417_b200/_lib.py) binds them with ctypes; see INTEGRATION.md.
+ *
+ * Conventions
+ *  - All matrices are fp64, device-resident, row-major with an explicit
+ *    leading dimension (elements), unless a `*_colmajor` flag says otherwise.
+ *  - Index vectors are int64 (numpy np.intp) device arrays.
+ *  - `stream` is a cudaStream_t passed as void*; every call is asynchronous on
+ *    it and takes no global lock.  No call allocates or frees device memory:
+ *    scratch comes from a caller-owned `workspace` of rs_workspace_bytes().
+ *  - Return value: 0 = ok, <0 = error (RS_ERR_*), see rs_status_string().
+ *    Numerical outcomes (zero pivots) are reported through device outputs
+ *    (`ncols_dev`), mirroring `_lupp_partial`'s ncols (`dense.py:284-298`).
+ */
+#ifndef RSKEL_H
+#define RSKEL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RS_ABI_VERSION 1
+#define RS_OK 0
+#define RS_ERR_ARG -1
+#define RS_ERR_CUDA -2
+#define RS_ERR_CAPACITY -3
+
+int rs_abi_version(void);
+const char* rs_status_string(int status);
+
+/* Bytes of scratch the composite calls need (panel candidates, reduction
+ * partials, the b x b inverse).  One workspace per stream. */
+size_t rs_workspace_bytes(void);
+
+/* Number of kernels this library has launched in the process (instrumentation). */
+unsigned long long rs_launch_count(void);
+
+/* C = alpha * op(A) * B + beta * Cin (row gathers optional, NULL = identity).
+ * A: M x K, row-major (A[aidx[i]*lda + k]) or, with a_colmajor, column-major
+ * (A[k*lda + i]; aidx must be NULL).  B: K x N row-major, row k at bidx[k].
+ * Cin row i at cidx[i].  Replaces the OpenBLAS dgemm calls of `gemm`
+ * (dense.py:118-141), `GaussianSketch.apply` (sketching.py:122-128) and the
+ * Schur/trailing updates (dense.py:232, skeleton.py:322). */
+int rs_dgemm(int M, int N, int K, double alpha, const double* A, long long lda, int a_colmajor,
+             const int64_t* aidx, const double* B, long long ldb, const int64_t* bidx, double beta,
+             const double* Cin, long long ldcin, const int64_t* cidx, double* C, long long ldc,
+             void* stream);
+
+/* Y (m x ell) = A (m x n) * Omega (n x ell): the sketch `a @ omega`
+ * (sketching.py:128, 272).  a_colmajor selects the `a.T` view of a C-ordered
+ * matrix (column ID / `rand_lupp_adaptive(A.T, ...)`). */
+int rs_sketch_gemm(int m, int n, int ell, const double* A, long long lda, int a_colmajor,
+                   const double* Omega, long long ldo, double* Y, long long ldy, void* stream);
+
+/* Panel LU with partial pivoting of the R x w (w <= 64) block S, in place,
+ * rows kept in physical order: `_lupp_panel` (dense.py:185-207) over one
+ * block.  perm_out[p] = physical row at position p afterwards (`sub.perm`);
+ * *ncols_dev = eliminated columns (< w iff an exactly-zero pivot column was
+ * met, dense.py:195-198).  Physical row r of S then holds, for its position
+ * p < ncols, L[p, :p] and U[p, p:], and for p >= ncols the multipliers. */
+int rs_panel_lupp(double* S, long long lds, int R, int w, int64_t* perm_out, int* ncols_dev,
+                  void* workspace, void* stream);
+
+/* Schur block of a fresh sketch block against the T-form state
+ * (`_schur_of_block`, skeleton.py:317-323):
+ *   S = Y[perm[k:]] - T * Y[perm[:k]],   *e2_dev = ||S||_F^2
+ * with T = L2 L1^{-1} ((m-k) x k, ld ldt) the interpolation block of the
+ * current rank-k state.  k = 0 gathers Y[perm].  The norm reduction is
+ * deterministic (fixed order), `frobenius_norm` (dense.py:144-146). */
+int rs_schur_block(int m, int k, int b, const double* Y, long long ldy, const int64_t* perm,
+                   const double* T, long long ldt, double* S, long long lds, double* e2_dev,
+                   void* workspace, void* stream);
+
+/* Absorb a factored Schur block (the first nc of its columns) into the
+ * T-form state (`_extend_state`, skeleton.py:326-351, expressed on
+ * T = L2 L1^{-1}):
+ *   W_hat = L_r L_1^{-1},  T_new = [T[Q_hat] - W_hat T[P_hat], W_hat]
+ *   perm_new[:k] = perm[:k],  perm_new[k:] = perm[k:][sub_perm]
+ * T_new is (m-k-nc) x (k+nc) with ld k+nc and must not alias T. */
+int rs_absorb_block(int m, int k, int nc, const double* S, long long lds, const int64_t* sub_perm,
+                    const double* T, long long ldt, double* T_new, const int64_t* perm,
+                    int64_t* perm_new, void* workspace, void* stream);
+
+/* W (m x k, row-major) with W[perm[:k]] = I and W[perm[k:]] = T
+ * (`_w_from_parts`, skeleton.py:176-182). */
+int rs_scatter_interp(const double* T, long long ldt, const int64_t* perm, int m, int k, double* W,
+                      long long ldw, void* stream);
+
+/* dst[i, :] = src[idx[i], :]  (skeleton gathers `a[row_idx]`, skeleton.py:569,640). */
+int rs_gather_rows(const double* src, long long lds, const int64_t* idx, int nrows, int ncols,
+                   double* dst, long long ldd, void* stream);
+
+/* *out = ||X||_F^2, deterministic two-stage reduction. */
+int rs_sumsq(const double* X, long long ldx, int R, int w, double* out, void* workspace,
+             void* stream);
+
+/* Inverse of an n x n (n <= 64) triangular matrix whose (i, j) element is
+ * T[ridx(i)*rs + j*cs]; out n x n row-major.  Used for L_1^{-1}. */
+int rs_trinv(const double* T, long long rs, long long cs, const int64_t* ridx, int n, int lower,
+             int unit, double* out, long long ldo, void* stream);
+
+/* perm_new[:k] = perm[:k], perm_new[k+i] = perm[k + sub[i]] (skeleton.py:345). */
+int rs_perm_update(const int64_t* perm, int64_t* perm_new, int m, int k, const int64_t* sub,
+                   void* stream);
+
+/* dst (cols x rows, row-major) = src (rows x cols, row-major)^T. */
+int rs_transpose(const double* src, long long lds, int rows, int cols, double* dst, long long ldd,
+                 void* stream);
+
+/* p[i] = i. */
+int rs_iota(int64_t* p, int n, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RSKEL_H */

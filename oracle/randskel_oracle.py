@@ -1,0 +1,324 @@
+"""CPU oracle for the sketched-LUPP ID / CUR hot path.  TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
+arm may import this module, and only as the checker (or the timed CPU
+baseline).  The product path (paper_2310_09417_b200) never imports it.
+
+This is a numpy/scipy restatement of the reference algorithm
+(`/root/reference/pkg/src/randskel`, cited per function as file:line).  It is
+*pinned* against the reference itself: tests/golden/make_golden.py imports
+the reference from /root/reference (in the build container) and freezes its
+outputs as fixtures; tests/test_oracle_golden.py checks this module against
+them bit-for-bit on indices and to 1e-13 on values.
+
+Algorithmic choices that matter for parity, restated:
+  * LUPP pivot = first index of max |v| among the *current* positions of the
+    active rows; full-row swaps; an exactly-zero pivot column stops the
+    factorization (`dense.py:185-207`).  Panel width 64, blocked right-looking
+    update with a unit-lower triangular solve + GEMM (`dense.py:210-233`).
+  * Omega: numpy Philox4x64 keyed [seed, stream], C-order standard normals,
+    ``/= sqrt(ell)`` for 'inv_sqrt_ell' (`sketching.py:55-72,191-204`).
+  * Adaptive loop: block t uses child(t); estimate = ||S||_F of the Schur
+    block; stop at e <= tau, or when rank + b > max_rank, or truncate on a
+    zero pivot (`skeleton.py:391-460`).
+"""
+
+import numpy as np
+import scipy.linalg
+
+PANEL = 64            # dense.py:46
+PINV_RCOND = 1e-12    # dense.py:49
+COND_LIMIT = 1e14     # skeleton.py:72
+_M64 = (1 << 64) - 1
+
+
+class OracleRankDeficient(Exception):
+    def __init__(self, step):
+        super().__init__(step)
+        self.step = step
+
+
+# ---------------------------------------------------------------- streams --
+def splitmix64(z):
+    """`sketching.py:47-52`"""
+    z = (z + 0x9E3779B97F4A7C15) & _M64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+    return z ^ (z >> 31)
+
+
+def child_stream(stream, i):
+    """`sketching.py:71-72`: child(i) of stream id ``stream``."""
+    return splitmix64((stream & _M64) ^ splitmix64(i & _M64))
+
+
+def gaussian(seed, stream, n, ell, unit=False):
+    """`sketching.py:191-204` with the key of `sketching.py:67-69`."""
+    gen = np.random.Generator(np.random.Philox(key=[seed & _M64, stream & _M64]))
+    om = gen.standard_normal((n, ell))
+    if not unit:
+        om /= np.sqrt(ell)
+    return om
+
+
+# ------------------------------------------------------------------- LUPP --
+def lupp_inplace(A, allow_partial):
+    """Blocked right-looking LUPP of the F-ordered workspace A (m x n), in
+    place.  Returns (perm, ncols).  `dense.py:185-233`."""
+    m, n = A.shape
+    perm = np.arange(m, dtype=np.intp)
+    for c0 in range(0, n, PANEL):
+        c1 = min(n, c0 + PANEL)
+        for j in range(c0, c1):
+            p = j + int(np.argmax(np.abs(A[j:, j])))
+            if A[p, j] == 0.0:
+                if allow_partial:
+                    return perm, j
+                raise OracleRankDeficient(j)
+            if p != j:
+                A[[j, p], :] = A[[p, j], :]
+                perm[[j, p]] = perm[[p, j]]
+            if j + 1 < m:
+                A[j + 1:, j] /= A[j, j]
+                if j + 1 < c1:
+                    A[j + 1:, j + 1:c1] -= np.outer(A[j + 1:, j], A[j, j + 1:c1])
+        if c1 < n:
+            A[c0:c1, c1:] = scipy.linalg.solve_triangular(
+                A[c0:c1, c0:c1], A[c0:c1, c1:], lower=True, unit_diagonal=True)
+            A[c1:, c1:] -= A[c1:, c0:c1] @ A[c0:c1, c1:]
+    return perm, n
+
+
+def lupp(a, allow_partial=False):
+    """(L, U, perm, ncols) with a[perm] = L U.  `dense.py:247-298`."""
+    a = np.asarray(a, dtype=np.float64)
+    m, n = a.shape
+    if m < n:
+        raise ValueError("lupp requires rows >= cols")
+    if not np.isfinite(a).all():
+        raise ValueError("non-finite entries")
+    A = np.array(a, order="F", copy=True)
+    perm, nc = lupp_inplace(A, allow_partial)
+    L = np.tril(A[:, :nc], -1)
+    L[np.arange(nc), np.arange(nc)] = 1.0
+    U = np.triu(A[:nc, :nc])
+    return L, U, perm, nc
+
+
+def interp_from_lu(L, perm):
+    """W with W[perm[:k]] = I, W[perm[k:]] = L2 L1^{-1}.  `skeleton.py:176-189`,
+    right-side solve as `dense.py:553-560`."""
+    k = L.shape[1]
+    t = scipy.linalg.solve_triangular(L[:k], L[k:].T, lower=True, trans=1,
+                                      unit_diagonal=True).T
+    return scatter_interp(perm, k, t)
+
+
+def scatter_interp(perm, k, t):
+    w = np.zeros((perm.shape[0], k))
+    w[perm[:k], np.arange(k)] = 1.0
+    w[perm[k:]] = t
+    return w
+
+
+# ------------------------------------------------------- fixed-rank IDs --
+def rand_lupp(a, k, seed, stream=0, unit=False):
+    """`skeleton.py:207-234`: returns (row_idx, w)."""
+    a = np.asarray(a, dtype=np.float64)
+    om = gaussian(seed, stream, a.shape[1], k, unit)
+    L, _, perm, _ = lupp(a @ om)
+    return perm[:k].copy(), interp_from_lu(L, perm)
+
+
+def column_id(a, k, seed, stream=0, unit=False):
+    """`skeleton.py:574-589`: returns (col_idx, x)."""
+    a = np.asarray(a, dtype=np.float64)
+    gam = gaussian(seed, stream, a.shape[0], k, unit)
+    L, _, perm, _ = lupp(a.T @ gam)
+    return perm[:k].copy(), interp_from_lu(L, perm).T
+
+
+# ----------------------------------------------------------- adaptive ID --
+class LUState:
+    """ysofar[perm] = [L1; L2] U1 (`skeleton.py:152-173`)."""
+
+    def __init__(self, L1, L2, U1, perm, ysofar):
+        self.L1, self.L2, self.U1, self.perm, self.ysofar = L1, L2, U1, perm, ysofar
+
+    @property
+    def rank(self):
+        return self.U1.shape[0]
+
+
+def block(a, seed, stream, t, b):
+    """Sketch block t: a @ Omega_t, Omega_t ~ N(0, 1/b) from child(t)
+    (`skeleton.py:286-295`)."""
+    return a @ gaussian(seed, child_stream(stream, t), a.shape[1], b)
+
+
+def schur(state, y):
+    """`skeleton.py:317-323`: (u2, S)."""
+    k = state.rank
+    py = y[state.perm]
+    u2 = scipy.linalg.solve_triangular(state.L1, py[:k], lower=True, unit_diagonal=True)
+    return u2, py[k:] - state.L2 @ u2
+
+
+def extend(state, y, u2, L, U, sperm, nc):
+    """`skeleton.py:326-351`."""
+    if nc == 0:
+        return state
+    k = state.rank
+    l2p = state.L2[sperm]
+    L1 = np.block([[state.L1, np.zeros((k, nc))], [l2p[:nc], L[:nc]]])
+    L2 = np.hstack([l2p[nc:], L[nc:]])
+    U1 = np.block([[state.U1, u2[:, :nc]], [np.zeros((nc, k)), U]])
+    perm = state.perm.copy()
+    perm[k:] = perm[k:][sperm]
+    return LUState(L1, L2, U1, perm, np.hstack([state.ysofar, y[:, :nc]]))
+
+
+def adaptive_init(a, b, seed, stream=0):
+    """`skeleton.py:298-314`."""
+    y = block(a, seed, stream, 0, b)
+    L, U, perm, _ = lupp(y)
+    return LUState(L[:b].copy(), L[b:].copy(), U, perm, y)
+
+
+def rand_lupp_adaptive(a, b, tau, seed, stream=0, max_rank=None, want_w=True, max_blocks=None):
+    """`skeleton.py:391-460`: returns dict(rank, row_idx, w, trace, status).
+
+    ``max_blocks`` (not in the reference) stops after that many sketch blocks
+    -- the bounded CPU-baseline sample of bench.py."""
+    a = np.asarray(a, dtype=np.float64)
+    m, n = a.shape
+    if max_rank is None:
+        max_rank = max(b, min(m, n) - b)
+    max_rank = min(max_rank, min(m, n))
+    state = adaptive_init(a, b, seed, stream)
+    trace, status, t = [], "not_converged", 1
+    while max_blocks is None or t < max_blocks:
+        y = block(a, seed, stream, t, b)
+        u2, s = schur(state, y)
+        e = float(np.linalg.norm(s))
+        trace.append((state.rank, e))
+        if e <= tau:
+            status = "ok"
+            break
+        if state.rank + b > max_rank:
+            break
+        L, U, sperm, nc = lupp(s, allow_partial=True)
+        state = extend(state, y, u2, L, U, sperm, nc)
+        t += 1
+        if nc < b:
+            status = "rank_exhausted"
+            break
+    k = state.rank
+    out = dict(rank=k, row_idx=state.perm[:k].copy(), trace=trace, status=status, state=state)
+    if want_w:
+        tb = scipy.linalg.solve_triangular(state.L1, state.L2.T, lower=True, trans=1,
+                                           unit_diagonal=True).T
+        out["w"] = scatter_interp(state.perm, k, tb)
+    return out
+
+
+# ------------------------------------------------------ two-sided / CUR --
+def columns_from_rows(a, row_idx, k):
+    """`skeleton.py:565-571`."""
+    L, _, perm, _ = lupp(a[row_idx].T)
+    return perm[:k].copy(), interp_from_lu(L, perm).T
+
+
+def cond1(s):
+    """1-norm condition estimate via getrf + gecon (`skeleton.py:592-603`)."""
+    anorm = float(np.abs(s).sum(axis=0).max())
+    if anorm == 0.0:
+        return np.inf
+    lu, _, info = scipy.linalg.lapack.dgetrf(s)
+    if info > 0:
+        return np.inf
+    rc, _ = scipy.linalg.lapack.dgecon(lu, anorm, norm="1")
+    return np.inf if rc == 0.0 else 1.0 / rc
+
+
+def pinv_apply(a, b):
+    """gelsd least squares, rcond 1e-12 (`dense.py:166-182`)."""
+    b = np.asarray(b, dtype=np.float64)
+    if b.ndim == 1:
+        b = b[:, None]
+    return scipy.linalg.lstsq(a, b, cond=PINV_RCOND, lapack_driver="gelsd")[0]
+
+
+def two_sided_id(a, k, seed, stream=0):
+    """`skeleton.py:606-625`."""
+    a = np.asarray(a, dtype=np.float64)
+    row_idx, w = rand_lupp(a, k, seed, stream)
+    col_idx, x = columns_from_rows(a, row_idx, k)
+    status = "ill_conditioned" if cond1(a[np.ix_(row_idx, col_idx)]) > COND_LIMIT else "ok"
+    return dict(row_idx=row_idx, col_idx=col_idx, w=w, x=x, status=status)
+
+
+def cur_from_rows(a, row_idx, k):
+    """CUR assembly given row skeletons (`skeleton.py:637-647`)."""
+    col_idx, _ = columns_from_rows(a, row_idx, k)
+    c = a[:, col_idx]
+    ar = pinv_apply(a[row_idx].T, a.T).T
+    u_mid = pinv_apply(c, ar)
+    status = "ill_conditioned" if cond1(a[np.ix_(row_idx, col_idx)]) > COND_LIMIT else "ok"
+    return dict(row_idx=row_idx, col_idx=col_idx, u_mid=u_mid, status=status)
+
+
+def cur_decompose(a, k, seed, stream=0):
+    """`skeleton.py:628-647`."""
+    a = np.asarray(a, dtype=np.float64)
+    row_idx, _ = rand_lupp(a, k, seed, stream)
+    return cur_from_rows(a, row_idx, k)
+
+
+# --------------------------------------------------- evaluators / inputs --
+def row_id_error(a, row_idx, w):
+    """`skeleton.py:542-547`."""
+    return float(np.linalg.norm(a - w @ a[row_idx]))
+
+
+def stable_row_id_error(a, row_idx):
+    """`skeleton.py:550-562`."""
+    q, _ = np.linalg.qr(a[row_idx].T)
+    at = a.T
+    return float(np.linalg.norm(at - q @ (q.T @ at)))
+
+
+def gen_fast_decay(m, n, beta, seed, stream=0):
+    """Haar bases, singular values beta^((i-1)/(n-1)) (`zoo.py:36-75`)."""
+    gen = np.random.Generator(np.random.Philox(key=[seed & _M64, stream & _M64]))
+
+    def haar(r, c):
+        q, rr = np.linalg.qr(gen.standard_normal((r, c)))
+        s = np.sign(np.diagonal(rr))
+        s[s == 0] = 1.0
+        return q * s
+
+    u = haar(m, n)
+    v = haar(n, n)
+    d = np.ones(1) if n == 1 else beta ** (np.arange(n) / (n - 1))
+    return (u * d) @ v.T, d
+
+
+def gen_kahan(n, zeta=0.99):
+    """`zoo.py:78-88`."""
+    phi = np.sqrt(1.0 - zeta * zeta)
+    k = np.eye(n) - phi * np.triu(np.ones((n, n)), 1)
+    return zeta ** np.arange(n)[:, None] * k
+
+
+def gen_chan(n):
+    """`zoo.py:91-104`."""
+    a = np.eye(n) - np.tril(np.ones((n, n)), -1)
+    a[:, -1] = 1.0
+    return a
+
+
+def exact_rank(m, n, r, seed):
+    """`test_skeleton.py:12-14`."""
+    g = np.random.default_rng(seed)
+    return g.standard_normal((m, r)) @ g.standard_normal((r, n))

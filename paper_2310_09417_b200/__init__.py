@@ -1,0 +1,39 @@
+"""B200-native randomized skeletonization (sketched LUPP ID / CUR).
+
+Drop-in for the hot path of the reference package `randskel`
+(`/root/reference/pkg/src/randskel/__init__.py:9-86`): same public names,
+signatures, result types, statuses and exceptions for the interpolative and
+CUR entry points, with the arithmetic in hand-written sm_100a kernels
+(librskel.so, C ABI in include/rskel.h).  There is no CPU fallback: without a
+CUDA device or the built library the entry points raise DeviceError.
+"""
+
+from .errors import (
+    DeviceError,
+    DimensionError,
+    NumericalError,
+    RankDeficientError,
+    SingularError,
+)
+from .sketching import (
+    GaussianSketch,
+    RngStream,
+    SketchSpec,
+    apply_sketch,
+    make_gaussian,
+    make_sketch,
+)
+from .skeleton import (
+    STATUS_ILL_CONDITIONED,
+    STATUS_NOT_CONVERGED,
+    STATUS_OK,
+    STATUS_RANK_EXHAUSTED,
+    ErrorTrace,
+    SkeletonResult,
+    TraceRecord,
+    column_id,
+    rand_lupp,
+    rand_lupp_adaptive,
+)
+
+__version__ = "0.1.0"

@@ -1,0 +1,184 @@
+"""Device plumbing: matrix descriptors, host<->device transfer, streams and
+workspaces.  PyTorch is used only to own device/pinned memory and streams;
+all arithmetic on the skeleton path goes through librskel.so.
+
+Ownership mirrors the reference (`dense.py:52-62`): inputs are converted to
+float64 and never mutated; outputs are fresh arrays.  Results come back in
+the caller's container: numpy in -> numpy out, torch CPU -> torch CPU, torch
+CUDA -> torch CUDA (device-resident, no D2H).
+"""
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import DeviceError, DimensionError
+
+_workspaces = {}
+
+
+def device():
+    if not torch.cuda.is_available():
+        raise DeviceError("no CUDA device visible: the skeleton path runs on B200 only (no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_handle():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def workspace():
+    dev = device()
+    ws = _workspaces.get(dev.index)
+    if ws is None:
+        ws = torch.empty(_lib.load().rs_workspace_bytes(), dtype=torch.uint8, device=dev)
+        _workspaces[dev.index] = ws
+    return ws
+
+
+class Matrix:
+    """fp64 device matrix view.  Element (i, j) lives at ``base[i*ld + j]``
+    (row-major) or ``base[j*ld + i]`` (column-major).  ``kind`` records the
+    caller's container so results can be returned the same way."""
+
+    __slots__ = ("t", "rows", "cols", "ld", "colmajor", "kind")
+
+    def __init__(self, t, rows, cols, ld, colmajor, kind):
+        self.t, self.rows, self.cols, self.ld, self.colmajor, self.kind = t, rows, cols, ld, colmajor, kind
+
+    @property
+    def ptr(self):
+        return self.t.data_ptr()
+
+    @property
+    def shape(self):
+        return (self.rows, self.cols)
+
+    @property
+    def T(self):
+        return Matrix(self.t, self.cols, self.rows, self.ld, not self.colmajor, self.kind)
+
+    def row_major(self):
+        """A row-major view of the same matrix (device transpose copy if needed)."""
+        if not self.colmajor:
+            return self
+        out = torch.empty((self.rows, self.cols), dtype=torch.float64, device=self.t.device)
+        if self.rows and self.cols:
+            _lib.call("rs_transpose", self.ptr, self.ld, self.cols, self.rows, out.data_ptr(),
+                      self.cols, stream_handle())
+        return Matrix(out, self.rows, self.cols, self.cols, False, self.kind)
+
+
+def _from_tensor_2d(t, kind):
+    rows, cols = t.shape
+    s0, s1 = t.stride()
+    if rows == 0 or cols == 0:
+        t = t.contiguous()
+        return Matrix(t, rows, cols, max(cols, 1), False, kind)
+    if s1 == 1 and (rows == 1 or s0 >= cols):
+        return Matrix(t, rows, cols, s0 if rows > 1 else cols, False, kind)
+    if s0 == 1 and (cols == 1 or s1 >= rows):
+        return Matrix(t, rows, cols, s1 if cols > 1 else rows, True, kind)
+    t = t.contiguous()
+    return Matrix(t, rows, cols, cols, False, kind)
+
+
+def as_matrix(a, name="matrix"):
+    """Convert ``a`` (numpy / array_like / torch / Matrix) to an fp64 device Matrix."""
+    if isinstance(a, Matrix):
+        return a
+    dev = device()
+    if isinstance(a, torch.Tensor):
+        if a.dim() != 2:
+            raise DimensionError(f"{name} must be 2-dimensional, got shape {tuple(a.shape)}")
+        kind = "torch_cuda" if a.is_cuda else "torch_cpu"
+        if a.dtype != torch.float64:
+            a = a.to(torch.float64)
+        if not a.is_cuda:
+            a = a.contiguous() if not (a.is_contiguous() or a.t().is_contiguous()) else a
+            a = a.to(dev)
+        return _from_tensor_2d(a, kind)
+    arr = np.asarray(a, dtype=np.float64)
+    if arr.ndim != 2:
+        raise DimensionError(f"{name} must be 2-dimensional, got shape {arr.shape}")
+    if arr.flags.c_contiguous:
+        t = torch.as_tensor(arr).to(dev)
+        return Matrix(t, arr.shape[0], arr.shape[1], max(arr.shape[1], 1), False, "numpy")
+    if arr.flags.f_contiguous:
+        t = torch.as_tensor(arr.T).to(dev)
+        return Matrix(t, arr.shape[0], arr.shape[1], max(arr.shape[0], 1), True, "numpy")
+    arr = np.ascontiguousarray(arr)
+    t = torch.as_tensor(arr).to(dev)
+    return Matrix(t, arr.shape[0], arr.shape[1], max(arr.shape[1], 1), False, "numpy")
+
+
+def as_index(idx, kind):
+    """Index vector -> int64 device tensor."""
+    if isinstance(idx, torch.Tensor):
+        return idx.to(device=device(), dtype=torch.int64)
+    return torch.as_tensor(np.asarray(idx, dtype=np.int64)).to(device())
+
+
+def host_empty(shape, dtype=torch.float64):
+    """Pinned host buffer (fast DMA) as a torch tensor."""
+    return torch.empty(shape, dtype=dtype, pin_memory=True)
+
+
+def to_output(x, like):
+    """Return device tensor ``x`` in the container kind of ``like``."""
+    kind = like.kind if isinstance(like, Matrix) else like
+    if isinstance(x, Matrix):
+        x = x.t if not x.colmajor else x.t.t()
+    if kind == "torch_cuda":
+        return x
+    if x.numel() >= (1 << 20):
+        h = host_empty(tuple(x.shape), x.dtype)
+        h.copy_(x, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+    else:
+        h = x.cpu()
+    if kind == "torch_cpu":
+        return h
+    return h.numpy()
+
+
+def to_host_index(x, kind):
+    if kind == "torch_cuda":
+        return x
+    h = x.cpu()
+    return h if kind == "torch_cpu" else h.numpy().astype(np.intp, copy=False)
+
+
+def dgemm(a, b, alpha=1.0, beta=0.0, cin=None, out=None, aidx=None, bidx=None, cidx=None):
+    """C = alpha * a @ b + beta * cin on the DMMA kernel.  a: Matrix (any
+    layout), b: row-major Matrix; returns a row-major (M x N) torch tensor."""
+    M, K = a.shape
+    if aidx is not None:
+        M = aidx.numel()
+    N = b.cols
+    if b.colmajor:
+        b = b.row_major()
+    if out is None:
+        out = torch.empty((M, N), dtype=torch.float64, device=device())
+    if cin is not None and cin.colmajor:
+        cin = cin.row_major()
+    _lib.call(
+        "rs_dgemm", M, N, K, float(alpha), a.ptr, a.ld, int(a.colmajor),
+        aidx.data_ptr() if aidx is not None else None,
+        b.ptr, b.ld, bidx.data_ptr() if bidx is not None else None,
+        float(beta), cin.ptr if cin is not None else None, cin.ld if cin is not None else 0,
+        cidx.data_ptr() if cidx is not None else None,
+        out.data_ptr(), out.stride(0) if out.dim() == 2 else N, stream_handle(),
+    )
+    return out
+
+
+def sketch(a, omega):
+    """Y = a @ omega with omega a host (n x ell) float64 array (host-RNG draw)."""
+    m, n = a.shape
+    ell = omega.shape[1]
+    om = torch.as_tensor(np.ascontiguousarray(omega, dtype=np.float64)).to(device())
+    y = torch.empty((m, ell), dtype=torch.float64, device=device())
+    _lib.call("rs_sketch_gemm", m, n, ell, a.ptr, a.ld, int(a.colmajor), om.data_ptr(),
+              max(ell, 1), y.data_ptr(), max(ell, 1), stream_handle())
+    return y

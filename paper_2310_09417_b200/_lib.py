@@ -1,0 +1,81 @@
+"""ctypes binding of librskel.so (the C ABI declared in include/rskel.h).
+
+This is the only place Python touches the native library.  Device buffers are
+passed as raw pointers (``tensor.data_ptr()``) and streams as
+``cudaStream_t`` handles; there are no torch types in the ABI.  A missing or
+broken library raises :class:`DeviceError` -- there is no CPU fallback.
+"""
+
+import ctypes
+import os
+
+from .errors import DeviceError
+
+_PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG_DIR, "librskel.so")
+
+_c_int = ctypes.c_int
+_c_ll = ctypes.c_longlong
+_c_double = ctypes.c_double
+_p = ctypes.c_void_p
+
+# name -> (restype, argtypes); must match include/rskel.h
+SIGNATURES = {
+    "rs_abi_version": (_c_int, []),
+    "rs_status_string": (ctypes.c_char_p, [_c_int]),
+    "rs_workspace_bytes": (ctypes.c_size_t, []),
+    "rs_launch_count": (ctypes.c_ulonglong, []),
+    "rs_dgemm": (_c_int, [_c_int, _c_int, _c_int, _c_double, _p, _c_ll, _c_int, _p, _p, _c_ll, _p,
+                          _c_double, _p, _c_ll, _p, _p, _c_ll, _p]),
+    "rs_sketch_gemm": (_c_int, [_c_int, _c_int, _c_int, _p, _c_ll, _c_int, _p, _c_ll, _p, _c_ll, _p]),
+    "rs_panel_lupp": (_c_int, [_p, _c_ll, _c_int, _c_int, _p, _p, _p, _p]),
+    "rs_schur_block": (_c_int, [_c_int, _c_int, _c_int, _p, _c_ll, _p, _p, _c_ll, _p, _c_ll, _p, _p, _p]),
+    "rs_absorb_block": (_c_int, [_c_int, _c_int, _c_int, _p, _c_ll, _p, _p, _c_ll, _p, _p, _p, _p, _p]),
+    "rs_scatter_interp": (_c_int, [_p, _c_ll, _p, _c_int, _c_int, _p, _c_ll, _p]),
+    "rs_gather_rows": (_c_int, [_p, _c_ll, _p, _c_int, _c_int, _p, _c_ll, _p]),
+    "rs_sumsq": (_c_int, [_p, _c_ll, _c_int, _c_int, _p, _p, _p]),
+    "rs_trinv": (_c_int, [_p, _c_ll, _c_ll, _p, _c_int, _c_int, _c_int, _p, _c_ll, _p]),
+    "rs_perm_update": (_c_int, [_p, _p, _c_int, _c_int, _p, _p]),
+    "rs_transpose": (_c_int, [_p, _c_ll, _c_int, _c_int, _p, _c_ll, _p]),
+    "rs_iota": (_c_int, [_p, _c_int, _p]),
+}
+
+ABI_VERSION = 1
+
+_lib = None
+
+
+def load(path=LIB_PATH):
+    """Load (once) and type the shared library; raise DeviceError if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise DeviceError(
+            f"{path} is missing: build it with `python -m paper_2310_09417_b200._build` "
+            "(nvcc, sm_100a); the skeleton path has no CPU fallback"
+        )
+    try:
+        lib = ctypes.CDLL(path)
+    except OSError as exc:  # pragma: no cover - environment specific
+        raise DeviceError(f"cannot load {path}: {exc}") from exc
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.rs_abi_version() != ABI_VERSION:
+        raise DeviceError("librskel.so ABI version mismatch; rebuild it")
+    _lib = lib
+    return lib
+
+
+def check(status, what):
+    if status != 0:
+        msg = load().rs_status_string(status).decode()
+        raise DeviceError(f"{what} failed: {msg} (status {status})")
+
+
+def call(name, *args):
+    """Invoke ``name`` and raise DeviceError on a non-zero status."""
+    status = getattr(load(), name)(*args)
+    check(status, name)

@@ -1,0 +1,237 @@
+// Bandwidth-bound helper kernels of the skeleton path: row gathers, the
+// deterministic Frobenius reduction, the small triangular inverse used for
+// W_hat = L_r L_1^{-1}, the permutation update and the interpolation-matrix
+// scatter (`skeleton.py:176-182`).
+#include "common.cuh"
+#include "rskel_internal.h"
+
+
+namespace rs {
+
+// dst[i, c] = src[idx[i], c] (idx == nullptr: identity), row-major.
+__global__ void gather_rows_kernel(const double* __restrict__ src, long long lds,
+                                   const int64_t* __restrict__ idx, int nrows, int ncols,
+                                   double* __restrict__ dst, long long ldd) {
+  for (int i = blockIdx.x; i < nrows; i += gridDim.x) {
+    long long r = idx ? idx[i] : i;
+    const double* s = src + r * lds;
+    double* d = dst + (long long)i * ldd;
+    for (int c = threadIdx.x; c < ncols; c += blockDim.x) d[c] = s[c];
+  }
+}
+
+int launch_gather_rows(const double* src, long long lds, const int64_t* idx, int nrows, int ncols,
+                       double* dst, long long ldd, cudaStream_t st) {
+  if (nrows < 0 || ncols < 0) return RS_ERR_ARG;
+  if (nrows == 0 || ncols == 0) return RS_OK;
+  int threads = ncols >= 256 ? 256 : ((ncols + 31) / 32) * 32;
+  int grid = nrows < 148 * 16 ? nrows : 148 * 16;
+  gather_rows_kernel<<<grid, threads, 0, st>>>(src, lds, idx, nrows, ncols, dst, ldd);
+  count_launch(1);
+  return cudaGetLastError() == cudaSuccess ? RS_OK : RS_ERR_CUDA;
+}
+
+// ---- deterministic sum of squares ---------------------------------------
+// Stage 1: CTA b reduces rows [b*rows_per, ...) in a fixed order; stage 2 adds
+// the partials in CTA order.  The result is independent of scheduling.
+constexpr int SS_THREADS = 256;
+constexpr int SS_MAX_CTAS = 1024;
+
+__global__ void sumsq_stage1(const double* __restrict__ X, long long ldx, int R, int w, int rows_per,
+                             double* __restrict__ partial) {
+  __shared__ double red[SS_THREADS];
+  int r0 = blockIdx.x * rows_per, r1 = min(R, r0 + rows_per);
+  double acc = 0.0;
+  long long n = (long long)(r1 > r0 ? r1 - r0 : 0) * w;
+  for (long long e = threadIdx.x; e < n; e += SS_THREADS) {
+    int i = (int)(e / w), c = (int)(e - (long long)i * w);
+    double v = X[(long long)(r0 + i) * ldx + c];
+    acc = fma(v, v, acc);
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = SS_THREADS / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}
+
+__global__ void sumsq_stage2(const double* __restrict__ partial, int n, double* __restrict__ out) {
+  __shared__ double red[SS_THREADS];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += SS_THREADS) acc += partial[i];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = SS_THREADS / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = red[0];
+}
+
+size_t sumsq_workspace_bytes() { return SS_MAX_CTAS * sizeof(double); }
+
+int launch_sumsq(const double* X, long long ldx, int R, int w, double* partial_ws, double* out,
+                 cudaStream_t st) {
+  if (R < 0 || w < 0) return RS_ERR_ARG;
+  if (R == 0 || w == 0) {
+    cudaMemsetAsync(out, 0, sizeof(double), st);
+    return cudaGetLastError() == cudaSuccess ? RS_OK : RS_ERR_CUDA;
+  }
+  int ctas = (R + 63) / 64;
+  if (ctas > 296) ctas = 296;
+  int rows_per = (R + ctas - 1) / ctas;
+  ctas = (R + rows_per - 1) / rows_per;
+  sumsq_stage1<<<ctas, SS_THREADS, 0, st>>>(X, ldx, R, w, rows_per, partial_ws);
+  count_launch(1);
+  sumsq_stage2<<<1, SS_THREADS, 0, st>>>(partial_ws, ctas, out);
+  count_launch(1);
+  return cudaGetLastError() == cudaSuccess ? RS_OK : RS_ERR_CUDA;
+}
+
+// ---- small triangular inverse (n <= 64) ---------------------------------
+// Element (i, j) of the input triangle is T[ridx(i) * rs + j * cs].  Thread c
+// computes column c of the inverse by substitution; out is n x n row-major.
+constexpr int TI_MAX = 64;
+__global__ void trinv_kernel(const double* __restrict__ T, long long rs_, long long cs_,
+                             const int64_t* __restrict__ ridx, int n, int lower, int unit,
+                             double* __restrict__ out, long long ldo) {
+  extern __shared__ double ti_smem[];
+  double (*L)[TI_MAX + 1] = reinterpret_cast<double (*)[TI_MAX + 1]>(ti_smem);
+  double (*X)[TI_MAX + 1] = reinterpret_cast<double (*)[TI_MAX + 1]>(ti_smem + TI_MAX * (TI_MAX + 1));
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    int i = e / n, j = e - i * n;
+    long long r = ridx ? ridx[i] : i;
+    L[i][j] = T[r * rs_ + (long long)j * cs_];
+  }
+  __syncthreads();
+  int c = threadIdx.x;
+  if (c < n) {
+    if (lower) {
+      for (int i = 0; i < n; ++i) {
+        double s = (i == c) ? 1.0 : 0.0;
+        if (i > c) {
+          for (int q = c; q < i; ++q) s -= L[i][q] * X[q][c];
+        }
+        X[i][c] = (i < c) ? 0.0 : (unit ? s : s / L[i][i]);
+      }
+    } else {
+      for (int i = n - 1; i >= 0; --i) {
+        double s = (i == c) ? 1.0 : 0.0;
+        if (i < c) {
+          for (int q = i + 1; q <= c; ++q) s -= L[i][q] * X[q][c];
+        }
+        X[i][c] = (i > c) ? 0.0 : (unit ? s : s / L[i][i]);
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    int i = e / n, j = e - i * n;
+    out[(long long)i * ldo + j] = X[i][j];
+  }
+}
+
+int launch_trinv(const double* T, long long rs_, long long cs_, const int64_t* ridx, int n, int lower,
+                 int unit, double* out, long long ldo, cudaStream_t st) {
+  if (n < 0 || n > TI_MAX) return RS_ERR_ARG;
+  if (n == 0) return RS_OK;
+  constexpr int smem = 2 * TI_MAX * (TI_MAX + 1) * sizeof(double);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(trinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    configured = true;
+  }
+  trinv_kernel<<<1, TI_MAX, smem, st>>>(T, rs_, cs_, ridx, n, lower, unit, out, ldo);
+  count_launch(1);
+  return cudaGetLastError() == cudaSuccess ? RS_OK : RS_ERR_CUDA;
+}
+
+// ---- permutation update: perm'[:k] = perm[:k]; perm'[k+i] = perm[k + sub[i]] ----
+__global__ void perm_update_kernel(const int64_t* __restrict__ perm, int64_t* __restrict__ perm_new,
+                                   int m, int k, const int64_t* __restrict__ sub) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  perm_new[i] = (i < k) ? perm[i] : perm[k + sub[i - k]];
+}
+
+int launch_perm_update(const int64_t* perm, int64_t* perm_new, int m, int k, const int64_t* sub,
+                       cudaStream_t st) {
+  if (m < 0 || k < 0 || k > m) return RS_ERR_ARG;
+  if (m == 0) return RS_OK;
+  perm_update_kernel<<<(m + 255) / 256, 256, 0, st>>>(perm, perm_new, m, k, sub);
+  count_launch(1);
+  return cudaGetLastError() == cudaSuccess ? RS_OK : RS_ERR_CUDA;
+}
+
+__global__ void iota_kernel(int64_t* p, int n) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = i;
+}
+
+int launch_iota(int64_t* p, int n, cudaStream_t st) {
+  if (n <= 0) return n == 0 ? RS_OK : RS_ERR_ARG;
+  iota_kernel<<<(n + 255) / 256, 256, 0, st>>>(p, n);
+  count_launch(1);
+  return cudaGetLastError() == cudaSuccess ? RS_OK : RS_ERR_CUDA;
+}
+
+// ---- W[perm[p]] = e_p (p < k), W[perm[p]] = T[p - k] (p >= k) ---------------
+// One CTA row-sweep per position; writes every W element exactly once.
+__global__ void scatter_interp_kernel(const double* __restrict__ T, long long ldt,
+                                      const int64_t* __restrict__ perm, int m, int k,
+                                      double* __restrict__ W, long long ldw) {
+  for (int p = blockIdx.x; p < m; p += gridDim.x) {
+    double* wr = W + perm[p] * ldw;
+    if (p < k) {
+      for (int c = threadIdx.x; c < k; c += blockDim.x) wr[c] = (c == p) ? 1.0 : 0.0;
+    } else {
+      const double* tr = T + (long long)(p - k) * ldt;
+      for (int c = threadIdx.x; c < k; c += blockDim.x) wr[c] = tr[c];
+    }
+  }
+}
+
+int launch_scatter_interp(const double* T, long long ldt, const int64_t* perm, int m, int k, double* W,
+                          long long ldw, cudaStream_t st) {
+  if (m < 0 || k < 0 || k > m) return RS_ERR_ARG;
+  if (m == 0 || k == 0) return RS_OK;
+  int threads = k >= 256 ? 256 : ((k + 31) / 32) * 32;
+  int grid = m < 148 * 32 ? m : 148 * 32;
+  scatter_interp_kernel<<<grid, threads, 0, st>>>(T, ldt, perm, m, k, W, ldw);
+  count_launch(1);
+  return cudaGetLastError() == cudaSuccess ? RS_OK : RS_ERR_CUDA;
+}
+
+}  // namespace rs
+
+namespace rs {
+
+// ---- dst (cols x rows) = src (rows x cols)^T, 32x32 smem tiles ------------
+__global__ void transpose_kernel(const double* __restrict__ src, long long lds, int rows, int cols,
+                                 double* __restrict__ dst, long long ldd) {
+  __shared__ double tile[32][33];
+  int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int y = threadIdx.y; y < 32; y += 8) {
+    int i = by + y, j = bx + threadIdx.x;
+    if (i < rows && j < cols) tile[y][threadIdx.x] = src[(long long)i * lds + j];
+  }
+  __syncthreads();
+  for (int y = threadIdx.y; y < 32; y += 8) {
+    int j = bx + y, i = by + threadIdx.x;
+    if (i < rows && j < cols) dst[(long long)j * ldd + i] = tile[threadIdx.x][y];
+  }
+}
+
+int launch_transpose(const double* src, long long lds, int rows, int cols, double* dst, long long ldd,
+                     cudaStream_t st) {
+  if (rows < 0 || cols < 0) return RS_ERR_ARG;
+  if (rows == 0 || cols == 0) return RS_OK;
+  dim3 grid((cols + 31) / 32, (rows + 31) / 32);
+  transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(src, lds, rows, cols, dst, ldd);
+  count_launch(1);
+  return cudaGetLastError() == cudaSuccess ? RS_OK : RS_ERR_CUDA;
+}
+
+}  // namespace rs

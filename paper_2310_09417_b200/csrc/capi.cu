@@ -1,0 +1,154 @@
+// extern "C" boundary of librskel.so (declared in include/rskel.h).
+// Composite calls (Schur block, absorb block) are sequences of the kernels in
+// gemm_f64.cu / panel.cu / aux.cu enqueued on the caller's stream.
+#include <atomic>
+
+#include "common.cuh"
+#include "rskel_internal.h"
+
+namespace rs {
+static std::atomic<unsigned long long> g_launch_count{0};
+void count_launch(int n) { g_launch_count.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
+}  // namespace rs
+
+namespace {
+
+constexpr int kMaxB = 64;
+
+struct WorkspaceLayout {
+  size_t panel_off, sumsq_off, linv_off, total;
+};
+
+WorkspaceLayout layout() {
+  WorkspaceLayout L;
+  auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
+  L.panel_off = 0;
+  L.sumsq_off = up(rs::panel_workspace_bytes());
+  L.linv_off = L.sumsq_off + up(rs::sumsq_workspace_bytes());
+  L.total = L.linv_off + up(sizeof(double) * kMaxB * kMaxB);
+  return L;
+}
+
+inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+inline char* W(void* ws, size_t off) { return static_cast<char*>(ws) + off; }
+
+}  // namespace
+
+extern "C" {
+
+int rs_abi_version(void) { return RS_ABI_VERSION; }
+
+const char* rs_status_string(int status) {
+  switch (status) {
+    case RS_OK: return "ok";
+    case RS_ERR_ARG: return "invalid argument";
+    case RS_ERR_CUDA: return "CUDA launch error";
+    case RS_ERR_CAPACITY: return "problem exceeds on-chip capacity of the panel kernel";
+    default: return "unknown status";
+  }
+}
+
+size_t rs_workspace_bytes(void) { return layout().total; }
+
+unsigned long long rs_launch_count(void) { return rs::g_launch_count.load(); }
+
+int rs_dgemm(int M, int N, int K, double alpha, const double* A, long long lda, int a_colmajor,
+             const int64_t* aidx, const double* B, long long ldb, const int64_t* bidx, double beta,
+             const double* Cin, long long ldcin, const int64_t* cidx, double* C, long long ldc,
+             void* stream) {
+  if (a_colmajor && aidx) return RS_ERR_ARG;
+  if (beta != 0.0 && Cin == nullptr) return RS_ERR_ARG;
+  rs::DGemmParams p{M, N, K, A, lda, aidx, B, ldb, bidx, Cin, ldcin, cidx, C, ldc, alpha, beta};
+  return rs::launch_dgemm(p, a_colmajor != 0, S(stream));
+}
+
+int rs_sketch_gemm(int m, int n, int ell, const double* A, long long lda, int a_colmajor,
+                   const double* Omega, long long ldo, double* Y, long long ldy, void* stream) {
+  return rs_dgemm(m, ell, n, 1.0, A, lda, a_colmajor, nullptr, Omega, ldo, nullptr, 0.0, nullptr, 0,
+                  nullptr, Y, ldy, stream);
+}
+
+int rs_panel_lupp(double* S_, long long lds, int R, int w, int64_t* perm_out, int* ncols_dev,
+                  void* workspace, void* stream) {
+  return rs::launch_panel(S_, lds, R, w, perm_out, ncols_dev, W(workspace, layout().panel_off),
+                          S(stream));
+}
+
+int rs_sumsq(const double* X, long long ldx, int R, int w, double* out, void* workspace, void* stream) {
+  return rs::launch_sumsq(X, ldx, R, w, reinterpret_cast<double*>(W(workspace, layout().sumsq_off)),
+                          out, S(stream));
+}
+
+int rs_schur_block(int m, int k, int b, const double* Y, long long ldy, const int64_t* perm,
+                   const double* T, long long ldt, double* S_, long long lds, double* e2_dev,
+                   void* workspace, void* stream) {
+  if (m < 0 || k < 0 || k > m || b < 0 || b > kMaxB) return RS_ERR_ARG;
+  const int R = m - k;
+  int rc;
+  if (k == 0) {
+    rc = rs::launch_gather_rows(Y, ldy, perm, R, b, S_, lds, S(stream));
+  } else {
+    rs::DGemmParams p{R, b, k, T, ldt, nullptr, Y, ldy, perm, Y, ldy, perm + k, S_, lds, -1.0, 1.0};
+    rc = rs::launch_dgemm(p, false, S(stream));
+  }
+  if (rc != RS_OK) return rc;
+  if (e2_dev) rc = rs_sumsq(S_, lds, R, b, e2_dev, workspace, stream);
+  return rc;
+}
+
+int rs_absorb_block(int m, int k, int nc, const double* S_, long long lds, const int64_t* sub_perm,
+                    const double* T, long long ldt, double* T_new, const int64_t* perm,
+                    int64_t* perm_new, void* workspace, void* stream) {
+  if (m < 0 || k < 0 || nc < 0 || nc > kMaxB || k + nc > m) return RS_ERR_ARG;
+  const int R = m - k;
+  const long long ldn = k + nc;
+  double* linv = reinterpret_cast<double*>(W(workspace, layout().linv_off));
+  int rc = RS_OK;
+  if (nc > 0) {
+    // L_1^{-1}: unit lower triangle of the pivot rows (positions 0..nc-1).
+    rc = rs::launch_trinv(S_, lds, 1, sub_perm, nc, 1, 1, linv, kMaxB, S(stream));
+    if (rc != RS_OK) return rc;
+    // W_hat = L_r L_1^{-1} -> T_new[:, k:k+nc]
+    rs::DGemmParams pw{R - nc, nc, nc, S_, lds, sub_perm + nc, linv, kMaxB, nullptr, nullptr, 0,
+                       nullptr, T_new + k, ldn, 1.0, 0.0};
+    rc = rs::launch_dgemm(pw, false, S(stream));
+    if (rc != RS_OK) return rc;
+    if (k > 0) {
+      // T_new[:, :k] = T[Q_hat] - W_hat T[P_hat]
+      rs::DGemmParams pt{R - nc, k, nc, T_new + k, ldn, nullptr, T, ldt, sub_perm, T, ldt,
+                         sub_perm + nc, T_new, ldn, -1.0, 1.0};
+      rc = rs::launch_dgemm(pt, false, S(stream));
+      if (rc != RS_OK) return rc;
+    }
+  }
+  return rs::launch_perm_update(perm, perm_new, m, k, sub_perm, S(stream));
+}
+
+int rs_scatter_interp(const double* T, long long ldt, const int64_t* perm, int m, int k, double* Wm,
+                      long long ldw, void* stream) {
+  return rs::launch_scatter_interp(T, ldt, perm, m, k, Wm, ldw, S(stream));
+}
+
+int rs_gather_rows(const double* src, long long lds, const int64_t* idx, int nrows, int ncols,
+                   double* dst, long long ldd, void* stream) {
+  return rs::launch_gather_rows(src, lds, idx, nrows, ncols, dst, ldd, S(stream));
+}
+
+int rs_trinv(const double* T, long long rs_, long long cs_, const int64_t* ridx, int n, int lower,
+             int unit, double* out, long long ldo, void* stream) {
+  return rs::launch_trinv(T, rs_, cs_, ridx, n, lower, unit, out, ldo, S(stream));
+}
+
+int rs_perm_update(const int64_t* perm, int64_t* perm_new, int m, int k, const int64_t* sub,
+                   void* stream) {
+  return rs::launch_perm_update(perm, perm_new, m, k, sub, S(stream));
+}
+
+int rs_transpose(const double* src, long long lds, int rows, int cols, double* dst, long long ldd,
+                 void* stream) {
+  return rs::launch_transpose(src, lds, rows, cols, dst, ldd, S(stream));
+}
+
+int rs_iota(int64_t* p, int n, void* stream) { return rs::launch_iota(p, n, S(stream)); }
+
+}  // extern "C"

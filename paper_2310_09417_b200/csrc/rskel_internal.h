@@ -1,0 +1,54 @@
+// Internal launch interfaces shared by the kernel translation units and the
+// C-ABI layer (capi.cu).  Nothing here crosses the library boundary.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rs {
+
+// Every kernel launch of the library bumps this counter (rs_launch_count()).
+void count_launch(int n);
+
+struct DGemmParams {
+  int M, N, K;
+  const double* A;
+  long long lda;
+  const int64_t* aidx;  // row-major A only: row i of A is A[aidx[i]]
+  const double* B;
+  long long ldb;
+  const int64_t* bidx;  // row k of B is B[bidx[k]]
+  const double* Cin;
+  long long ldcin;
+  const int64_t* cidx;  // row i of Cin is Cin[cidx[i]]
+  double* C;
+  long long ldc;
+  double alpha, beta;
+};
+
+int launch_dgemm(const DGemmParams& p, bool a_col, cudaStream_t st);
+
+// Panel LUPP (cooperative grid).  Factors the R x w row-major block S in
+// place with partial pivoting (first maximum in the current position wins,
+// `dense.py:185-207`); rows stay in physical order, the position map is
+// returned as perm_out (position -> physical row), *ncols_dev receives the
+// number of eliminated columns.  Workspace: see panel_workspace_bytes().
+size_t panel_workspace_bytes();
+int launch_panel(double* S, long long lds, int R, int w, int64_t* perm_out, int* ncols_dev,
+                 void* workspace, cudaStream_t st);
+
+int launch_gather_rows(const double* src, long long lds, const int64_t* idx, int nrows, int ncols,
+                       double* dst, long long ldd, cudaStream_t st);
+size_t sumsq_workspace_bytes();
+int launch_sumsq(const double* X, long long ldx, int R, int w, double* partial_ws, double* out,
+                 cudaStream_t st);
+int launch_trinv(const double* T, long long rs_, long long cs_, const int64_t* ridx, int n, int lower,
+                 int unit, double* out, long long ldo, cudaStream_t st);
+int launch_perm_update(const int64_t* perm, int64_t* perm_new, int m, int k, const int64_t* sub,
+                       cudaStream_t st);
+int launch_iota(int64_t* p, int n, cudaStream_t st);
+int launch_scatter_interp(const double* T, long long ldt, const int64_t* perm, int m, int k, double* W,
+                          long long ldw, cudaStream_t st);
+int launch_transpose(const double* src, long long lds, int rows, int cols, double* dst, long long ldd,
+                     cudaStream_t st);
+
+}  // namespace rs
