@@ -267,12 +267,17 @@ def main():
     a_host = a_host_t.numpy()
     torch.cuda.synchronize()
     e2e_ms = []
-    for _ in range(args.e2e_steps):
+    res_h = None
+    for i in range(args.e2e_steps + 1):  # first call warms the pinned host pool (not timed)
+        nb = None if res_h is None else (len(res_h.trace) + 1, res_h.rank)
+        res_h = None  # the caller consumed the previous result: its pinned block is reused
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         res_h = rs.rand_lupp_adaptive(a_host.T, b, tau, spec, rs.RngStream(seed))
         torch.cuda.synchronize()
-        e2e_ms.append(1e3 * (time.perf_counter() - t0))
+        if i > 0:
+            e2e_ms.append(1e3 * (time.perf_counter() - t0))
+    del nb
     e2e_t = torch.tensor([float(np.median(e2e_ms))], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)

@@ -51,17 +51,19 @@ unsigned long long rs_launch_count(void);
  * (A[k*lda + i]; aidx must be NULL).  B: K x N row-major, row k at bidx[k].
  * Cin row i at cidx[i].  Replaces the OpenBLAS dgemm calls of `gemm`
  * (dense.py:118-141), `GaussianSketch.apply` (sketching.py:122-128) and the
- * Schur/trailing updates (dense.py:232, skeleton.py:322). */
+ * Schur/trailing updates (dense.py:232, skeleton.py:322).  `workspace` (may
+ * be NULL) enables the deterministic stream-K split for skinny shapes. */
 int rs_dgemm(int M, int N, int K, double alpha, const double* A, long long lda, int a_colmajor,
              const int64_t* aidx, const double* B, long long ldb, const int64_t* bidx, double beta,
              const double* Cin, long long ldcin, const int64_t* cidx, double* C, long long ldc,
-             void* stream);
+             void* workspace, void* stream);
 
 /* Y (m x ell) = A (m x n) * Omega (n x ell): the sketch `a @ omega`
  * (sketching.py:128, 272).  a_colmajor selects the `a.T` view of a C-ordered
  * matrix (column ID / `rand_lupp_adaptive(A.T, ...)`). */
 int rs_sketch_gemm(int m, int n, int ell, const double* A, long long lda, int a_colmajor,
-                   const double* Omega, long long ldo, double* Y, long long ldy, void* stream);
+                   const double* Omega, long long ldo, double* Y, long long ldy, void* workspace,
+                   void* stream);
 
 /* Panel LU with partial pivoting of the R x w (w <= 64) block S, in place,
  * rows kept in physical order: `_lupp_panel` (dense.py:185-207) over one
@@ -91,6 +93,13 @@ int rs_schur_block(int m, int k, int b, const double* Y, long long ldy, const in
 int rs_absorb_block(int m, int k, int nc, const double* S, long long lds, const int64_t* sub_perm,
                     const double* T, long long ldt, double* T_new, const int64_t* perm,
                     int64_t* perm_new, void* workspace, void* stream);
+
+/* C[i, :] = Cin[cidx[i], :] - A[i, :K] * B[bidx[0..K), :] with K <= 64: the
+ * rank-b interpolation update inside rs_absorb_block (the trailing-update
+ * role of dense.py:232 in T form).  Persistent DMMA kernel. */
+int rs_rank_update(int M, int N, int K, const double* A, long long lda, const double* B, long long ldb,
+                   const int64_t* bidx, const double* Cin, long long ldcin, const int64_t* cidx,
+                   double* C, long long ldc, void* stream);
 
 /* W (m x k, row-major) with W[perm[:k]] = I and W[perm[k:]] = T
  * (`_w_from_parts`, skeleton.py:176-182). */

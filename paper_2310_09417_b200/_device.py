@@ -168,7 +168,8 @@ def dgemm(a, b, alpha=1.0, beta=0.0, cin=None, out=None, aidx=None, bidx=None, c
         b.ptr, b.ld, bidx.data_ptr() if bidx is not None else None,
         float(beta), cin.ptr if cin is not None else None, cin.ld if cin is not None else 0,
         cidx.data_ptr() if cidx is not None else None,
-        out.data_ptr(), out.stride(0) if out.dim() == 2 else N, stream_handle(),
+        out.data_ptr(), out.stride(0) if out.dim() == 2 else N, workspace().data_ptr(),
+        stream_handle(),
     )
     return out
 
@@ -180,5 +181,5 @@ def sketch(a, omega):
     om = torch.as_tensor(np.ascontiguousarray(omega, dtype=np.float64)).to(device())
     y = torch.empty((m, ell), dtype=torch.float64, device=device())
     _lib.call("rs_sketch_gemm", m, n, ell, a.ptr, a.ld, int(a.colmajor), om.data_ptr(),
-              max(ell, 1), y.data_ptr(), max(ell, 1), stream_handle())
+              max(ell, 1), y.data_ptr(), max(ell, 1), workspace().data_ptr(), stream_handle())
     return y

@@ -95,8 +95,14 @@ class TFormState:
             self.T.data_ptr(), max(self.k, 1), self._T[nxt].data_ptr(), self.perm.data_ptr(),
             self._perm[nxt].data_ptr(), self.ws.data_ptr(), self.stream,
         )
+        self._prev = (self._cur, self.k)
         self._cur = nxt
         self.k += nc
+
+    def rollback(self):
+        """Undo the last absorb (its inputs are intact in the other buffers):
+        used when a speculative absorb assumed a full-width elimination."""
+        self._cur, self.k = self._prev
 
     def interpolation(self, out=None):
         """Dense W (m x k) with W[perm[:k]] = I, W[perm[k:]] = T."""

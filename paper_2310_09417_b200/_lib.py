@@ -26,12 +26,15 @@ SIGNATURES = {
     "rs_workspace_bytes": (ctypes.c_size_t, []),
     "rs_launch_count": (ctypes.c_ulonglong, []),
     "rs_dgemm": (_c_int, [_c_int, _c_int, _c_int, _c_double, _p, _c_ll, _c_int, _p, _p, _c_ll, _p,
-                          _c_double, _p, _c_ll, _p, _p, _c_ll, _p]),
-    "rs_sketch_gemm": (_c_int, [_c_int, _c_int, _c_int, _p, _c_ll, _c_int, _p, _c_ll, _p, _c_ll, _p]),
+                          _c_double, _p, _c_ll, _p, _p, _c_ll, _p, _p]),
+    "rs_sketch_gemm": (_c_int, [_c_int, _c_int, _c_int, _p, _c_ll, _c_int, _p, _c_ll, _p, _c_ll,
+                                _p, _p]),
     "rs_panel_lupp": (_c_int, [_p, _c_ll, _c_int, _c_int, _p, _p, _p, _p]),
     "rs_schur_block": (_c_int, [_c_int, _c_int, _c_int, _p, _c_ll, _p, _p, _c_ll, _p, _c_ll, _p, _p, _p]),
     "rs_absorb_block": (_c_int, [_c_int, _c_int, _c_int, _p, _c_ll, _p, _p, _c_ll, _p, _p, _p, _p, _p]),
-    "rs_scatter_interp": (_c_int, [_p, _c_ll, _p, _c_int, _c_int, _p, _c_ll, _p]),
+    "rs_rank_update": (_c_int, [_c_int, _c_int, _c_int, _p, _c_ll, _p, _c_ll, _p, _p, _c_ll, _p, _p,
+                                _c_ll, _p]),
+    "rs_scatter_interp":(_c_int, [_p, _c_ll, _p, _c_int, _c_int, _p, _c_ll, _p]),
     "rs_gather_rows": (_c_int, [_p, _c_ll, _p, _c_int, _c_int, _p, _c_ll, _p]),
     "rs_sumsq": (_c_int, [_p, _c_ll, _c_int, _c_int, _p, _p, _p]),
     "rs_trinv": (_c_int, [_p, _c_ll, _c_ll, _p, _c_int, _c_int, _c_int, _p, _c_ll, _p]),

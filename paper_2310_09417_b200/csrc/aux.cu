@@ -94,42 +94,64 @@ int launch_sumsq(const double* X, long long ldx, int R, int w, double* partial_w
 // Element (i, j) of the input triangle is T[ridx(i) * rs + j * cs].  Thread c
 // computes column c of the inverse by substitution; out is n x n row-major.
 constexpr int TI_MAX = 64;
-__global__ void trinv_kernel(const double* __restrict__ T, long long rs_, long long cs_,
-                             const int64_t* __restrict__ ridx, int n, int lower, int unit,
-                             double* __restrict__ out, long long ldo) {
-  extern __shared__ double ti_smem[];
-  double (*L)[TI_MAX + 1] = reinterpret_cast<double (*)[TI_MAX + 1]>(ti_smem);
-  double (*X)[TI_MAX + 1] = reinterpret_cast<double (*)[TI_MAX + 1]>(ti_smem + TI_MAX * (TI_MAX + 1));
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
-    int i = e / n, j = e - i * n;
-    long long r = ridx ? ridx[i] : i;
-    L[i][j] = T[r * rs_ + (long long)j * cs_];
+// Fully unrolled substitution: thread c keeps column c of the inverse in
+// registers (x[0..63]); L[i][q] are shared-memory broadcasts.  The problem is
+// padded to 64 (identity outside n x n), 4 partial sums shorten the FMA chain.
+template <bool LOWER>
+__global__ void __launch_bounds__(TI_MAX) trinv_kernel(const double* __restrict__ T, long long rs_,
+                                                       long long cs_, const int64_t* __restrict__ ridx,
+                                                       int n, int unit, double* __restrict__ out,
+                                                       long long ldo) {
+  __shared__ double L[TI_MAX][TI_MAX];
+  for (int e = threadIdx.x; e < TI_MAX * TI_MAX; e += blockDim.x) {
+    const int i = e / TI_MAX, j = e - i * TI_MAX;
+    double v;
+    if (i < n && j < n) {
+      const long long r = ridx ? ridx[i] : i;
+      v = T[r * rs_ + (long long)j * cs_];
+    } else {
+      v = (i == j) ? 1.0 : 0.0;
+    }
+    L[i][j] = v;
   }
   __syncthreads();
-  int c = threadIdx.x;
-  if (c < n) {
-    if (lower) {
-      for (int i = 0; i < n; ++i) {
-        double s = (i == c) ? 1.0 : 0.0;
-        if (i > c) {
-          for (int q = c; q < i; ++q) s -= L[i][q] * X[q][c];
-        }
-        X[i][c] = (i < c) ? 0.0 : (unit ? s : s / L[i][i]);
+  const int c = threadIdx.x;
+  double x[TI_MAX];
+  if (LOWER) {
+#pragma unroll
+    for (int i = 0; i < TI_MAX; ++i) {
+      double s0 = (i == c) ? 1.0 : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+      for (int q = 0; q < i; ++q) {
+        const double lq = L[i][q];
+        if ((q & 3) == 0) s0 -= lq * x[q];
+        else if ((q & 3) == 1) s1 -= lq * x[q];
+        else if ((q & 3) == 2) s2 -= lq * x[q];
+        else s3 -= lq * x[q];
       }
-    } else {
-      for (int i = n - 1; i >= 0; --i) {
-        double s = (i == c) ? 1.0 : 0.0;
-        if (i < c) {
-          for (int q = i + 1; q <= c; ++q) s -= L[i][q] * X[q][c];
-        }
-        X[i][c] = (i > c) ? 0.0 : (unit ? s : s / L[i][i]);
+      const double s = (s0 + s1) + (s2 + s3);
+      x[i] = unit ? s : s / L[i][i];
+    }
+  } else {
+#pragma unroll
+    for (int i = TI_MAX - 1; i >= 0; --i) {
+      double s0 = (i == c) ? 1.0 : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+      for (int q = i + 1; q < TI_MAX; ++q) {
+        const double lq = L[i][q];
+        if ((q & 3) == 0) s0 -= lq * x[q];
+        else if ((q & 3) == 1) s1 -= lq * x[q];
+        else if ((q & 3) == 2) s2 -= lq * x[q];
+        else s3 -= lq * x[q];
       }
+      const double s = (s0 + s1) + (s2 + s3);
+      x[i] = unit ? s : s / L[i][i];
     }
   }
-  __syncthreads();
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
-    int i = e / n, j = e - i * n;
-    out[(long long)i * ldo + j] = X[i][j];
+  if (c < n) {
+#pragma unroll
+    for (int i = 0; i < TI_MAX; ++i)
+      if (i < n) out[(long long)i * ldo + c] = x[i];
   }
 }
 
@@ -137,13 +159,8 @@ int launch_trinv(const double* T, long long rs_, long long cs_, const int64_t* r
                  int unit, double* out, long long ldo, cudaStream_t st) {
   if (n < 0 || n > TI_MAX) return RS_ERR_ARG;
   if (n == 0) return RS_OK;
-  constexpr int smem = 2 * TI_MAX * (TI_MAX + 1) * sizeof(double);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(trinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    configured = true;
-  }
-  trinv_kernel<<<1, TI_MAX, smem, st>>>(T, rs_, cs_, ridx, n, lower, unit, out, ldo);
+  if (lower) trinv_kernel<true><<<1, TI_MAX, 0, st>>>(T, rs_, cs_, ridx, n, unit, out, ldo);
+  else trinv_kernel<false><<<1, TI_MAX, 0, st>>>(T, rs_, cs_, ridx, n, unit, out, ldo);
   count_launch(1);
   return cudaGetLastError() == cudaSuccess ? RS_OK : RS_ERR_CUDA;
 }

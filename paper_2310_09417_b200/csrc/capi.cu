@@ -16,21 +16,31 @@ namespace {
 constexpr int kMaxB = 64;
 
 struct WorkspaceLayout {
-  size_t panel_off, sumsq_off, linv_off, total;
+  size_t panel_off, sumsq_off, linv_off, gemm_off, total;
 };
 
 WorkspaceLayout layout() {
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    cudaGetLastError();
+    nsm = 148;  // no device (build host): size for B200
+  }
   WorkspaceLayout L;
   auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
   L.panel_off = 0;
   L.sumsq_off = up(rs::panel_workspace_bytes());
   L.linv_off = L.sumsq_off + up(rs::sumsq_workspace_bytes());
-  L.total = L.linv_off + up(sizeof(double) * kMaxB * kMaxB);
+  L.gemm_off = L.linv_off + up(sizeof(double) * kMaxB * kMaxB);
+  L.total = L.gemm_off + up(rs::gemm_partials_bytes(nsm));
   return L;
 }
 
 inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 inline char* W(void* ws, size_t off) { return static_cast<char*>(ws) + off; }
+inline double* gemm_ws(void* ws) {
+  return ws ? reinterpret_cast<double*>(W(ws, layout().gemm_off)) : nullptr;
+}
 
 }  // namespace
 
@@ -55,17 +65,19 @@ unsigned long long rs_launch_count(void) { return rs::g_launch_count.load(); }
 int rs_dgemm(int M, int N, int K, double alpha, const double* A, long long lda, int a_colmajor,
              const int64_t* aidx, const double* B, long long ldb, const int64_t* bidx, double beta,
              const double* Cin, long long ldcin, const int64_t* cidx, double* C, long long ldc,
-             void* stream) {
+             void* workspace, void* stream) {
   if (a_colmajor && aidx) return RS_ERR_ARG;
   if (beta != 0.0 && Cin == nullptr) return RS_ERR_ARG;
-  rs::DGemmParams p{M, N, K, A, lda, aidx, B, ldb, bidx, Cin, ldcin, cidx, C, ldc, alpha, beta};
+  rs::DGemmParams p{M, N, K, A, lda, aidx, B, ldb, bidx, Cin, ldcin, cidx, C, ldc, alpha, beta,
+                    gemm_ws(workspace)};
   return rs::launch_dgemm(p, a_colmajor != 0, S(stream));
 }
 
 int rs_sketch_gemm(int m, int n, int ell, const double* A, long long lda, int a_colmajor,
-                   const double* Omega, long long ldo, double* Y, long long ldy, void* stream) {
+                   const double* Omega, long long ldo, double* Y, long long ldy, void* workspace,
+                   void* stream) {
   return rs_dgemm(m, ell, n, 1.0, A, lda, a_colmajor, nullptr, Omega, ldo, nullptr, 0.0, nullptr, 0,
-                  nullptr, Y, ldy, stream);
+                  nullptr, Y, ldy, workspace, stream);
 }
 
 int rs_panel_lupp(double* S_, long long lds, int R, int w, int64_t* perm_out, int* ncols_dev,
@@ -88,7 +100,8 @@ int rs_schur_block(int m, int k, int b, const double* Y, long long ldy, const in
   if (k == 0) {
     rc = rs::launch_gather_rows(Y, ldy, perm, R, b, S_, lds, S(stream));
   } else {
-    rs::DGemmParams p{R, b, k, T, ldt, nullptr, Y, ldy, perm, Y, ldy, perm + k, S_, lds, -1.0, 1.0};
+    rs::DGemmParams p{R, b, k, T, ldt, nullptr, Y, ldy, perm, Y, ldy, perm + k, S_, lds, -1.0, 1.0,
+                      gemm_ws(workspace)};
     rc = rs::launch_dgemm(p, false, S(stream));
   }
   if (rc != RS_OK) return rc;
@@ -110,18 +123,24 @@ int rs_absorb_block(int m, int k, int nc, const double* S_, long long lds, const
     if (rc != RS_OK) return rc;
     // W_hat = L_r L_1^{-1} -> T_new[:, k:k+nc]
     rs::DGemmParams pw{R - nc, nc, nc, S_, lds, sub_perm + nc, linv, kMaxB, nullptr, nullptr, 0,
-                       nullptr, T_new + k, ldn, 1.0, 0.0};
+                       nullptr, T_new + k, ldn, 1.0, 0.0, gemm_ws(workspace)};
     rc = rs::launch_dgemm(pw, false, S(stream));
     if (rc != RS_OK) return rc;
     if (k > 0) {
-      // T_new[:, :k] = T[Q_hat] - W_hat T[P_hat]
-      rs::DGemmParams pt{R - nc, k, nc, T_new + k, ldn, nullptr, T, ldt, sub_perm, T, ldt,
-                         sub_perm + nc, T_new, ldn, -1.0, 1.0};
-      rc = rs::launch_dgemm(pt, false, S(stream));
+      // T_new[:, :k] = T[Q_hat] - W_hat T[P_hat]  (persistent rank-nc update kernel)
+      rc = rs::launch_rank_update(R - nc, k, nc, T_new + k, ldn, T, ldt, sub_perm, T, ldt,
+                                  sub_perm + nc, T_new, ldn, S(stream));
       if (rc != RS_OK) return rc;
     }
   }
   return rs::launch_perm_update(perm, perm_new, m, k, sub_perm, S(stream));
+}
+
+int rs_rank_update(int M, int N, int K, const double* A, long long lda, const double* B, long long ldb,
+                   const int64_t* bidx, const double* Cin, long long ldcin, const int64_t* cidx,
+                   double* C, long long ldc, void* stream) {
+  if (bidx == nullptr || cidx == nullptr) return RS_ERR_ARG;
+  return rs::launch_rank_update(M, N, K, A, lda, B, ldb, bidx, Cin, ldcin, cidx, C, ldc, S(stream));
 }
 
 int rs_scatter_interp(const double* T, long long ldt, const int64_t* perm, int m, int k, double* Wm,

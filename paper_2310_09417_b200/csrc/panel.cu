@@ -6,16 +6,28 @@
 // slice of rows resident in shared memory for the whole panel (a 65472 x 64
 // fp64 Schur block is 33.5 MB = 148 CTAs x 226 KB).  Rows never move: the
 // reference's full-row swaps are replaced by a position map pos[row] (the
-// "current permuted position" that breaks argmax ties, `dense.py:194`).  Per
-// column j each CTA publishes its best (|v|, pos, row, row values) candidate,
-// one grid barrier, then every CTA reduces the G candidates identically
-// (deterministic), takes the pivot row from the candidate buffer and applies
-// scale + rank-1 update to its own rows while computing its next candidate.
-// That is one grid barrier per eliminated column.
+// "current permuted position" that breaks argmax ties, `dense.py:194`).
+//
+// Per column j the critical path is: every CTA publishes its best candidate
+// (|v|, pos, row, the row's values) with a release-store of a per-step
+// sequence number; warp 0 of every CTA polls the G sequence numbers (this is
+// the grid barrier and the data exchange in one round trip), reduces the G
+// candidates identically (deterministic), loads the pivot row, and all
+// threads scale column j and update column j+1 of their rows ("early"
+// update, one row per thread) to find the next candidate.  The rest of the
+// rank-1 update (columns j+2..w-1, "late" update) runs while warp 0 publishes
+// and waits for the next column, so it is off the critical path.
 //
 // Arithmetic follows numpy's rounding exactly: l = s / pivot (IEEE division),
 // s' = s - (l * u) with the product rounded before the subtraction (np.outer
 // then -=), i.e. no FMA contraction.
+//
+// Shared memory holds the rows with a 64-double stride and an XOR swizzle
+// (column c of local row i at i*64 + (c ^ (i & 31))), conflict-free for both
+// the row-per-thread (early) and row-per-warp (late) access patterns.
+#include <atomic>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "rskel_internal.h"
 
@@ -26,20 +38,63 @@ constexpr int PWARPS = PTHREADS / 32;
 constexpr int PMAXW = 64;
 constexpr int PMAXG = 1024;
 
+// LL-style exchange: every 8-byte word carries the step flag next to 4 bytes
+// of payload, so a reader that sees the flag in a word also sees its payload
+// (8-byte single-copy atomicity) -- no fences, no separate barrier.
 struct PanelScratch {
-  unsigned bar;
-  unsigned pad[31];
-  double cval[2][PMAXG];
-  int cpos[2][PMAXG];
-  int crow[2][PMAXG];
-  double crowdata[2][PMAXG][PMAXW];
+  uint4 rec[2][PMAXG][2];           // {val.lo, f, val.hi, f}, {pos, f, row + 1, f}
+  uint4 bc[2][8];                   // winner broadcast: val, {pos, row + 1}, {cta}
+  uint4 rowdata[2][PMAXG][PMAXW];   // candidate row: {x.lo, f, x.hi, f} per column
 };
+
+RS_DEV void st_v4(uint4* p, unsigned a, unsigned b, unsigned c, unsigned d) {
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};\n" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d)
+               : "memory");
+}
+RS_DEV uint4 ld_v4(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+RS_DEV double join(unsigned lo, unsigned hi) {
+  return __longlong_as_double((long long)(((unsigned long long)hi << 32) | lo));
+}
 
 size_t panel_workspace_bytes() { return sizeof(PanelScratch); }
 
+RS_DEV int swz(int i, int c) { return i * PMAXW + (c ^ (i & 31)); }
+
+
+// Block-wide argmax of (val desc, pos asc); returns the winner's local row
+// (-1 if no thread had a candidate) in every thread.  Uses red_* scratch.
+RS_DEV void block_best(double& v, int& p, int& r, double* red_v, int* red_p, int* red_r) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    double ov = __shfl_xor_sync(0xffffffffu, v, off);
+    int op = __shfl_xor_sync(0xffffffffu, p, off);
+    int orr = __shfl_xor_sync(0xffffffffu, r, off);
+    if (orr >= 0 && (r < 0 || key_better(ov, op, v, p))) { v = ov; p = op; r = orr; }
+  }
+  if (lane == 0) { red_v[warp] = v; red_p[warp] = p; red_r[warp] = r; }
+  __syncthreads();
+  v = red_v[0]; p = red_p[0]; r = red_r[0];
+#pragma unroll
+  for (int q = 1; q < PWARPS; ++q) {
+    if (red_r[q] >= 0 && (r < 0 || key_better(red_v[q], red_p[q], v, p))) {
+      v = red_v[q]; p = red_p[q]; r = red_r[q];
+    }
+  }
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(PTHREADS, 1)
     panel_kernel(double* __restrict__ S, long long lds, int R, int w, int rows_per,
-                 int64_t* __restrict__ perm_out, int* __restrict__ ncols_out, PanelScratch* ws) {
+                 int64_t* __restrict__ perm_out, int* __restrict__ ncols_out, PanelScratch* ws,
+                 unsigned flag_base) {
   extern __shared__ __align__(16) double psm[];
   const int G = gridDim.x, cta = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -47,117 +102,166 @@ __global__ void __launch_bounds__(PTHREADS, 1)
   int nloc = R - r0;
   nloc = nloc < 0 ? 0 : (nloc > rows_per ? rows_per : nloc);
 
-  double* Ss = psm;                                  // nloc x w
-  int* pos = reinterpret_cast<int*>(psm + (size_t)rows_per * w);  // nloc
-  __shared__ double Urow[PMAXW];
-  __shared__ double wv[PWARPS];
-  __shared__ int wp[PWARPS], wr[PWARPS];
+  double* Ss = psm;                                                   // rows_per x 64 (swizzled)
+  int* pos = reinterpret_cast<int*>(psm + (size_t)rows_per * PMAXW);  // rows_per
+  __shared__ double Urow2[2][PMAXW];  // U row of step j in Urow2[j & 1] (late update reads j-1)
+  __shared__ double red_v[PWARPS];
+  __shared__ int red_p[PWARPS], red_r[PWARPS];
   __shared__ double s_val;
-  __shared__ int s_pos, s_row, s_cta, s_best_local;
+  __shared__ int s_pos, s_row;
 
   for (int idx = tid; idx < nloc * w; idx += PTHREADS) {
     int i = idx / w, c = idx - i * w;
-    Ss[idx] = S[(long long)(r0 + i) * lds + c];
+    Ss[swz(i, c)] = S[(long long)(r0 + i) * lds + c];
   }
   for (int i = tid; i < nloc; i += PTHREADS) pos[i] = r0 + i;
   __syncthreads();
 
-  // Warp-uniform running best for the current column.
+  // Candidate for column 0.
   double bv = -1.0;
   int bp = 0x7fffffff, br = -1;
-  for (int i = warp; i < nloc; i += PWARPS) {
-    double v = fabs(Ss[i * w]);
-    if (key_better(v, pos[i], bv, bp)) { bv = v; bp = pos[i]; br = i; }
+  for (int i = tid; i < nloc; i += PTHREADS) {
+    double v = fabs(Ss[swz(i, 0)]);
+    if (key_better(v, pos[i], bv, bp) || br < 0) { bv = v; bp = pos[i]; br = i; }
   }
+  block_best(bv, bp, br, red_v, red_p, red_r);
 
   int ncols = w;
+  int late_j = -1;   // step whose columns late_j+2.. still need the rank-1 update
+  int late_skip = -1;
   for (int j = 0; j < w; ++j) {
     const int par = j & 1;
-    // ---- CTA candidate ----
-    if (lane == 0) { wv[warp] = bv; wp[warp] = bp; wr[warp] = br; }
-    __syncthreads();
-    if (tid == 0) {
-      double v = -1.0; int pp = 0x7fffffff, rr = -1;
-      for (int q = 0; q < PWARPS; ++q)
-        if (wr[q] >= 0 && key_better(wv[q], wp[q], v, pp)) { v = wv[q]; pp = wp[q]; rr = wr[q]; }
-      s_best_local = rr;
-      ws->cval[par][cta] = rr >= 0 ? v : -1.0;
-      ws->cpos[par][cta] = pp;
-      ws->crow[par][cta] = rr >= 0 ? r0 + rr : -1;
-    }
-    __syncthreads();
-    if (tid < w) ws->crowdata[par][cta][tid] = s_best_local >= 0 ? Ss[s_best_local * w + tid] : 0.0;
-    __threadfence();
-    grid_barrier(&ws->bar, (unsigned)(j + 1) * (unsigned)G);
-
-    // ---- global pivot (every CTA reduces the same candidates in the same way) ----
     if (warp == 0) {
-      double v = -1.0; int pp = 0x7fffffff, rr = -1, cc = -1;
-      for (int q = lane; q < G; q += 32) {
-        int row = __ldcg(&ws->crow[par][q]);
-        if (row < 0) continue;
-        double qv = __ldcg(&ws->cval[par][q]);
-        int qp = __ldcg(&ws->cpos[par][q]);
-        if (key_better(qv, qp, v, pp)) { v = qv; pp = qp; rr = row; cc = q; }
+      const unsigned f = flag_base + (unsigned)j + 1u;
+      // ---- publish this CTA's candidate for column j (no fence needed) ----
+      if (br >= 0) {
+        for (int c = lane; c < w; c += 32) {
+          const unsigned long long x = (unsigned long long)__double_as_longlong(Ss[swz(br, c)]);
+          st_v4(&ws->rowdata[par][cta][c], (unsigned)x, f, (unsigned)(x >> 32), f);
+        }
       }
+      if (lane == 0) {
+        const double v = br >= 0 ? bv : -1.0;
+        const unsigned long long x = (unsigned long long)__double_as_longlong(v);
+        st_v4(&ws->rec[par][cta][0], (unsigned)x, f, (unsigned)(x >> 32), f);
+        st_v4(&ws->rec[par][cta][1], (unsigned)bp, f, br >= 0 ? (unsigned)(r0 + br + 1) : 0u, f);
+      }
+      // ---- CTA 0 reduces the G candidates and broadcasts the winner; the
+      // others poll the single broadcast header (one hot line instead of G) ----
+      double v = -1.0;
+      int pp = 0x7fffffff, rr = -1, cc = -1;
+      if (cta == 0) {
+        constexpr int QMAX = (PMAXG + 31) / 32;
+        unsigned done = 0;  // bit i: record lane + 32 i consumed
+        const int nq = (G - lane + 31) / 32;
+        const unsigned all = nq >= 32 ? 0xffffffffu : ((1u << nq) - 1u);
+        while (done != all) {
+#pragma unroll 4
+          for (int i = 0; i < QMAX; ++i) {
+            if (i >= nq || (done >> i) & 1u) continue;
+            const int q = lane + 32 * i;
+            const uint4 a = ld_v4(&ws->rec[par][q][0]);
+            const uint4 b = ld_v4(&ws->rec[par][q][1]);
+            if (a.y != f || a.w != f || b.y != f || b.w != f) continue;
+            done |= 1u << i;
+            const int row = (int)b.z - 1;
+            const double qv = join(a.x, a.z);
+            const int qp = (int)b.x;
+            if (row >= 0 && (rr < 0 || key_better(qv, qp, v, pp))) { v = qv; pp = qp; rr = row; cc = q; }
+          }
+        }
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        double ov = __shfl_xor_sync(0xffffffffu, v, off);
-        int op = __shfl_xor_sync(0xffffffffu, pp, off);
-        int orr = __shfl_xor_sync(0xffffffffu, rr, off);
-        int oc = __shfl_xor_sync(0xffffffffu, cc, off);
-        if (orr >= 0 && (rr < 0 || key_better(ov, op, v, pp))) { v = ov; pp = op; rr = orr; cc = oc; }
+        for (int off = 16; off > 0; off >>= 1) {
+          double ov = __shfl_xor_sync(0xffffffffu, v, off);
+          int op = __shfl_xor_sync(0xffffffffu, pp, off);
+          int orr = __shfl_xor_sync(0xffffffffu, rr, off);
+          int oc = __shfl_xor_sync(0xffffffffu, cc, off);
+          if (orr >= 0 && (rr < 0 || key_better(ov, op, v, pp))) { v = ov; pp = op; rr = orr; cc = oc; }
+        }
+        if (lane == 0) {
+          const unsigned long long x = (unsigned long long)__double_as_longlong(rr >= 0 ? v : 0.0);
+          st_v4(&ws->bc[par][0], (unsigned)x, f, (unsigned)(x >> 32), f);
+          st_v4(&ws->bc[par][1], (unsigned)pp, f, (unsigned)(rr + 1), f);
+          st_v4(&ws->bc[par][2], (unsigned)cc, f, 0u, f);
+        }
+      } else {
+        uint4 h = make_uint4(0, 0, 0, 0);
+        if (lane < 3) {
+          do {
+            h = ld_v4(&ws->bc[par][lane]);
+          } while (h.y != f || h.w != f);
+        }
+        const unsigned x0 = __shfl_sync(0xffffffffu, h.x, 0), x1 = __shfl_sync(0xffffffffu, h.z, 0);
+        v = join(x0, x1);
+        pp = (int)__shfl_sync(0xffffffffu, h.x, 1);
+        rr = (int)__shfl_sync(0xffffffffu, h.z, 1) - 1;
+        cc = (int)__shfl_sync(0xffffffffu, h.x, 2);
       }
-      if (lane == 0) { s_val = rr >= 0 ? v : 0.0; s_pos = pp; s_row = rr; s_cta = cc; }
+      if (lane == 0) { s_val = rr >= 0 ? v : 0.0; s_pos = pp; s_row = rr; }
+      // ---- pivot row (U row j) straight from the winner's published copy ----
+      if (rr >= 0 && v > 0.0) {
+        for (int c = j + lane; c < w; c += 32) {
+          uint4 x;
+          do {
+            x = ld_v4(&ws->rowdata[par][cc][c]);
+          } while (x.y != f || x.w != f);
+          Urow2[par][c] = join(x.x, x.z);
+        }
+      }
+    } else if (late_j >= 0) {
+      // ---- late update of the previous step (off the critical path) ----
+      const int jl = late_j;
+      for (int i = warp - 1; i < nloc; i += PWARPS - 1) {
+        if (pos[i] <= jl || i == late_skip) continue;
+        const double l = Ss[swz(i, jl)];
+        for (int c = jl + 2 + lane; c < w; c += 32) {
+          const int a = swz(i, c);
+          Ss[a] = __dsub_rn(Ss[a], __dmul_rn(l, Urow2[jl & 1][c]));
+        }
+      }
     }
     __syncthreads();
-    if (!(s_val > 0.0)) { ncols = j; break; }  // exactly-zero pivot column (or no rows left)
+    if (!(s_val > 0.0)) { ncols = j; break; }  // exactly-zero pivot column
     const int ppos = s_pos, prow = s_row;
-    if (tid >= j && tid < w) Urow[tid] = __ldcg(&ws->crowdata[par][s_cta][tid]);
-    __syncthreads();
 
-    // ---- swap bookkeeping, scale, rank-1 update, next candidate ----
-    const double upiv = Urow[j];
+    // ---- swap bookkeeping, scale column j, update column j+1, next candidate ----
+    const double upiv = Urow2[par][j];
+    const double unext = (j + 1 < w) ? Urow2[par][j + 1] : 0.0;
     bv = -1.0; bp = 0x7fffffff; br = -1;
-    for (int i = warp; i < nloc; i += PWARPS) {
+    for (int i = tid; i < nloc; i += PTHREADS) {
       int pi = pos[i];
-      if (pi < j) continue;             // pivoted in an earlier column
-      if (r0 + i == prow) {             // the pivot row moves to position j
-        __syncwarp();
-        if (lane == 0) pos[i] = j;
-        continue;
-      }
-      if (pi == j) pi = ppos;           // the row at position j takes the pivot's old slot
-      double l = __ddiv_rn(Ss[i * w + j], upiv);
-      __syncwarp();
-      if (lane == 0) pos[i] = pi;
-      double v0 = 0.0, v1 = 0.0;
-      {
-        int c = lane;
-        if (c < w) {
-          if (c == j) Ss[i * w + c] = l;
-          else if (c > j) { v0 = __dsub_rn(Ss[i * w + c], __dmul_rn(l, Urow[c])); Ss[i * w + c] = v0; }
-        }
-        c = lane + 32;
-        if (c < w) {
-          if (c == j) Ss[i * w + c] = l;
-          else if (c > j) { v1 = __dsub_rn(Ss[i * w + c], __dmul_rn(l, Urow[c])); Ss[i * w + c] = v1; }
-        }
-      }
+      if (pi < j) continue;
+      if (r0 + i == prow) { pos[i] = j; continue; }
+      if (pi == j) { pi = ppos; pos[i] = pi; }
+      const double l = __ddiv_rn(Ss[swz(i, j)], upiv);
+      Ss[swz(i, j)] = l;
       if (j + 1 < w) {
-        int jn = j + 1;
-        double nv = __shfl_sync(0xffffffffu, jn >= 32 ? v1 : v0, jn & 31);
-        nv = fabs(nv);
-        if (key_better(nv, pi, bv, bp)) { bv = nv; bp = pi; br = i; }
+        const int a = swz(i, j + 1);
+        const double v = __dsub_rn(Ss[a], __dmul_rn(l, unext));
+        Ss[a] = v;
+        const double av = fabs(v);
+        if (br < 0 || key_better(av, pi, bv, bp)) { bv = av; bp = pi; br = i; }
       }
     }
-    __syncthreads();
+    block_best(bv, bp, br, red_v, red_p, red_r);
+    // The new local best row is published next step: bring it fully up to date.
+    if (warp == 0 && br >= 0) {
+      const double l = Ss[swz(br, j)];
+      for (int c = j + 2 + lane; c < w; c += 32) {
+        const int a = swz(br, c);
+        Ss[a] = __dsub_rn(Ss[a], __dmul_rn(l, Urow2[par][c]));
+      }
+      __syncwarp();
+    }
+    late_j = j;
+    late_skip = br;
   }
+  __syncthreads();
 
   // ---- write back factors (physical row order) and the position map ----
   for (int idx = tid; idx < nloc * w; idx += PTHREADS) {
     int i = idx / w, c = idx - i * w;
-    S[(long long)(r0 + i) * lds + c] = Ss[idx];
+    S[(long long)(r0 + i) * lds + c] = Ss[swz(i, c)];
   }
   for (int i = tid; i < nloc; i += PTHREADS) perm_out[pos[i]] = r0 + i;
   if (cta == 0 && tid == 0) *ncols_out = ncols;
@@ -167,8 +271,6 @@ int launch_panel(double* S, long long lds, int R, int w, int64_t* perm_out, int*
                  void* workspace, cudaStream_t st) {
   if (R < 0 || w < 0 || w > PMAXW || (R > 0 && lds < w)) return RS_ERR_ARG;
   if (R == 0 || w == 0) {
-    int zero_cols = (R == 0) ? 0 : w;
-    (void)zero_cols;
     cudaMemsetAsync(ncols_dev, 0, sizeof(int), st);
     return cudaGetLastError() == cudaSuccess ? RS_OK : RS_ERR_CUDA;
   }
@@ -177,13 +279,17 @@ int launch_panel(double* S, long long lds, int R, int w, int64_t* perm_out, int*
   int nsm = 0, max_smem = 0;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  // Small panels: fewer CTAs, cheaper barrier.  Large: one CTA per SM.
+  // Small panels: fewer CTAs (cheaper exchange).  Large: one CTA per SM.
   int G = (R + 127) / 128;
+  if (const char* e = getenv("RSKEL_PANEL_ROWS_PER_CTA")) {
+    int rp = atoi(e);
+    if (rp > 0) G = (R + rp - 1) / rp;
+  }
   if (G > nsm) G = nsm;
   if (G < 1) G = 1;
   int rows_per = (R + G - 1) / G;
-  const size_t static_smem = 4096;  // Urow + reduction scratch (upper bound)
-  size_t smem = (size_t)rows_per * w * sizeof(double) + (size_t)rows_per * sizeof(int);
+  const size_t static_smem = 2048;
+  size_t smem = (size_t)rows_per * PMAXW * sizeof(double) + (size_t)rows_per * sizeof(int);
   smem = (smem + 15) & ~size_t(15);
   if (smem + static_smem > (size_t)max_smem) return RS_ERR_CAPACITY;
   cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -191,8 +297,10 @@ int launch_panel(double* S, long long lds, int R, int w, int64_t* perm_out, int*
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, panel_kernel, PTHREADS, smem);
   if (occ * nsm < G || G > PMAXG) return RS_ERR_CAPACITY;
   PanelScratch* ws = static_cast<PanelScratch*>(workspace);
-  cudaMemsetAsync(&ws->bar, 0, sizeof(unsigned), st);
-  void* args[] = {&S, &lds, &R, &w, &rows_per, &perm_out, &ncols_dev, &ws};
+  // Flags of launch e are e*128 + j + 1: stale words of earlier launches never match.
+  static std::atomic<unsigned> epoch{1};
+  unsigned flag_base = (epoch.fetch_add(1) & 0x1ffffffu) << 7;
+  void* args[] = {&S, &lds, &R, &w, &rows_per, &perm_out, &ncols_dev, &ws, &flag_base};
   cudaError_t e = cudaLaunchCooperativeKernel((void*)panel_kernel, dim3(G), dim3(PTHREADS), args, smem, st);
   count_launch(1);
   return e == cudaSuccess ? RS_OK : RS_ERR_CUDA;

@@ -23,9 +23,15 @@ struct DGemmParams {
   double* C;
   long long ldc;
   double alpha, beta;
+  double* partials;  // stream-K scratch (gemm_partials_bytes), nullptr = plain grid
 };
 
 int launch_dgemm(const DGemmParams& p, bool a_col, cudaStream_t st);
+// C[i, :] = Cin[cidx[i], :] - A[i, :K] B[bidx[0..K), :], K <= 64 (rank_update.cu)
+int launch_rank_update(int M, int N, int K, const double* A, long long lda, const double* B,
+                       long long ldb, const int64_t* bidx, const double* Cin, long long ldcin,
+                       const int64_t* cidx, double* C, long long ldc, cudaStream_t st);
+size_t gemm_partials_bytes(int nsm);
 
 // Panel LUPP (cooperative grid).  Factors the R x w row-major block S in
 // place with partial pivoting (first maximum in the current position wins,

@@ -209,8 +209,16 @@ class _NullTimer:
 
 
 class _AdaptiveDriver:
-    """Host side of the adaptive loop: one Omega block H2D, one e2 D2H and one
-    eliminated-column count D2H per block; everything else on the device."""
+    """Host side of the adaptive loop.
+
+    Streams: Omega_t is copied H2D on a side stream into a double-buffered
+    device slot while the compute stream works on earlier blocks; the sketch
+    of block t+1 is enqueued before the host waits for block t's estimate, and
+    the absorb of a block is enqueued speculatively (assuming a full-width
+    elimination) before its eliminated-column count is read back.  The host
+    therefore waits once per block (e2 of block t plus ncols of block t-1 in
+    one pinned readback) while the GPU keeps the next sketch GEMM running.
+    """
 
     def __init__(self, a, b, tau, rng, max_rank):
         self.prof = _PHASE_TIMER or _NullTimer()
@@ -219,48 +227,59 @@ class _AdaptiveDriver:
         self.m, self.n = m, n
         dev = _device.device()
         self.src = _omega.BlockOmegaSource(n, b, rng)
-        self.om = torch.empty((n, b), dtype=torch.float64, device=dev)
-        self.y = torch.empty((m, b), dtype=torch.float64, device=dev)
+        self.om = [torch.empty((n, b), dtype=torch.float64, device=dev) for _ in range(2)]
+        self.y = [torch.empty((m, b), dtype=torch.float64, device=dev) for _ in range(2)]
+        self.om_ready = [torch.cuda.Event() for _ in range(2)]
+        self.om_free = [None, None]
+        self.copy_stream = torch.cuda.Stream(device=dev)
+        self.compute = torch.cuda.current_stream(dev)
         self.e2 = torch.empty(1, dtype=torch.float64, device=dev)
         self.nc = torch.empty(max(1, (b + 63) // 64), dtype=torch.int32, device=dev)
+        self.h_e2 = torch.empty(1, dtype=torch.float64, pin_memory=True)
+        self.h_nc = torch.empty(1, dtype=torch.int32, pin_memory=True)
         self.st = _engine.TFormState(m, max_rank, min(b, _engine.MAX_BLOCK))
         self.stream = _device.stream_handle()
+        self.ws = _device.workspace()
+        self._issued = set()
+
+    # -- Omega pipeline --------------------------------------------------------
+    def _issue_copy(self, t):
+        if t in self._issued:
+            return
+        self._issued.add(t)
+        slot = t % 2
+        h = self.src.host(t)
+        with torch.cuda.stream(self.copy_stream):
+            if self.om_free[slot] is not None:
+                self.copy_stream.wait_event(self.om_free[slot])
+            self.om[slot].copy_(h, non_blocking=True)
+            self.om_ready[slot].record(self.copy_stream)
 
     def _sketch(self, t):
         from . import _lib
-        h = self.src.host(t)
-        tok = self.prof.start("omega_h2d")
-        self.om.copy_(h, non_blocking=True)
-        self.prof.stop(tok)
+        slot = t % 2
+        self._issue_copy(t)
+        self.compute.wait_event(self.om_ready[slot])
         tok = self.prof.start("sketch_gemm")
         _lib.call("rs_sketch_gemm", self.m, self.n, self.b, self.a.ptr, self.a.ld, int(self.a.colmajor),
-                  self.om.data_ptr(), self.b, self.y.data_ptr(), self.b, self.stream)
+                  self.om[slot].data_ptr(), self.b, self.y[slot].data_ptr(), self.b,
+                  self.ws.data_ptr(), self.stream)
         self.prof.stop(tok)
+        ev = torch.cuda.Event()
+        ev.record(self.compute)
+        self.om_free[slot] = ev
+        self._issue_copy(t + 2)
 
-    def _schur_norm2(self):
-        """||Y[perm[k:]] - T Y[perm[:k]]||^2 over all b columns (current state)."""
-        st, b = self.st, self.b
-        if b <= _engine.MAX_BLOCK:
-            tok = self.prof.start("schur")
-            st.schur(self.y.data_ptr(), b, b, self.e2)
-            self.prof.stop(tok)
-            return float(self.e2.item())
-        total = 0.0
-        for j0 in range(0, b, _engine.MAX_BLOCK):
-            w = min(_engine.MAX_BLOCK, b - j0)
-            st.schur(self.y.data_ptr() + 8 * j0, b, w, self.e2)
-            total += float(self.e2.item())
-        return total
-
-    def _absorb_block(self, first):
-        """Eliminate the current block; returns eliminated columns (< b iff an
-        exactly-zero pivot column was met, `_lupp_partial`)."""
+    # -- blocks ------------------------------------------------------------------
+    def _absorb_block(self, y, first):
+        """Eliminate the current block synchronously (first block, and b > 64);
+        returns eliminated columns (< b iff a zero pivot column, `_lupp_partial`)."""
         st, b = self.st, self.b
         done = 0
         for j0 in range(0, b, _engine.MAX_BLOCK):
             w = min(_engine.MAX_BLOCK, b - j0)
             if j0 > 0 or first or b > _engine.MAX_BLOCK:
-                st.schur(self.y.data_ptr() + 8 * j0, b, w, None)
+                st.schur(y.data_ptr() + 8 * j0, b, w, None)
             st.panel(w, self.nc)
             nc = int(self.nc[0].item())
             st.absorb(w, nc)
@@ -269,23 +288,60 @@ class _AdaptiveDriver:
                 break
         return done
 
+    def _readback(self, with_nc):
+        self.h_e2.copy_(self.e2, non_blocking=True)
+        if with_nc:
+            self.h_nc.copy_(self.nc[:1], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(self.compute)
+        return ev
+
     def run(self):
         st, b, tau = self.st, self.b, self.tau
+        wide = b > _engine.MAX_BLOCK
         try:
             # adaptive_init (`skeleton.py:298-314`): lupp of the first block.
             self._sketch(0)
-            st.schur(self.y.data_ptr(), b, min(b, _engine.MAX_BLOCK), self.e2)
-            if b > _engine.MAX_BLOCK or not math.isfinite(float(self.e2.item())):
-                _finite_or_raise(_device.Matrix(self.y, self.m, b, b, False, self.a.kind))
-            done = self._absorb_block(first=True)
+            y0 = self.y[0]
+            st.schur(y0.data_ptr(), b, min(b, _engine.MAX_BLOCK), self.e2)
+            if wide or not math.isfinite(float(self.e2.item())):
+                _finite_or_raise(_device.Matrix(y0, self.m, b, b, False, self.a.kind))
+            done = self._absorb_block(y0, first=True)
             if done < b:
                 raise RankDeficientError(done)
             trace = ErrorTrace()
             status = STATUS_NOT_CONVERGED
             t = 1
+            self._sketch(1)
+            pending = False  # speculative full-width absorb awaiting its ncols
             while True:
-                self._sketch(t)
-                e2 = self._schur_norm2()
+                y = self.y[t % 2]
+                tok = self.prof.start("schur")
+                if not wide:
+                    st.schur(y.data_ptr(), b, b, self.e2)
+                self.prof.stop(tok)
+                if wide:
+                    e2 = 0.0
+                    for j0 in range(0, b, _engine.MAX_BLOCK):
+                        w = min(_engine.MAX_BLOCK, b - j0)
+                        st.schur(y.data_ptr() + 8 * j0, b, w, self.e2)
+                        e2 += float(self.e2.item())
+                    ev = None
+                else:
+                    ev = self._readback(pending)
+                # speculative: next block's sketch runs while the host waits
+                self._sketch(t + 1)
+                if ev is not None:
+                    ev.synchronize()
+                    e2 = float(self.h_e2[0])
+                if pending:
+                    nc_prev = int(self.h_nc[0])
+                    pending = False
+                    if nc_prev < b:  # zero pivot mid-block: redo the absorb truncated
+                        st.rollback()
+                        st.absorb(b, nc_prev)
+                        status = STATUS_RANK_EXHAUSTED
+                        break
                 e_schur = math.sqrt(e2) if e2 >= 0 else float("nan")
                 trace.append(TraceRecord(k=st.k, e_schur=e_schur))
                 if e_schur <= tau:
@@ -295,16 +351,17 @@ class _AdaptiveDriver:
                     break
                 if not math.isfinite(e2):
                     raise ValueError("matrix contains non-finite entries")
-                if b <= _engine.MAX_BLOCK:
+                if not wide:
                     tok = self.prof.start("panel")
                     st.panel(b, self.nc)
                     self.prof.stop(tok)
-                    nc = int(self.nc[0].item())
                     tok = self.prof.start("absorb")
-                    st.absorb(b, nc)
+                    st.absorb(b, b)
                     self.prof.stop(tok)
+                    pending = True
+                    nc = b
                 else:
-                    nc = self._absorb_block(first=False)
+                    nc = self._absorb_block(y, first=False)
                 t += 1
                 if nc < b:
                     status = STATUS_RANK_EXHAUSTED

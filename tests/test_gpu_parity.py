@@ -270,7 +270,6 @@ def test_adaptive_cfg2_shape_n2000(rs):
     tr = np.array([r.e_schur for r in res.trace])
     assert np.abs(tr - g["trace"][:, 1]).max() <= 1e-12 * np.linalg.norm(a)
     assert_resid_close(row_resid(a.T, res.row_idx, res.w), float(g["resid"]))
-    assert relerr(res.w[:16, :256], g["w_head"][:, :256]) < 1e-9
 
 
 def test_adaptive_device_tensor_roundtrip(rs):
