@@ -83,6 +83,17 @@ def _from_tensor_2d(t, kind):
     return Matrix(t, rows, cols, cols, False, kind)
 
 
+def shape_of(a, name="matrix"):
+    """(m, n) of a matrix-like without touching the device; DimensionError if
+    it is not 2-D (mirrors `_require_2d`, skeleton.py:200-204)."""
+    if isinstance(a, Matrix):
+        return a.shape
+    shp = tuple(a.shape) if hasattr(a, "shape") else np.shape(a)
+    if len(shp) != 2:
+        raise DimensionError(f"{name} must be 2-dimensional, got shape {shp}")
+    return shp
+
+
 def as_matrix(a, name="matrix"):
     """Convert ``a`` (numpy / array_like / torch / Matrix) to an fp64 device Matrix."""
     if isinstance(a, Matrix):

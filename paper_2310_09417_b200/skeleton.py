@@ -118,10 +118,10 @@ def _finite_or_raise(y, name="matrix"):
 
 def rand_lupp(a, k, spec, rng):
     """Row skeletons by LUPP of ``a @ Omega`` (fixed rank k)."""
-    a = _device.as_matrix(a)
-    m, n = a.shape
+    m, n = _device.shape_of(a)
     _check_rank(k, m, n)
     op = make_sketch(spec.with_dims(n, k), rng)
+    a = _device.as_matrix(a)
     y = _device.Matrix(_device.sketch(a, op.omega), m, k, k, False, a.kind)
     _finite_or_raise(y)
     st, w = _factor_sketch(y, a.kind)
@@ -132,10 +132,10 @@ def rand_lupp(a, k, spec, rng):
 
 def column_id(a, k, spec, rng):
     """Column skeletons by LUPP of ``a.T @ Gamma``; ``x[:, col_idx] = I``."""
-    a = _device.as_matrix(a)
-    m, n = a.shape
+    m, n = _device.shape_of(a)
     _check_rank(k, m, n)
     op = make_sketch(spec.with_dims(m, k), rng)
+    a = _device.as_matrix(a)
     y = _device.Matrix(_device.sketch(a.T, op.omega), n, k, k, False, a.kind)
     _finite_or_raise(y)
     st, w = _factor_sketch(y, a.kind)
@@ -154,8 +154,7 @@ def rand_lupp_adaptive(a, b, tau, spec, rng, max_rank=None):
     ('not_converged'), or when a Schur block is exactly rank deficient
     ('rank_exhausted', truncated to the successful pivots).
     """
-    a = _device.as_matrix(a)
-    m, n = a.shape
+    m, n = _device.shape_of(a)
     if tau <= 0:
         raise ValueError(f"tau must be positive, got {tau}")
     if not 1 <= b <= min(m, n):
@@ -165,7 +164,7 @@ def rand_lupp_adaptive(a, b, tau, spec, rng, max_rank=None):
     max_rank = min(max_rank, min(m, n))
     if spec.kind != "gaussian":
         make_sketch(spec.with_dims(n, b), rng)  # raises NotImplementedError
-    return _AdaptiveDriver(a, b, tau, rng, max_rank).run()
+    return _AdaptiveDriver(_device.as_matrix(a), b, tau, rng, max_rank).run()
 
 
 class PhaseTimer:
