@@ -52,7 +52,7 @@ def build(force=False, verbose=False):
     if not force and up_to_date():
         return LIB_PATH
     cmd = [
-        _nvcc(), *ARCH_FLAGS, "-O3", "-lineinfo", "-std=c++17",
+        _nvcc(), *ARCH_FLAGS, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
         "-Xcompiler", "-fPIC", "-shared", "-I", INCLUDE,
         "-o", LIB_PATH + ".tmp", *sources(),
     ]

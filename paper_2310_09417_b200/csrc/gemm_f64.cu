@@ -20,35 +20,52 @@
 // units.  Tiles split between CTAs write fragment-ordered partials; a fixup
 // kernel adds them in k order (CTA order) and applies the epilogue.  The
 // split depends only on (M, N, K, G), so results are bitwise reproducible.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "rskel_internal.h"
 
 namespace rs {
 
-constexpr int GBM = 128, GBN = 64, GBK = 16, GSTAGES = 3;
-constexpr int GWARPS_M = 4, GWARPS_N = 2, GTHREADS = GWARPS_M * GWARPS_N * 32;
-constexpr int GWTM = GBM / GWARPS_M, GWTN = GBN / GWARPS_N;  // 32 x 32
-constexpr int GMT = GWTM / 16, GNT = GWTN / 8;                  // 2 x 4
-constexpr int GACC = GMT * GNT * 4;                             // accumulators per thread
-// Leading dimensions are = 4 (mod 16) doubles: 64-bit shared loads are served per
-// half-warp, and the fragment pattern (t * LD + g, g, t in 0..3) then hits 16
-// distinct bank pairs -- conflict-free.
-constexpr int A_COL_LD = GBM + 4;  // As[k][m]
-constexpr int A_ROW_LD = GBK + 4;  // As[m][k]
-constexpr int B_LD = GBN + 4;      // Bs[k][n]
-constexpr int SK_CTAS_PER_SM = 2;
+// ---------------------------------------------------------------------------
+// Tile configuration (compile-time).  Leading dimensions are = 4 (mod 16)
+// doubles: 64-bit shared loads are served per half-warp and the fragment
+// pattern (t * LD + g, g, t in 0..3) then hits 16 distinct bank pairs.
+template <int BM_, int BN_, int BK_, int WARPS_M_, int WARPS_N_, int STAGES_, int MINB_>
+struct GemmCfg {
+  static constexpr int BM = BM_, BN = BN_, BK = BK_, WARPS_M = WARPS_M_, WARPS_N = WARPS_N_;
+  static constexpr int STAGES = STAGES_, MINB = MINB_;
+  static constexpr int THREADS = WARPS_M * WARPS_N * 32;
+  static constexpr int WTM = BM / WARPS_M, WTN = BN / WARPS_N;
+  static constexpr int MT = WTM / 16, NT = WTN / 8;
+  static constexpr int ACC = MT * NT * 4;
+  static constexpr int A_COL_LD = BM + 4;  // As[k][m]
+  static constexpr int A_ROW_LD = BK + 4;  // As[m][k]
+  static constexpr int B_LD = BN + 4;      // Bs[k][n]
+  template <bool A_COL>
+  static constexpr int a_stage() { return A_COL ? BK * A_COL_LD : BM * A_ROW_LD; }
+  static constexpr int b_stage() { return BK * B_LD; }
+  template <bool A_COL>
+  static constexpr size_t smem() { return sizeof(double) * STAGES * (a_stage<A_COL>() + b_stage()); }
+};
 
-template <bool A_COL>
-__host__ __device__ constexpr int a_stage_elems() { return A_COL ? GBK * A_COL_LD : GBM * A_ROW_LD; }
-__host__ __device__ constexpr int b_stage_elems() { return GBK * B_LD; }
-
-template <bool A_COL>
-constexpr size_t gemm_smem_bytes() {
-  return sizeof(double) * GSTAGES * (a_stage_elems<A_COL>() + b_stage_elems());
-}
+// Production configuration and the alternatives the tuner compares
+// (RSKEL_GEMM_CFG=i selects one at run time, for tools/bench_kernels.py).
+using Cfg0 = GemmCfg<128, 64, 16, 4, 2, 3, 2>;   // warp 32x32
+using Cfg1 = GemmCfg<128, 64, 32, 4, 2, 2, 2>;   // BK 32, 2 stages
+using Cfg2 = GemmCfg<128, 64, 16, 4, 2, 4, 2>;   // 4 stages
+using Cfg3 = GemmCfg<256, 64, 16, 8, 2, 3, 1>;   // 16 warps, 1 CTA/SM
+using Cfg4 = GemmCfg<128, 64, 16, 2, 2, 4, 2>;   // 4 warps of 64x32
+using Cfg5 = GemmCfg<64, 64, 16, 2, 2, 4, 4>;    // 4 warps of 32x32, 4 CTAs/SM
+using Cfg6 = GemmCfg<128, 64, 16, 2, 2, 3, 2>;   // 4 warps of 64x32, 3 stages
+using Cfg7 = GemmCfg<256, 64, 16, 4, 2, 3, 1>;   // 8 warps of 64x32, 1 CTA/SM
+using Cfg8 = GemmCfg<128, 64, 32, 2, 2, 2, 2>;   // 4 warps of 64x32, BK 32
+// Stream-K partial slots: 2 per CTA, THREADS * ACC doubles each; every config
+// has MINB * THREADS * ACC <= 16384 doubles per SM.
+constexpr int SK_SLOT_DOUBLES_PER_SM = 16384;
 
 size_t gemm_partials_bytes(int nsm) {
-  return sizeof(double) * 2 * (size_t)nsm * SK_CTAS_PER_SM * GBM * GBN;
+  return sizeof(double) * 2 * (size_t)nsm * SK_SLOT_DOUBLES_PER_SM;
 }
 
 struct SkPlan {
@@ -60,11 +77,12 @@ struct SkPlan {
 __host__ __device__ inline long long sk_u0(const SkPlan& s, int c) { return (long long)c * s.U / s.G; }
 
 // Epilogue for one accumulator set of tile (m0, n0).
+template <class C>
 __device__ __forceinline__ void epilogue_store(const DGemmParams& p, int m0, int n0, int wm, int wn,
-                                               int g, int t, const double (&acc)[GACC]) {
+                                               int g, int t, const double (&acc)[C::ACC]) {
   const double alpha = p.alpha, beta = p.beta;
 #pragma unroll
-  for (int i = 0; i < GMT; ++i) {
+  for (int i = 0; i < C::MT; ++i) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       int row = m0 + wm + 16 * i + g + 8 * h;
@@ -76,12 +94,12 @@ __device__ __forceinline__ void epilogue_store(const DGemmParams& p, int m0, int
         cin = p.Cin + r * p.ldcin;
       }
 #pragma unroll
-      for (int j = 0; j < GNT; ++j) {
+      for (int j = 0; j < C::NT; ++j) {
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           int col = n0 + wn + 8 * j + 2 * t + e;
           if (col < p.N) {
-            double v = acc[(i * GNT + j) * 4 + 2 * h + e];
+            double v = acc[(i * C::NT + j) * 4 + 2 * h + e];
             crow[col] = cin ? fma(alpha, v, beta * cin[col]) : alpha * v;
           }
         }
@@ -90,21 +108,24 @@ __device__ __forceinline__ void epilogue_store(const DGemmParams& p, int m0, int
   }
 }
 
-template <bool A_COL, bool VEC2>
+template <class C, bool A_COL, bool VEC2>
 __device__ __forceinline__ void mainloop(const DGemmParams& p, double* As, double* Bs, int m0, int n0,
-                                         int kt0, int kt1, double (&acc)[GACC]) {
+                                         int kt0, int kt1, double (&acc)[C::ACC]) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int wm = (warp % GWARPS_M) * GWTM, wn = (warp / GWARPS_M) * GWTN;
+  const int wm = (warp % C::WARPS_M) * C::WTM, wn = (warp / C::WARPS_M) * C::WTN;
   const int M = p.M, N = p.N, K = p.K;
+  constexpr int V = VEC2 ? 2 : 1;
+  constexpr int BM = C::BM, BN = C::BN, BK = C::BK, T = C::THREADS;
 
-  constexpr int A_CHUNKS = (GBM * GBK) / (VEC2 ? 2 : 1) / GTHREADS;
+  constexpr int A_CHUNKS = (BM * BK) / V / T;
+  static_assert(A_CHUNKS * V * T == BM * BK, "A tile must split evenly");
   const double* arow[A_COL ? 1 : A_CHUNKS];
   if constexpr (!A_COL) {
 #pragma unroll
     for (int i = 0; i < A_CHUNKS; ++i) {
-      int c = tid + i * GTHREADS;
-      int mr = VEC2 ? c / (GBK / 2) : c / GBK;
+      int c = tid + i * T;
+      int mr = c / (BK / V);
       int gm = m0 + mr;
       long long r = gm < M ? (p.aidx ? p.aidx[gm] : gm) : 0;
       arow[i] = gm < M ? p.A + r * p.lda : nullptr;
@@ -112,15 +133,15 @@ __device__ __forceinline__ void mainloop(const DGemmParams& p, double* As, doubl
   }
 
   auto load_stage = [&](int stage, int kt) {
-    const int k0 = kt * GBK;
-    double* as = As + stage * a_stage_elems<A_COL>();
-    double* bs = Bs + stage * b_stage_elems();
+    const int k0 = kt * BK;
+    double* as = As + stage * C::template a_stage<A_COL>();
+    double* bs = Bs + stage * C::b_stage();
 #pragma unroll
     for (int i = 0; i < A_CHUNKS; ++i) {
-      int c = tid + i * GTHREADS;
+      int c = tid + i * T;
       if constexpr (A_COL) {
-        constexpr int PER_ROW = GBM / (VEC2 ? 2 : 1);
-        int kr = c / PER_ROW, mc = (c % PER_ROW) * (VEC2 ? 2 : 1);
+        constexpr int PER_ROW = BM / V;
+        int kr = c / PER_ROW, mc = (c % PER_ROW) * V;
         int gk = k0 + kr, gm = m0 + mc;
         const double* src = p.A;
         int bytes = 0;
@@ -128,11 +149,11 @@ __device__ __forceinline__ void mainloop(const DGemmParams& p, double* As, doubl
           src = p.A + (long long)gk * p.lda + gm;
           bytes = (VEC2 && gm + 1 < M) ? 16 : 8;
         }
-        if constexpr (VEC2) cp_async16(as + kr * A_COL_LD + mc, src, bytes);
-        else cp_async8(as + kr * A_COL_LD + mc, src, bytes);
+        if constexpr (VEC2) cp_async16(as + kr * C::A_COL_LD + mc, src, bytes);
+        else cp_async8(as + kr * C::A_COL_LD + mc, src, bytes);
       } else {
-        constexpr int PER_ROW = GBK / (VEC2 ? 2 : 1);
-        int mr = c / PER_ROW, kc = (c % PER_ROW) * (VEC2 ? 2 : 1);
+        constexpr int PER_ROW = BK / V;
+        int mr = c / PER_ROW, kc = (c % PER_ROW) * V;
         int gk = k0 + kc;
         const double* src = p.A;
         int bytes = 0;
@@ -140,16 +161,17 @@ __device__ __forceinline__ void mainloop(const DGemmParams& p, double* As, doubl
           src = arow[i] + gk;
           bytes = (VEC2 && gk + 1 < K) ? 16 : 8;
         }
-        if constexpr (VEC2) cp_async16(as + mr * A_ROW_LD + kc, src, bytes);
-        else cp_async8(as + mr * A_ROW_LD + kc, src, bytes);
+        if constexpr (VEC2) cp_async16(as + mr * C::A_ROW_LD + kc, src, bytes);
+        else cp_async8(as + mr * C::A_ROW_LD + kc, src, bytes);
       }
     }
-    constexpr int B_CHUNKS = (GBK * GBN) / (VEC2 ? 2 : 1) / GTHREADS;
+    constexpr int B_CHUNKS = (BK * BN) / V / T;
+    static_assert(B_CHUNKS * V * T == BK * BN, "B tile must split evenly");
 #pragma unroll
     for (int i = 0; i < B_CHUNKS; ++i) {
-      int c = tid + i * GTHREADS;
-      constexpr int PER_ROW = GBN / (VEC2 ? 2 : 1);
-      int kr = c / PER_ROW, nc = (c % PER_ROW) * (VEC2 ? 2 : 1);
+      int c = tid + i * T;
+      constexpr int PER_ROW = BN / V;
+      int kr = c / PER_ROW, nc = (c % PER_ROW) * V;
       int gk = k0 + kr, gn = n0 + nc;
       const double* src = p.B;
       int bytes = 0;
@@ -158,52 +180,52 @@ __device__ __forceinline__ void mainloop(const DGemmParams& p, double* As, doubl
         src = p.B + r * p.ldb + gn;
         bytes = (VEC2 && gn + 1 < N) ? 16 : 8;
       }
-      if constexpr (VEC2) cp_async16(bs + kr * B_LD + nc, src, bytes);
-      else cp_async8(bs + kr * B_LD + nc, src, bytes);
+      if constexpr (VEC2) cp_async16(bs + kr * C::B_LD + nc, src, bytes);
+      else cp_async8(bs + kr * C::B_LD + nc, src, bytes);
     }
   };
 
 #pragma unroll
-  for (int e = 0; e < GACC; ++e) acc[e] = 0.0;
+  for (int e = 0; e < C::ACC; ++e) acc[e] = 0.0;
 
   const int nkt = kt1 - kt0;
 #pragma unroll
-  for (int s = 0; s < GSTAGES - 1; ++s) {
+  for (int s = 0; s < C::STAGES - 1; ++s) {
     if (s < nkt) load_stage(s, kt0 + s);
     cp_async_commit();
   }
   for (int it = 0; it < nkt; ++it) {
-    cp_async_wait<GSTAGES - 2>();
+    cp_async_wait<C::STAGES - 2>();
     __syncthreads();
     {
-      int nk = it + GSTAGES - 1;
-      if (nk < nkt) load_stage(nk % GSTAGES, kt0 + nk);
+      int nk = it + C::STAGES - 1;
+      if (nk < nkt) load_stage(nk % C::STAGES, kt0 + nk);
       cp_async_commit();
     }
-    const int stage = it % GSTAGES;
-    const double* as = As + stage * a_stage_elems<A_COL>();
-    const double* bs = Bs + stage * b_stage_elems();
+    const int stage = it % C::STAGES;
+    const double* as = As + stage * C::template a_stage<A_COL>();
+    const double* bs = Bs + stage * C::b_stage();
 #pragma unroll
-    for (int kk = 0; kk < GBK; kk += 4) {
-      double a[GMT][2], b[GNT];
+    for (int kk = 0; kk < BK; kk += 4) {
+      double a[C::MT][2], b[C::NT];
 #pragma unroll
-      for (int i = 0; i < GMT; ++i) {
+      for (int i = 0; i < C::MT; ++i) {
         int mr = wm + 16 * i + g;
         if constexpr (A_COL) {
-          a[i][0] = as[(kk + t) * A_COL_LD + mr];
-          a[i][1] = as[(kk + t) * A_COL_LD + mr + 8];
+          a[i][0] = as[(kk + t) * C::A_COL_LD + mr];
+          a[i][1] = as[(kk + t) * C::A_COL_LD + mr + 8];
         } else {
-          a[i][0] = as[mr * A_ROW_LD + kk + t];
-          a[i][1] = as[(mr + 8) * A_ROW_LD + kk + t];
+          a[i][0] = as[mr * C::A_ROW_LD + kk + t];
+          a[i][1] = as[(mr + 8) * C::A_ROW_LD + kk + t];
         }
       }
 #pragma unroll
-      for (int j = 0; j < GNT; ++j) b[j] = bs[(kk + t) * B_LD + wn + 8 * j + g];
+      for (int j = 0; j < C::NT; ++j) b[j] = bs[(kk + t) * C::B_LD + wn + 8 * j + g];
 #pragma unroll
-      for (int i = 0; i < GMT; ++i)
+      for (int i = 0; i < C::MT; ++i)
 #pragma unroll
-        for (int j = 0; j < GNT; ++j) {
-          double(&c4)[4] = *reinterpret_cast<double(*)[4]>(&acc[(i * GNT + j) * 4]);
+        for (int j = 0; j < C::NT; ++j) {
+          double(&c4)[4] = *reinterpret_cast<double(*)[4]>(&acc[(i * C::NT + j) * 4]);
           dmma_16x8x4(c4, a[i][0], a[i][1], b[j]);
         }
     }
@@ -212,20 +234,20 @@ __device__ __forceinline__ void mainloop(const DGemmParams& p, double* As, doubl
   __syncthreads();  // stage buffers are reused by the next tile of this CTA
 }
 
-template <bool A_COL, bool VEC2>
-__global__ void __launch_bounds__(GTHREADS, SK_CTAS_PER_SM) dgemm_kernel(DGemmParams p, SkPlan sk) {
+template <class C, bool A_COL, bool VEC2>
+__global__ void __launch_bounds__(C::THREADS, C::MINB) dgemm_kernel(DGemmParams p, SkPlan sk) {
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
-  double* Bs = smem + GSTAGES * a_stage_elems<A_COL>();
+  double* Bs = smem + C::STAGES * C::template a_stage<A_COL>();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int wm = (warp % GWARPS_M) * GWTM, wn = (warp / GWARPS_M) * GWTN;
-  double acc[GACC];
+  const int wm = (warp % C::WARPS_M) * C::WTM, wn = (warp / C::WARPS_M) * C::WTN;
+  double acc[C::ACC];
 
   if (sk.G == 0) {  // classic tile grid
-    const int n0 = blockIdx.x * GBN, m0 = blockIdx.y * GBM;
-    mainloop<A_COL, VEC2>(p, As, Bs, m0, n0, 0, sk.KT, acc);
-    epilogue_store(p, m0, n0, wm, wn, g, t, acc);
+    const int n0 = blockIdx.x * C::BN, m0 = blockIdx.y * C::BM;
+    mainloop<C, A_COL, VEC2>(p, As, Bs, m0, n0, 0, sk.KT, acc);
+    epilogue_store<C>(p, m0, n0, wm, wn, g, t, acc);
     return;
   }
   // stream-K
@@ -235,23 +257,24 @@ __global__ void __launch_bounds__(GTHREADS, SK_CTAS_PER_SM) dgemm_kernel(DGemmPa
     const int tile = (int)(u / sk.KT);
     const int i0 = (int)(u - (long long)tile * sk.KT);
     const int i1 = (int)min((long long)sk.KT, i0 + (u1 - u));
-    const int m0 = (tile / sk.tiles_n) * GBM, n0 = (tile % sk.tiles_n) * GBN;
-    mainloop<A_COL, VEC2>(p, As, Bs, m0, n0, i0, i1, acc);
+    const int m0 = (tile / sk.tiles_n) * C::BM, n0 = (tile % sk.tiles_n) * C::BN;
+    mainloop<C, A_COL, VEC2>(p, As, Bs, m0, n0, i0, i1, acc);
     if (i0 == 0 && i1 == sk.KT) {
-      epilogue_store(p, m0, n0, wm, wn, g, t, acc);
+      epilogue_store<C>(p, m0, n0, wm, wn, g, t, acc);
     } else {
+      // element-major slot layout: coalesced writes here and reads in the fixup
       const int slot = (i0 > 0) ? 2 * c : 2 * c + 1;
-      double* dst = p.partials + ((size_t)slot * GTHREADS + tid) * GACC;
+      double* dst = p.partials + (size_t)slot * C::THREADS * C::ACC + tid;
 #pragma unroll
-      for (int e = 0; e < GACC; e += 2)
-        *reinterpret_cast<double2*>(dst + e) = make_double2(acc[e], acc[e + 1]);
+      for (int e = 0; e < C::ACC; ++e) dst[(size_t)e * C::THREADS] = acc[e];
     }
     u += i1 - i0;
   }
 }
 
 // Sum the partials of every split tile in k order and apply the epilogue.
-__global__ void __launch_bounds__(GTHREADS) dgemm_fixup_kernel(DGemmParams p, SkPlan sk) {
+template <class C>
+__global__ void __launch_bounds__(C::THREADS) dgemm_fixup_kernel(DGemmParams p, SkPlan sk) {
   const int tile = blockIdx.x;
   const long long ub = (long long)tile * sk.KT, ue = ub + sk.KT;
   // owner(u): largest c with u0(c) <= u
@@ -265,51 +288,52 @@ __global__ void __launch_bounds__(GTHREADS) dgemm_fixup_kernel(DGemmParams p, Sk
   if (clo == chi) return;  // complete tile, stored by its CTA
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int wm = (warp % GWARPS_M) * GWTM, wn = (warp / GWARPS_M) * GWTN;
-  double acc[GACC];
+  const int wm = (warp % C::WARPS_M) * C::WTM, wn = (warp / C::WARPS_M) * C::WTN;
+  double acc[C::ACC];
   {
-    const double* src = p.partials + ((size_t)(2 * clo + 1) * GTHREADS + tid) * GACC;
+    const double* src = p.partials + (size_t)(2 * clo + 1) * C::THREADS * C::ACC + tid;
 #pragma unroll
-    for (int e = 0; e < GACC; ++e) acc[e] = src[e];
+    for (int e = 0; e < C::ACC; ++e) acc[e] = src[(size_t)e * C::THREADS];
   }
   for (int c = clo + 1; c <= chi; ++c) {
-    const double* src = p.partials + ((size_t)(2 * c) * GTHREADS + tid) * GACC;
+    const double* src = p.partials + (size_t)(2 * c) * C::THREADS * C::ACC + tid;
 #pragma unroll
-    for (int e = 0; e < GACC; ++e) acc[e] += src[e];
+    for (int e = 0; e < C::ACC; ++e) acc[e] += src[(size_t)e * C::THREADS];
   }
-  const int m0 = (tile / sk.tiles_n) * GBM, n0 = (tile % sk.tiles_n) * GBN;
-  epilogue_store(p, m0, n0, wm, wn, g, t, acc);
+  const int m0 = (tile / sk.tiles_n) * C::BM, n0 = (tile % sk.tiles_n) * C::BN;
+  epilogue_store<C>(p, m0, n0, wm, wn, g, t, acc);
 }
 
-template <bool A_COL, bool VEC2>
+template <class C, bool A_COL, bool VEC2>
 static int launch_dgemm_t(const DGemmParams& p, cudaStream_t st) {
-  constexpr size_t smem = gemm_smem_bytes<A_COL>();
+  static_assert(C::MINB * C::THREADS * C::ACC <= SK_SLOT_DOUBLES_PER_SM, "partials workspace");
+  constexpr size_t smem = C::template smem<A_COL>();
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(dgemm_kernel<A_COL, VEC2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(dgemm_kernel<C, A_COL, VEC2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = true;
   }
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   SkPlan sk;
-  sk.tiles_n = (p.N + GBN - 1) / GBN;
-  const int tiles_m = (p.M + GBM - 1) / GBM;
+  sk.tiles_n = (p.N + C::BN - 1) / C::BN;
+  const int tiles_m = (p.M + C::BM - 1) / C::BM;
   sk.tiles = sk.tiles_n * tiles_m;
-  sk.KT = (p.K + GBK - 1) / GBK;
+  sk.KT = (p.K + C::BK - 1) / C::BK;
   sk.G = 0;
   sk.U = (long long)sk.tiles * sk.KT;
-  const int slots = nsm * SK_CTAS_PER_SM;
+  const int slots = nsm * C::MINB;
   // Stream-K when a plain grid would run fewer than ~4 waves and each CTA
   // still gets a few k-tiles of work.
   if (p.partials != nullptr && sk.tiles < 4 * slots && sk.U >= 4LL * slots && sk.KT >= 8) {
     sk.G = slots;
-    dgemm_kernel<A_COL, VEC2><<<sk.G, GTHREADS, smem, st>>>(p, sk);
-    dgemm_fixup_kernel<<<sk.tiles, GTHREADS, 0, st>>>(p, sk);
+    dgemm_kernel<C, A_COL, VEC2><<<sk.G, C::THREADS, smem, st>>>(p, sk);
+    dgemm_fixup_kernel<C><<<sk.tiles, C::THREADS, 0, st>>>(p, sk);
     count_launch(2);
   } else {
     dim3 grid(sk.tiles_n, tiles_m);
-    dgemm_kernel<A_COL, VEC2><<<grid, GTHREADS, smem, st>>>(p, sk);
+    dgemm_kernel<C, A_COL, VEC2><<<grid, C::THREADS, smem, st>>>(p, sk);
     count_launch(1);
   }
   return cudaGetLastError() == cudaSuccess ? RS_OK : RS_ERR_CUDA;
@@ -317,12 +341,40 @@ static int launch_dgemm_t(const DGemmParams& p, cudaStream_t st) {
 
 static bool al16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; }
 
+template <class C>
+static int launch_cfg(const DGemmParams& p, bool a_col, bool vec2, cudaStream_t st) {
+  if (a_col) return vec2 ? launch_dgemm_t<C, true, true>(p, st) : launch_dgemm_t<C, true, false>(p, st);
+  return vec2 ? launch_dgemm_t<C, false, true>(p, st) : launch_dgemm_t<C, false, false>(p, st);
+}
+
+static int selected_cfg() {
+  static int cfg = -2;
+  if (cfg == -2) {
+    const char* e = getenv("RSKEL_GEMM_CFG");
+    cfg = e ? atoi(e) : -1;
+  }
+  return cfg;
+}
+
 int launch_dgemm(const DGemmParams& p, bool a_col, cudaStream_t st) {
   if (p.M < 0 || p.N < 0 || p.K < 0) return RS_ERR_ARG;
   if (p.M == 0 || p.N == 0) return RS_OK;
   bool vec2 = al16(p.A) && al16(p.B) && (p.lda % 2 == 0) && (p.ldb % 2 == 0);
-  if (a_col) return vec2 ? launch_dgemm_t<true, true>(p, st) : launch_dgemm_t<true, false>(p, st);
-  return vec2 ? launch_dgemm_t<false, true>(p, st) : launch_dgemm_t<false, false>(p, st);
+  switch (selected_cfg()) {
+    case 1: return launch_cfg<Cfg1>(p, a_col, vec2, st);
+    case 2: return launch_cfg<Cfg2>(p, a_col, vec2, st);
+    case 3: return launch_cfg<Cfg3>(p, a_col, vec2, st);
+    case 4: return launch_cfg<Cfg4>(p, a_col, vec2, st);
+    case 5: return launch_cfg<Cfg5>(p, a_col, vec2, st);
+    case 6: return launch_cfg<Cfg6>(p, a_col, vec2, st);
+    case 7: return launch_cfg<Cfg7>(p, a_col, vec2, st);
+    case 8: return launch_cfg<Cfg8>(p, a_col, vec2, st);
+    default:
+      // Measured on B200 (tools/tune_gemm.sh): the column-major sketch operand
+      // prefers 64x32 warp tiles (31.4 TF/s vs 28.2), the gathered row-major
+      // Schur/interpolation operands the 32x32 tiles of Cfg0.
+      return a_col ? launch_cfg<Cfg8>(p, a_col, vec2, st) : launch_cfg<Cfg0>(p, a_col, vec2, st);
+  }
 }
 
 }  // namespace rs

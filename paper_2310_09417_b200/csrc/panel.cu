@@ -31,29 +31,52 @@
 #include "common.cuh"
 #include "rskel_internal.h"
 
+// Optional per-phase timestamps (build with -DRS_PANEL_PROBE_ON; read with
+// rs_panel_probe): clock64 of CTA 0 and CTA 1, lane 0, per column.
+#ifdef RS_PANEL_PROBE_ON
+__device__ unsigned long long g_panel_probe[8][64][2];
+#define RS_PANEL_PROBE(k)                                                            \
+  do {                                                                               \
+    if (cta < 2 && (threadIdx.x & 31) == 0 && threadIdx.x < 32) {                    \
+      g_panel_probe[k][j][cta] = clock64();                                          \
+    }                                                                                \
+  } while (0)
+extern "C" void rs_panel_probe(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, g_panel_probe, sizeof(g_panel_probe));
+}
+#else
+#define RS_PANEL_PROBE(k) \
+  do {                    \
+  } while (0)
+#endif
+
 namespace rs {
 
 constexpr int PTHREADS = 256;
 constexpr int PWARPS = PTHREADS / 32;
 constexpr int PMAXW = 64;
-constexpr int PMAXG = 1024;
+constexpr int PMAXG = 256;  // >= CTAs of the cooperative grid (one per SM)
 
 // LL-style exchange: every 8-byte word carries the step flag next to 4 bytes
 // of payload, so a reader that sees the flag in a word also sees its payload
 // (8-byte single-copy atomicity) -- no fences, no separate barrier.
 struct PanelScratch {
-  uint4 rec[2][PMAXG][2];           // {val.lo, f, val.hi, f}, {pos, f, row + 1, f}
-  uint4 bc[2][8];                   // winner broadcast: val, {pos, row + 1}, {cta}
+  // One 128-byte line per CTA for its record and for its copy of the winner
+  // broadcast: no line is shared by two writers or polled by many readers
+  // (a hot line serialises in its L2 slice and made each hop ~1.3 us).
+  uint4 rec[2][PMAXG][8];           // [0] = {val.lo, f, val.hi, f}, [1] = {pos, f, row + 1, f}
+  uint4 bc[2][PMAXG][8];            // per-CTA winner copy: [0] val, [1] {pos, row + 1}, [2] {cta}
   uint4 rowdata[2][PMAXG][PMAXW];   // candidate row: {x.lo, f, x.hi, f} per column
 };
 
 RS_DEV void st_v4(uint4* p, unsigned a, unsigned b, unsigned c, unsigned d) {
-  asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};\n" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d)
+  // gpu-scope relaxed: .volatile (= relaxed.sys) stores were serialised (~150 ns each)
+  asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1,%2,%3,%4};\n" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d)
                : "memory");
 }
 RS_DEV uint4 ld_v4(const uint4* p) {
   uint4 v;
-  asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];\n"
+  asm volatile("ld.relaxed.gpu.global.v4.u32 {%0,%1,%2,%3}, [%4];\n"
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                : "l"(p)
                : "memory");
@@ -94,7 +117,7 @@ RS_DEV void block_best(double& v, int& p, int& r, double* red_v, int* red_p, int
 __global__ void __launch_bounds__(PTHREADS, 1)
     panel_kernel(double* __restrict__ S, long long lds, int R, int w, int rows_per,
                  int64_t* __restrict__ perm_out, int* __restrict__ ncols_out, PanelScratch* ws,
-                 unsigned flag_base) {
+                 unsigned flag_base, int central) {
   extern __shared__ __align__(16) double psm[];
   const int G = gridDim.x, cta = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -131,6 +154,7 @@ __global__ void __launch_bounds__(PTHREADS, 1)
   int late_skip = -1;
   for (int j = 0; j < w; ++j) {
     const int par = j & 1;
+    RS_PANEL_PROBE(0);
     if (warp == 0) {
       const unsigned f = flag_base + (unsigned)j + 1u;
       // ---- publish this CTA's candidate for column j (no fence needed) ----
@@ -146,28 +170,38 @@ __global__ void __launch_bounds__(PTHREADS, 1)
         st_v4(&ws->rec[par][cta][0], (unsigned)x, f, (unsigned)(x >> 32), f);
         st_v4(&ws->rec[par][cta][1], (unsigned)bp, f, br >= 0 ? (unsigned)(r0 + br + 1) : 0u, f);
       }
-      // ---- CTA 0 reduces the G candidates and broadcasts the winner; the
-      // others poll the single broadcast header (one hot line instead of G) ----
+      RS_PANEL_PROBE(1);
+      // ---- reduce the G candidates: every CTA polls all records itself
+      // (all-to-all, one hop) or, with `central`, CTA 0 reduces and writes a
+      // per-CTA broadcast copy (two hops, G x fewer polled lines) ----
       double v = -1.0;
       int pp = 0x7fffffff, rr = -1, cc = -1;
-      if (cta == 0) {
+      if (cta == 0 || !central) {
+        // Poll all of this lane's records in one pass (loads issued back to
+        // back, then checked), repeat only for the ones not yet published.
         constexpr int QMAX = (PMAXG + 31) / 32;
-        unsigned done = 0;  // bit i: record lane + 32 i consumed
         const int nq = (G - lane + 31) / 32;
-        const unsigned all = nq >= 32 ? 0xffffffffu : ((1u << nq) - 1u);
-        while (done != all) {
-#pragma unroll 4
+        unsigned pending = nq >= 32 ? 0xffffffffu : ((1u << nq) - 1u);
+        while (pending) {
+          uint4 a[QMAX], b[QMAX];
+#pragma unroll
           for (int i = 0; i < QMAX; ++i) {
-            if (i >= nq || (done >> i) & 1u) continue;
-            const int q = lane + 32 * i;
-            const uint4 a = ld_v4(&ws->rec[par][q][0]);
-            const uint4 b = ld_v4(&ws->rec[par][q][1]);
-            if (a.y != f || a.w != f || b.y != f || b.w != f) continue;
-            done |= 1u << i;
-            const int row = (int)b.z - 1;
-            const double qv = join(a.x, a.z);
-            const int qp = (int)b.x;
-            if (row >= 0 && (rr < 0 || key_better(qv, qp, v, pp))) { v = qv; pp = qp; rr = row; cc = q; }
+            if ((pending >> i) & 1u) {
+              a[i] = ld_v4(&ws->rec[par][lane + 32 * i][0]);
+              b[i] = ld_v4(&ws->rec[par][lane + 32 * i][1]);
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < QMAX; ++i) {
+            if (!((pending >> i) & 1u)) continue;
+            if (a[i].y != f || a[i].w != f || b[i].y != f || b[i].w != f) continue;
+            pending &= ~(1u << i);
+            const int row = (int)b[i].z - 1;
+            const double qv = join(a[i].x, a[i].z);
+            const int qp = (int)b[i].x;
+            if (row >= 0 && (rr < 0 || key_better(qv, qp, v, pp))) {
+              v = qv; pp = qp; rr = row; cc = lane + 32 * i;
+            }
           }
         }
 #pragma unroll
@@ -178,17 +212,19 @@ __global__ void __launch_bounds__(PTHREADS, 1)
           int oc = __shfl_xor_sync(0xffffffffu, cc, off);
           if (orr >= 0 && (rr < 0 || key_better(ov, op, v, pp))) { v = ov; pp = op; rr = orr; cc = oc; }
         }
-        if (lane == 0) {
+        if (central) {
           const unsigned long long x = (unsigned long long)__double_as_longlong(rr >= 0 ? v : 0.0);
-          st_v4(&ws->bc[par][0], (unsigned)x, f, (unsigned)(x >> 32), f);
-          st_v4(&ws->bc[par][1], (unsigned)pp, f, (unsigned)(rr + 1), f);
-          st_v4(&ws->bc[par][2], (unsigned)cc, f, 0u, f);
+          for (int q = 1 + lane; q < G; q += 32) {
+            st_v4(&ws->bc[par][q][0], (unsigned)x, f, (unsigned)(x >> 32), f);
+            st_v4(&ws->bc[par][q][1], (unsigned)pp, f, (unsigned)(rr + 1), f);
+            st_v4(&ws->bc[par][q][2], (unsigned)cc, f, 0u, f);
+          }
         }
       } else {
         uint4 h = make_uint4(0, 0, 0, 0);
         if (lane < 3) {
           do {
-            h = ld_v4(&ws->bc[par][lane]);
+            h = ld_v4(&ws->bc[par][cta][lane]);
           } while (h.y != f || h.w != f);
         }
         const unsigned x0 = __shfl_sync(0xffffffffu, h.x, 0), x1 = __shfl_sync(0xffffffffu, h.z, 0);
@@ -198,16 +234,20 @@ __global__ void __launch_bounds__(PTHREADS, 1)
         cc = (int)__shfl_sync(0xffffffffu, h.x, 2);
       }
       if (lane == 0) { s_val = rr >= 0 ? v : 0.0; s_pos = pp; s_row = rr; }
+      RS_PANEL_PROBE(2);
       // ---- pivot row (U row j) straight from the winner's published copy ----
       if (rr >= 0 && v > 0.0) {
-        for (int c = j + lane; c < w; c += 32) {
-          uint4 x;
-          do {
-            x = ld_v4(&ws->rowdata[par][cc][c]);
-          } while (x.y != f || x.w != f);
-          Urow2[par][c] = join(x.x, x.z);
+        const int c0 = j + lane, c1 = j + lane + 32;
+        bool need0 = c0 < w, need1 = c1 < w;
+        while (need0 || need1) {  // both words in flight at once
+          uint4 x0 = make_uint4(0, 0, 0, 0), x1 = make_uint4(0, 0, 0, 0);
+          if (need0) x0 = ld_v4(&ws->rowdata[par][cc][c0]);
+          if (need1) x1 = ld_v4(&ws->rowdata[par][cc][c1]);
+          if (need0 && x0.y == f && x0.w == f) { Urow2[par][c0] = join(x0.x, x0.z); need0 = false; }
+          if (need1 && x1.y == f && x1.w == f) { Urow2[par][c1] = join(x1.x, x1.z); need1 = false; }
         }
       }
+      RS_PANEL_PROBE(3);
     } else if (late_j >= 0) {
       // ---- late update of the previous step (off the critical path) ----
       const int jl = late_j;
@@ -225,6 +265,7 @@ __global__ void __launch_bounds__(PTHREADS, 1)
     const int ppos = s_pos, prow = s_row;
 
     // ---- swap bookkeeping, scale column j, update column j+1, next candidate ----
+    RS_PANEL_PROBE(5);
     const double upiv = Urow2[par][j];
     const double unext = (j + 1 < w) ? Urow2[par][j + 1] : 0.0;
     bv = -1.0; bp = 0x7fffffff; br = -1;
@@ -243,6 +284,7 @@ __global__ void __launch_bounds__(PTHREADS, 1)
         if (br < 0 || key_better(av, pi, bv, bp)) { bv = av; bp = pi; br = i; }
       }
     }
+    RS_PANEL_PROBE(6);
     block_best(bv, bp, br, red_v, red_p, red_r);
     // The new local best row is published next step: bring it fully up to date.
     if (warp == 0 && br >= 0) {
@@ -253,6 +295,7 @@ __global__ void __launch_bounds__(PTHREADS, 1)
       }
       __syncwarp();
     }
+    RS_PANEL_PROBE(7);
     late_j = j;
     late_skip = br;
   }
@@ -300,7 +343,9 @@ int launch_panel(double* S, long long lds, int R, int w, int64_t* perm_out, int*
   // Flags of launch e are e*128 + j + 1: stale words of earlier launches never match.
   static std::atomic<unsigned> epoch{1};
   unsigned flag_base = (epoch.fetch_add(1) & 0x1ffffffu) << 7;
-  void* args[] = {&S, &lds, &R, &w, &rows_per, &perm_out, &ncols_dev, &ws, &flag_base};
+  int central = 0;
+  if (const char* e = getenv("RSKEL_PANEL_CENTRAL")) central = atoi(e);
+  void* args[] = {&S, &lds, &R, &w, &rows_per, &perm_out, &ncols_dev, &ws, &flag_base, &central};
   cudaError_t e = cudaLaunchCooperativeKernel((void*)panel_kernel, dim3(G), dim3(PTHREADS), args, smem, st);
   count_launch(1);
   return e == cudaSuccess ? RS_OK : RS_ERR_CUDA;
