@@ -4,26 +4,72 @@
 //   C[i, :] = Cin[cidx[i], :] - A[i, :K] * B[bidx[0..K), :]      (K <= 64)
 //
 // with C = T_new[:, :k] (M = m-k-nc rows, N = k columns), A = W_hat, B = the
-// pivot rows T[P_hat] and Cin = T[Q_hat].  The shape is short-K / huge-MN, so
-// the kernel is organised around the output stream rather than a k-pipeline:
-//  * persistent CTAs (2 per SM) walk contiguous chunks of 64 x 64 tiles, so
-//    the 64 x 64 A strip stays resident in shared memory across a row strip;
-//  * the B tile of the next tile is prefetched with cp.async (double buffer);
-//  * the Cin tile is prefetched straight into registers at the top of the
-//    tile (read-only path), so its HBM latency hides behind the 16 DMMA
-//    k-steps, and C is written with 16-byte stores.
-// Per tile: 64x64x64 FMAs, 32 KB of Cin read and 32 KB of C written.
+// pivot rows T[P_hat] and Cin = T[Q_hat].  Short K, huge M x N: the kernel is
+// a streaming pipeline, not a k-loop.
+//
+// Warp-specialised persistent design (one CTA per SM):
+//  * 1 producer warp issues 1-D bulk async copies (cp.async.bulk, the TMA
+//    engine's non-tensor form) of whole gathered rows -- the K B rows and the
+//    64 Cin rows of a 64 x 32 output tile, and the 64 x K A strip -- into a
+//    4-stage shared-memory ring, completion tracked by mbarrier transaction
+//    counts (no per-thread address math or cp.async groups);
+//  * 8 consumer warps (warp tile 16 x 16, DMMA m16n8k4) wait on the stage's
+//    full barrier, run the 16 k-steps, write C = Cin - A B with 16-byte
+//    stores straight from registers, and release the stage.
+// Rows are placed at padded strides (68 / 36 doubles, = 4 mod 16) so the
+// 64-bit fragment loads are bank-conflict free.  A generic cp.async kernel
+// (rank_update_kernel) remains for shapes the bulk path cannot take
+// (odd K, N or leading dimensions, misaligned pointers).
 #include "common.cuh"
 #include "rskel_internal.h"
 
 namespace rs {
 
-constexpr int UBM = 64, UBN = 64, UK = 64;
-constexpr int UTHREADS = 256;                       // 8 warps: 2 (M) x 4 (N), warp tile 32 x 16
-constexpr int UWM = 2, UWN = 4, UWTM = UBM / UWM, UWTN = UBN / UWN;
-constexpr int UMT = UWTM / 16, UNT = UWTN / 8;      // 2 x 2 m16n8 tiles per warp
-constexpr int UA_LD = UK + 4, UB_LD = UBN + 4;  // = 4 (mod 16): conflict-free 64-bit fragment loads
-constexpr size_t U_SMEM = sizeof(double) * (UBM * UA_LD + 2 * UK * UB_LD);
+// ------------------------------------------------------------ mbarrier/bulk --
+RS_DEV unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+RS_DEV void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+RS_DEV void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+RS_DEV void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+RS_DEV void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+RS_DEV void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// ------------------------------------------------------------- bulk kernel --
+#ifndef RS_RU_WBN
+#define RS_RU_WBN 64
+#endif
+#ifndef RS_RU_STAGES
+#define RS_RU_STAGES 2
+#endif
+constexpr int WBM = 64, WBN = RS_RU_WBN, WK = 64, WSTAGES = RS_RU_STAGES;
+constexpr int W_CONSUMERS = 8;                         // warps 0..7: 4 (M) x 2 (N), warp tile 16 x WBN/2
+constexpr int WNT = WBN / 16;                          // n8 tiles per warp
+constexpr int W_THREADS = (W_CONSUMERS + 1) * 32;      // + producer warp 8
+constexpr int WA_LD = WK + 4, WB_LD = WBN + 4, WC_LD = WBN + 4;  // = 4 (mod 16)
+constexpr int WA_ELEMS = WBM * WA_LD;
+constexpr int WB_ELEMS = WK * WB_LD, WC_ELEMS = WBM * WC_LD;
+constexpr int WSTAGE_ELEMS = WB_ELEMS + WC_ELEMS;
+constexpr size_t W_SMEM = sizeof(double) * (2 * WA_ELEMS + WSTAGES * WSTAGE_ELEMS) + 1024;
 
 struct RankUpdateParams {
   int M, N, K;
@@ -40,9 +86,152 @@ struct RankUpdateParams {
   int tiles_n, tiles;
 };
 
+__global__ void __launch_bounds__(W_THREADS, 1) rank_update_bulk_kernel(RankUpdateParams p) {
+  extern __shared__ __align__(128) double wsm[];
+  double* Abuf = wsm;                              // [2][WBM][WA_LD]
+  double* Sbuf = wsm + 2 * WA_ELEMS;               // [WSTAGES][B | C]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(Sbuf + WSTAGES * WSTAGE_ELEMS);
+  uint64_t* full = bars;                           // [WSTAGES]
+  uint64_t* empty = bars + WSTAGES;                // [WSTAGES]
+  uint64_t* a_full = bars + 2 * WSTAGES;           // [2]
+  uint64_t* a_empty = bars + 2 * WSTAGES + 2;      // [2]
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int G = gridDim.x, c = blockIdx.x;
+  const int t0 = (int)((long long)c * p.tiles / G), t1 = (int)((long long)(c + 1) * p.tiles / G);
+
+  // Zero the K padding of A and B once (the producer only writes columns /
+  // rows < K), then initialise the barriers.
+  for (int e = tid; e < 2 * WBM * (WA_LD - p.K); e += W_THREADS) {
+    const int r = e / (WA_LD - p.K), cc = p.K + e % (WA_LD - p.K);
+    Abuf[(r / WBM) * WA_ELEMS + (r % WBM) * WA_LD + cc] = 0.0;
+  }
+  for (int e = tid; e < WSTAGES * (WK - p.K) * WB_LD; e += W_THREADS) {
+    const int s = e / ((WK - p.K) * WB_LD), rem = e % ((WK - p.K) * WB_LD);
+    Sbuf[s * WSTAGE_ELEMS + (p.K + rem / WB_LD) * WB_LD + rem % WB_LD] = 0.0;
+  }
+  if (tid == 0) {
+    for (int s = 0; s < WSTAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], W_CONSUMERS);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&a_full[s], 1);
+      mbar_init(&a_empty[s], W_CONSUMERS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (t0 >= t1) return;
+
+  if (warp == W_CONSUMERS) {
+    // ================= producer =================
+    int stage = 0, phase = 0, a_slot = -1, strip = -1;
+    unsigned a_phase[2] = {0u, 0u};
+    const unsigned a_bytes = (unsigned)(p.K * 8);
+    for (int tile = t0; tile < t1; ++tile) {
+      const int tstrip = tile / p.tiles_n;
+      const int m0 = tstrip * WBM, n0 = (tile % p.tiles_n) * WBN;
+      const int rows = min(WBM, p.M - m0);
+      if (tstrip != strip) {
+        strip = tstrip;
+        a_slot = (a_slot + 1) & 1;
+        mbar_wait(&a_empty[a_slot], a_phase[a_slot] ^ 1u);
+        if (lane == 0) mbar_expect_tx(&a_full[a_slot], a_bytes * rows);
+        __syncwarp();
+        double* dst = Abuf + a_slot * WA_ELEMS;
+        for (int r = lane; r < rows; r += 32)
+          bulk_g2s(dst + r * WA_LD, p.A + (long long)(m0 + r) * p.lda, a_bytes, &a_full[a_slot]);
+        a_phase[a_slot] ^= 1u;
+      }
+      const int cols = min(WBN, p.N - n0);
+      const unsigned row_bytes = (unsigned)(cols * 8);
+      mbar_wait(&empty[stage], (unsigned)phase ^ 1u);
+      if (lane == 0) mbar_expect_tx(&full[stage], row_bytes * (p.K + rows));
+      __syncwarp();
+      double* bs = Sbuf + stage * WSTAGE_ELEMS;
+      double* cs = bs + WB_ELEMS;
+      for (int r = lane; r < p.K; r += 32)
+        bulk_g2s(bs + r * WB_LD, p.B + p.bidx[r] * p.ldb + n0, row_bytes, &full[stage]);
+      for (int r = lane; r < rows; r += 32)
+        bulk_g2s(cs + r * WC_LD, p.Cin + p.cidx[m0 + r] * p.ldcin + n0, row_bytes, &full[stage]);
+      if (++stage == WSTAGES) { stage = 0; phase ^= 1; }
+    }
+    return;
+  }
+
+  // ================= consumers =================
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp & 3) * 16, wn = (warp >> 2) * (WBN / 2);
+  int stage = 0, phase = 0, a_slot = -1, strip = -1;
+  unsigned a_phase[2] = {0u, 0u};
+  for (int tile = t0; tile < t1; ++tile) {
+    const int tstrip = tile / p.tiles_n;
+    const int m0 = tstrip * WBM, n0 = (tile % p.tiles_n) * WBN;
+    if (tstrip != strip) {
+      if (a_slot >= 0) {  // release the previous strip's A
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&a_empty[a_slot]);
+      }
+      strip = tstrip;
+      a_slot = (a_slot + 1) & 1;
+      mbar_wait(&a_full[a_slot], a_phase[a_slot]);
+      a_phase[a_slot] ^= 1u;
+    }
+    mbar_wait(&full[stage], (unsigned)phase);
+    const double* as = Abuf + a_slot * WA_ELEMS;
+    const double* bs = Sbuf + stage * WSTAGE_ELEMS;
+    const double* cs = bs + WB_ELEMS;
+    double acc[WNT][4];
+#pragma unroll
+    for (int j = 0; j < WNT; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[j][e] = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < WK; kk += 4) {
+      const double a0 = as[(wm + g) * WA_LD + kk + t];
+      const double a1 = as[(wm + g + 8) * WA_LD + kk + t];
+#pragma unroll
+      for (int j = 0; j < WNT; ++j) dmma_16x8x4(acc[j], a0, a1, bs[(kk + t) * WB_LD + wn + 8 * j + g]);
+    }
+    // epilogue: C = Cin - acc (one rounding, as cin - (a @ b)), 16-byte stores
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = wm + g + 8 * h;
+      const int gm = m0 + r;
+      if (gm < p.M) {
+        double* crow = p.C + (long long)gm * p.ldc;
+#pragma unroll
+        for (int j = 0; j < WNT; ++j) {
+          const int col = wn + 8 * j + 2 * t;
+          const int gn = n0 + col;
+          const double2 cin = *reinterpret_cast<const double2*>(cs + r * WC_LD + col);
+          const double v0 = cin.x - acc[j][2 * h];
+          const double v1 = cin.y - acc[j][2 * h + 1];
+          if (gn + 1 < p.N) {
+            *reinterpret_cast<double2*>(crow + gn) = make_double2(v0, v1);
+          } else if (gn < p.N) {
+            crow[gn] = v0;
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);
+    if (++stage == WSTAGES) { stage = 0; phase ^= 1; }
+  }
+}
+
+// -------------------------------------------------- generic cp.async kernel --
+constexpr int UBM = 64, UBN = 64, UK = 64;
+constexpr int UTHREADS = 256;                       // 8 warps: 2 (M) x 4 (N), warp tile 32 x 16
+constexpr int UWM = 2, UWN = 4, UWTM = UBM / UWM, UWTN = UBN / UWN;
+constexpr int UMT = UWTM / 16, UNT = UWTN / 8;      // 2 x 2 m16n8 tiles per warp
+constexpr int UA_LD = UK + 4, UB_LD = UBN + 4;      // = 4 (mod 16): conflict-free fragment loads
+constexpr size_t U_SMEM = sizeof(double) * (UBM * UA_LD + 2 * UK * UB_LD);
+
 template <bool VEC2>
 __device__ __forceinline__ void ru_copy(double* dst, const double* src, int valid) {
-  // valid: number of valid doubles in this chunk (0..2 for VEC2, 0..1 otherwise)
   if (valid == 0) {
     dst[0] = 0.0;
     if constexpr (VEC2) dst[1] = 0.0;
@@ -87,18 +276,16 @@ __global__ void __launch_bounds__(UTHREADS, 2) rank_update_kernel(RankUpdatePara
   load_A(strip * UBM);
   load_B((t0 % p.tiles_n) * UBN, 0);
   cp_async_commit();
-
   for (int tile = t0; tile < t1; ++tile) {
     const int buf = (tile - t0) & 1;
     const int tstrip = tile / p.tiles_n;
     const int m0 = tstrip * UBM, n0 = (tile % p.tiles_n) * UBN;
-    if (tstrip != strip) {  // new row strip (rare: chunks are contiguous): reload A
-      __syncthreads();       // everyone is done with the old A
+    if (tstrip != strip) {
+      __syncthreads();
       strip = tstrip;
       load_A(m0);
       cp_async_commit();
     }
-    // Cin of this tile -> registers (consumed by the epilogue, after the MMAs).
     double cin[UMT][2][UNT][2];
 #pragma unroll
     for (int i = 0; i < UMT; ++i)
@@ -109,22 +296,14 @@ __global__ void __launch_bounds__(UTHREADS, 2) rank_update_kernel(RankUpdatePara
 #pragma unroll
         for (int j = 0; j < UNT; ++j) {
           const int gn = n0 + wn + 8 * j + 2 * t;
-          if (crow != nullptr && VEC2 && gn + 1 < p.N) {
-            const double2 v = __ldg(reinterpret_cast<const double2*>(crow + gn));
-            cin[i][h][j][0] = v.x;
-            cin[i][h][j][1] = v.y;
-          } else {
-            cin[i][h][j][0] = (crow != nullptr && gn < p.N) ? __ldg(crow + gn) : 0.0;
-            cin[i][h][j][1] = (crow != nullptr && gn + 1 < p.N) ? __ldg(crow + gn + 1) : 0.0;
-          }
+          cin[i][h][j][0] = (crow != nullptr && gn < p.N) ? __ldg(crow + gn) : 0.0;
+          cin[i][h][j][1] = (crow != nullptr && gn + 1 < p.N) ? __ldg(crow + gn + 1) : 0.0;
         }
       }
-    // prefetch the next tile's B (its A, if a new strip, is loaded next iteration)
     if (tile + 1 < t1) load_B(((tile + 1) % p.tiles_n) * UBN, buf ^ 1);
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
-
     const double* bs = Bs + buf * UK * UB_LD;
     double acc[UMT][UNT][4];
 #pragma unroll
@@ -134,7 +313,7 @@ __global__ void __launch_bounds__(UTHREADS, 2) rank_update_kernel(RankUpdatePara
 #pragma unroll
         for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
 #pragma unroll
-    for (int kk = 0; kk < UK; kk += 4) {  // K zero-padded to 64 in shared memory
+    for (int kk = 0; kk < UK; kk += 4) {
       double a[UMT][2], b[UNT];
 #pragma unroll
       for (int i = 0; i < UMT; ++i) {
@@ -149,9 +328,8 @@ __global__ void __launch_bounds__(UTHREADS, 2) rank_update_kernel(RankUpdatePara
 #pragma unroll
         for (int j = 0; j < UNT; ++j) dmma_16x8x4(acc[i][j], a[i][0], a[i][1], b[j]);
     }
-    // epilogue: C = Cin - acc (one rounding, as cin - (a @ b)), 16-byte stores
 #pragma unroll
-    for (int i = 0; i < UMT; ++i) {
+    for (int i = 0; i < UMT; ++i)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int gm = m0 + wm + 16 * i + g + 8 * h;
@@ -160,18 +338,11 @@ __global__ void __launch_bounds__(UTHREADS, 2) rank_update_kernel(RankUpdatePara
 #pragma unroll
         for (int j = 0; j < UNT; ++j) {
           const int gn = n0 + wn + 8 * j + 2 * t;
-          const double v0 = cin[i][h][j][0] - acc[i][j][2 * h];
-          const double v1 = cin[i][h][j][1] - acc[i][j][2 * h + 1];
-          if (VEC2 && gn + 1 < p.N) {
-            *reinterpret_cast<double2*>(crow + gn) = make_double2(v0, v1);
-          } else {
-            if (gn < p.N) crow[gn] = v0;
-            if (gn + 1 < p.N) crow[gn + 1] = v1;
-          }
+          if (gn < p.N) crow[gn] = cin[i][h][j][0] - acc[i][j][2 * h];
+          if (gn + 1 < p.N) crow[gn + 1] = cin[i][h][j][1] - acc[i][j][2 * h + 1];
         }
       }
-    }
-    __syncthreads();  // B[buf] is refilled by the next iteration's prefetch
+    __syncthreads();
   }
   cp_async_wait<0>();
 }
@@ -181,28 +352,31 @@ int launch_rank_update(int M, int N, int K, const double* A, long long lda, cons
                        const int64_t* cidx, double* C, long long ldc, cudaStream_t st) {
   if (M < 0 || N < 0 || K < 0 || K > UK) return RS_ERR_ARG;
   if (M == 0 || N == 0) return RS_OK;
-  RankUpdateParams p{M, N, K, A, lda, B, ldb, bidx, Cin, ldcin, cidx, C, ldc, 0, 0};
-  p.tiles_n = (N + UBN - 1) / UBN;
-  p.tiles = p.tiles_n * ((M + UBM - 1) / UBM);
-  auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
-  const bool vec2 = al16(A) && al16(B) && al16(Cin) && al16(C) && lda % 2 == 0 && ldb % 2 == 0 &&
-                    ldcin % 2 == 0 && ldc % 2 == 0;
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  const int slots = 2 * nsm;
-  const int G = p.tiles < slots ? p.tiles : slots;
-  static bool configured[2] = {false, false};
-  if (vec2) {
-    if (!configured[1]) {
-      cudaFuncSetAttribute(rank_update_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)U_SMEM);
-      configured[1] = true;
+  auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  const bool bulk_ok = K > 0 && K % 2 == 0 && N % 2 == 0 && al16(A) && al16(B) && al16(Cin) && al16(C) &&
+                       lda % 2 == 0 && ldb % 2 == 0 && ldcin % 2 == 0 && ldc % 2 == 0;
+  RankUpdateParams p{M, N, K, A, lda, B, ldb, bidx, Cin, ldcin, cidx, C, ldc, 0, 0};
+  if (bulk_ok) {
+    p.tiles_n = (N + WBN - 1) / WBN;
+    p.tiles = p.tiles_n * ((M + WBM - 1) / WBM);
+    const int G = p.tiles < nsm ? p.tiles : nsm;
+    static bool configured = false;
+    if (!configured) {
+      cudaFuncSetAttribute(rank_update_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)W_SMEM);
+      configured = true;
     }
-    rank_update_kernel<true><<<G, UTHREADS, U_SMEM, st>>>(p);
+    rank_update_bulk_kernel<<<G, W_THREADS, W_SMEM, st>>>(p);
   } else {
-    if (!configured[0]) {
+    p.tiles_n = (N + UBN - 1) / UBN;
+    p.tiles = p.tiles_n * ((M + UBM - 1) / UBM);
+    const int G = p.tiles < 2 * nsm ? p.tiles : 2 * nsm;
+    static bool configured = false;
+    if (!configured) {
       cudaFuncSetAttribute(rank_update_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)U_SMEM);
-      configured[0] = true;
+      configured = true;
     }
     rank_update_kernel<false><<<G, UTHREADS, U_SMEM, st>>>(p);
   }
