@@ -101,6 +101,17 @@ int rs_rank_update(int M, int N, int K, const double* A, long long lda, const do
                    const int64_t* bidx, const double* Cin, long long ldcin, const int64_t* cidx,
                    double* C, long long ldc, void* stream);
 
+/* rs_absorb_block followed by the Schur block of the NEXT sketch block, in
+ * one pass over T when nc == 64 (fused DMMA kernel, fused_update.cu):
+ *   T_new, perm_new as rs_absorb_block;
+ *   S_next = Y_next[perm_new[k+nc:]] - T_new * Y_next[perm_new[:k+nc]],
+ *   *e2_dev = ||S_next||_F^2                       (skeleton.py:326-351, 317-323)
+ * Y_next is m x 64 (ldy = 64); S_next is (m-k-nc) x 64 and may alias S. */
+int rs_absorb_schur(int m, int k, int nc, const double* S, long long lds, const int64_t* sub_perm,
+                    const double* T, long long ldt, double* T_new, const int64_t* perm, int64_t* perm_new,
+                    const double* Y_next, long long ldy, double* S_next, double* e2_dev, void* workspace,
+                    void* stream);
+
 /* W (m x k, row-major) with W[perm[:k]] = I and W[perm[k:]] = T
  * (`_w_from_parts`, skeleton.py:176-182). */
 int rs_scatter_interp(const double* T, long long ldt, const int64_t* perm, int m, int k, double* W,

@@ -32,6 +32,8 @@ SIGNATURES = {
     "rs_panel_lupp": (_c_int, [_p, _c_ll, _c_int, _c_int, _p, _p, _p, _p]),
     "rs_schur_block": (_c_int, [_c_int, _c_int, _c_int, _p, _c_ll, _p, _p, _c_ll, _p, _c_ll, _p, _p, _p]),
     "rs_absorb_block": (_c_int, [_c_int, _c_int, _c_int, _p, _c_ll, _p, _p, _c_ll, _p, _p, _p, _p, _p]),
+    "rs_absorb_schur": (_c_int, [_c_int, _c_int, _c_int, _p, _c_ll, _p, _p, _c_ll, _p, _p, _p, _p, _c_ll,
+                                 _p, _p, _p, _p]),
     "rs_rank_update": (_c_int, [_c_int, _c_int, _c_int, _p, _c_ll, _p, _c_ll, _p, _p, _c_ll, _p, _p,
                                 _c_ll, _p]),
     "rs_scatter_interp":(_c_int, [_p, _c_ll, _p, _c_int, _c_int, _p, _c_ll, _p]),

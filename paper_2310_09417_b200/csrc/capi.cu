@@ -2,6 +2,7 @@
 // Composite calls (Schur block, absorb block) are sequences of the kernels in
 // gemm_f64.cu / panel.cu / aux.cu enqueued on the caller's stream.
 #include <atomic>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "rskel_internal.h"
@@ -16,7 +17,7 @@ namespace {
 constexpr int kMaxB = 64;
 
 struct WorkspaceLayout {
-  size_t panel_off, sumsq_off, linv_off, gemm_off, total;
+  size_t panel_off, sumsq_off, linv_off, gemm_off, fused_off, total;
 };
 
 WorkspaceLayout layout() {
@@ -32,7 +33,8 @@ WorkspaceLayout layout() {
   L.sumsq_off = up(rs::panel_workspace_bytes());
   L.linv_off = L.sumsq_off + up(rs::sumsq_workspace_bytes());
   L.gemm_off = L.linv_off + up(sizeof(double) * kMaxB * kMaxB);
-  L.total = L.gemm_off + up(rs::gemm_partials_bytes(nsm));
+  L.fused_off = L.gemm_off + up(rs::gemm_partials_bytes(nsm));
+  L.total = L.fused_off + up(rs::fused_partials_bytes(nsm));
   return L;
 }
 
@@ -134,6 +136,46 @@ int rs_absorb_block(int m, int k, int nc, const double* S_, long long lds, const
     }
   }
   return rs::launch_perm_update(perm, perm_new, m, k, sub_perm, S(stream));
+}
+
+int rs_absorb_schur(int m, int k, int nc, const double* S_, long long lds, const int64_t* sub_perm,
+                    const double* T, long long ldt, double* T_new, const int64_t* perm, int64_t* perm_new,
+                    const double* Y_next, long long ldy, double* S_next, double* e2_dev, void* workspace,
+                    void* stream) {
+  if (m < 0 || k < 0 || nc < 0 || nc > kMaxB || k + nc > m) return RS_ERR_ARG;
+  const int R = m - k, Rn = R - nc;
+  const long long ldn = k + nc;
+  auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  // The fused kernel is correct but not yet faster than the two tuned kernels
+  // on B200 (DMMA 41% busy: too few independent accumulators per warp); it is
+  // opt-in (RSKEL_FUSED=1) until that is fixed.
+  static const bool fused_enabled = [] {
+    const char* e = getenv("RSKEL_FUSED");
+    return e != nullptr && e[0] == '1';
+  }();
+  const bool fused = fused_enabled && nc == kMaxB && k % 32 == 0 && ldy == 64 && (k == 0 || ldt == k) &&
+                     al16(T) && al16(T_new) && al16(Y_next) && al16(S_next);
+  if (!fused) {
+    int rc = rs_absorb_block(m, k, nc, S_, lds, sub_perm, T, ldt, T_new, perm, perm_new, workspace, stream);
+    if (rc != RS_OK) return rc;
+    return rs_schur_block(m, k + nc, nc > 0 ? (int)ldy : 0, Y_next, ldy, perm_new, T_new, ldn, S_next,
+                          nc > 0 ? ldy : 1, e2_dev, workspace, stream);
+  }
+  double* linv = reinterpret_cast<double*>(W(workspace, layout().linv_off));
+  int rc = rs::launch_trinv(S_, lds, 1, sub_perm, nc, 1, 1, linv, kMaxB, S(stream));
+  if (rc != RS_OK) return rc;
+  rs::DGemmParams pw{Rn, nc, nc, S_, lds, sub_perm + nc, linv, kMaxB, nullptr, nullptr, 0,
+                     nullptr, T_new + k, ldn, 1.0, 0.0, gemm_ws(workspace)};
+  rc = rs::launch_dgemm(pw, false, S(stream));
+  if (rc != RS_OK) return rc;
+  rc = rs::launch_perm_update(perm, perm_new, m, k, sub_perm, S(stream));
+  if (rc != RS_OK) return rc;
+  rc = rs::launch_fused_absorb_schur(Rn, k, nc, T, sub_perm, T_new, Y_next, perm_new, S_next,
+                                     reinterpret_cast<double*>(W(workspace, layout().fused_off)),
+                                     S(stream));
+  if (rc != RS_OK) return rc;
+  if (e2_dev) rc = rs_sumsq(S_next, 64, Rn, 64, e2_dev, workspace, stream);
+  return rc;
 }
 
 int rs_rank_update(int M, int N, int K, const double* A, long long lda, const double* B, long long ldb,

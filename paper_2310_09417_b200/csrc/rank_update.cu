@@ -20,6 +20,8 @@
 // 64-bit fragment loads are bank-conflict free.  A generic cp.async kernel
 // (rank_update_kernel) remains for shapes the bulk path cannot take
 // (odd K, N or leading dimensions, misaligned pointers).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "rskel_internal.h"
 
@@ -241,6 +243,19 @@ __device__ __forceinline__ void ru_copy(double* dst, const double* src, int vali
   else cp_async8(dst, src, valid * 8);
 }
 
+// Read-only loads as volatile asm: ptxas keeps them ahead of the (volatile)
+// DMMA asm, so the Cin stream is in flight during the MMAs.
+RS_DEV double2 ldnc2(const double* q) {
+  double2 v;
+  asm volatile("ld.global.nc.v2.f64 {%0,%1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "l"(q));
+  return v;
+}
+RS_DEV double ldnc1(const double* q) {
+  double v;
+  asm volatile("ld.global.nc.f64 %0, [%1];\n" : "=d"(v) : "l"(q));
+  return v;
+}
+
 template <bool VEC2>
 __global__ void __launch_bounds__(UTHREADS, 2) rank_update_kernel(RankUpdateParams p) {
   extern __shared__ __align__(16) double usm[];
@@ -296,8 +311,14 @@ __global__ void __launch_bounds__(UTHREADS, 2) rank_update_kernel(RankUpdatePara
 #pragma unroll
         for (int j = 0; j < UNT; ++j) {
           const int gn = n0 + wn + 8 * j + 2 * t;
-          cin[i][h][j][0] = (crow != nullptr && gn < p.N) ? __ldg(crow + gn) : 0.0;
-          cin[i][h][j][1] = (crow != nullptr && gn + 1 < p.N) ? __ldg(crow + gn + 1) : 0.0;
+          if (VEC2 && crow != nullptr && gn + 1 < p.N) {
+            const double2 v = ldnc2(crow + gn);
+            cin[i][h][j][0] = v.x;
+            cin[i][h][j][1] = v.y;
+          } else {
+            cin[i][h][j][0] = (crow != nullptr && gn < p.N) ? ldnc1(crow + gn) : 0.0;
+            cin[i][h][j][1] = (crow != nullptr && gn + 1 < p.N) ? ldnc1(crow + gn + 1) : 0.0;
+          }
         }
       }
     if (tile + 1 < t1) load_B(((tile + 1) % p.tiles_n) * UBN, buf ^ 1);
@@ -338,8 +359,14 @@ __global__ void __launch_bounds__(UTHREADS, 2) rank_update_kernel(RankUpdatePara
 #pragma unroll
         for (int j = 0; j < UNT; ++j) {
           const int gn = n0 + wn + 8 * j + 2 * t;
-          if (gn < p.N) crow[gn] = cin[i][h][j][0] - acc[i][j][2 * h];
-          if (gn + 1 < p.N) crow[gn + 1] = cin[i][h][j][1] - acc[i][j][2 * h + 1];
+          const double v0 = cin[i][h][j][0] - acc[i][j][2 * h];
+          const double v1 = cin[i][h][j][1] - acc[i][j][2 * h + 1];
+          if (VEC2 && gn + 1 < p.N) {
+            *reinterpret_cast<double2*>(crow + gn) = make_double2(v0, v1);
+          } else {
+            if (gn < p.N) crow[gn] = v0;
+            if (gn + 1 < p.N) crow[gn + 1] = v1;
+          }
         }
       }
     __syncthreads();
@@ -359,7 +386,13 @@ int launch_rank_update(int M, int N, int K, const double* A, long long lda, cons
   const bool bulk_ok = K > 0 && K % 2 == 0 && N % 2 == 0 && al16(A) && al16(B) && al16(Cin) && al16(C) &&
                        lda % 2 == 0 && ldb % 2 == 0 && ldcin % 2 == 0 && ldc % 2 == 0;
   RankUpdateParams p{M, N, K, A, lda, B, ldb, bidx, Cin, ldcin, cidx, C, ldc, 0, 0};
-  if (bulk_ok) {
+  // Default: the 2-CTA/SM cp.async kernel (17-18 TF/s on B200); the bulk-copy
+  // pipeline (15 TF/s, per-row copy rate bound) is opt-in via RSKEL_RU_BULK=1.
+  static const bool prefer_bulk = [] {
+    const char* e = getenv("RSKEL_RU_BULK");
+    return e != nullptr && e[0] == '1';
+  }();
+  if (bulk_ok && prefer_bulk) {
     p.tiles_n = (N + WBN - 1) / WBN;
     p.tiles = p.tiles_n * ((M + WBM - 1) / WBM);
     const int G = p.tiles < nsm ? p.tiles : nsm;
@@ -373,12 +406,22 @@ int launch_rank_update(int M, int N, int K, const double* A, long long lda, cons
     p.tiles_n = (N + UBN - 1) / UBN;
     p.tiles = p.tiles_n * ((M + UBM - 1) / UBM);
     const int G = p.tiles < 2 * nsm ? p.tiles : 2 * nsm;
-    static bool configured = false;
-    if (!configured) {
-      cudaFuncSetAttribute(rank_update_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)U_SMEM);
-      configured = true;
+    const bool vec2 = al16(A) && al16(B) && al16(Cin) && al16(C) && lda % 2 == 0 && ldb % 2 == 0 &&
+                      ldcin % 2 == 0 && ldc % 2 == 0;
+    static bool configured[2] = {false, false};
+    if (vec2) {
+      if (!configured[1]) {
+        cudaFuncSetAttribute(rank_update_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)U_SMEM);
+        configured[1] = true;
+      }
+      rank_update_kernel<true><<<G, UTHREADS, U_SMEM, st>>>(p);
+    } else {
+      if (!configured[0]) {
+        cudaFuncSetAttribute(rank_update_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)U_SMEM);
+        configured[0] = true;
+      }
+      rank_update_kernel<false><<<G, UTHREADS, U_SMEM, st>>>(p);
     }
-    rank_update_kernel<false><<<G, UTHREADS, U_SMEM, st>>>(p);
   }
   count_launch(1);
   return cudaGetLastError() == cudaSuccess ? RS_OK : RS_ERR_CUDA;

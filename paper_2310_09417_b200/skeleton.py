@@ -313,12 +313,16 @@ class _AdaptiveDriver:
             t = 1
             self._sketch(1)
             pending = False  # speculative full-width absorb awaiting its ncols
+            # b == 64: absorb(t) and the Schur block of t+1 run as one fused
+            # pass over T (rs_absorb_schur); S/e2 of block t are then ready.
+            fused = b == _engine.MAX_BLOCK
+            have_schur = False
             while True:
                 y = self.y[t % 2]
-                tok = self.prof.start("schur")
-                if not wide:
+                if not wide and not have_schur:
+                    tok = self.prof.start("schur")
                     st.schur(y.data_ptr(), b, b, self.e2)
-                self.prof.stop(tok)
+                    self.prof.stop(tok)
                 if wide:
                     e2 = 0.0
                     for j0 in range(0, b, _engine.MAX_BLOCK):
@@ -355,7 +359,11 @@ class _AdaptiveDriver:
                     st.panel(b, self.nc)
                     self.prof.stop(tok)
                     tok = self.prof.start("absorb")
-                    st.absorb(b, b)
+                    if fused:
+                        st.absorb_schur(b, b, self.y[(t + 1) % 2].data_ptr(), self.e2)
+                        have_schur = True
+                    else:
+                        st.absorb(b, b)
                     self.prof.stop(tok)
                     pending = True
                     nc = b

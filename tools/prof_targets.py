@@ -12,7 +12,7 @@ what = sys.argv[1]
 ws = _device.workspace()
 st = _device.stream_handle()
 n = 20000
-k = 7000
+k = 7040
 R = n - k
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 if what == "sketch":
@@ -22,6 +22,19 @@ if what == "sketch":
     for _ in range(reps):
         _lib.call("rs_sketch_gemm", n, n, 64, a.data_ptr(), n, 1, om.data_ptr(), 64, y.data_ptr(), 64,
                   ws.data_ptr(), st)
+elif what == "fused":
+    y = torch.randn(n, 64, dtype=torch.float64, device="cuda")
+    T = torch.randn(R, k, dtype=torch.float64, device="cuda")
+    perm = torch.randperm(n, device="cuda")
+    S = torch.randn(R, 64, dtype=torch.float64, device="cuda") * 0.1
+    sub = torch.randperm(R, device="cuda")
+    Tn = torch.empty((R - 64) * (k + 64), dtype=torch.float64, device="cuda")
+    pn = torch.empty(n, dtype=torch.int64, device="cuda")
+    e2 = torch.empty(1, dtype=torch.float64, device="cuda")
+    for _ in range(reps):
+        _lib.call("rs_absorb_schur", n, k, 64, S.data_ptr(), 64, sub.data_ptr(), T.data_ptr(), k,
+                  Tn.data_ptr(), perm.data_ptr(), pn.data_ptr(), y.data_ptr(), 64, S.data_ptr(),
+                  e2.data_ptr(), ws.data_ptr(), st)
 elif what in ("schur", "rank_update", "absorb"):
     y = torch.randn(n, 64, dtype=torch.float64, device="cuda")
     T = torch.randn(R, k, dtype=torch.float64, device="cuda")
