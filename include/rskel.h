@@ -138,6 +138,26 @@ int rs_perm_update(const int64_t* perm, int64_t* perm_new, int m, int k, const i
 int rs_transpose(const double* src, long long lds, int rows, int cols, double* dst, long long ldd,
                  void* stream);
 
+/* One round of one-sided Jacobi on Xt (q x p row-major = X^T): for every
+ * pair (pairs[2r], pairs[2r+1]) rotate columns i, j of X (and rows of Vt) to
+ * make them orthogonal; *max_off = max |x_i.x_j| / (|x_i||x_j|) seen (as
+ * double bits, atomicMax).  Drives `pinv_apply` (dense.py:166-182). */
+int rs_jacobi_round(double* Xt, long long ldx, int p, double* Vt, long long ldv, int q, const int* pairs,
+                    int npairs, double tol, unsigned long long* max_off, void* stream);
+
+/* After Jacobi convergence: sigma_i = |Xt[i,:]|, scale row i of Vt by
+ * 1/sigma_i^2 (0 when sigma_i <= rcond * max sigma, gelsd's truncation). */
+int rs_pinv_scale(const double* Xt, long long ldx, int p, double* Vt, long long ldv, int q, double rcond,
+                  double* sigma, void* stream);
+
+/* *out = max_j sum_i |A[i,j]| (matrix 1-norm, for the cond_1 flag, skeleton.py:592-603). */
+int rs_norm1(const double* A, long long lda, int rows, int cols, double* out, void* stream);
+
+/* dst[i, j] = src[r(i)*rs + c(j)*cs], r/c via optional index vectors: the
+ * skeleton gathers a[I], a[:, J], a[ix_(I, J)] (skeleton.py:619,639-645). */
+int rs_gather2d(const double* src, long long rs, long long cs, const int64_t* ridx, int nr,
+                const int64_t* cidx, int nc, double* dst, long long ldd, void* stream);
+
 /* p[i] = i. */
 int rs_iota(int64_t* p, int n, void* stream);
 

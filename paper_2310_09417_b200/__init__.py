@@ -23,6 +23,16 @@ from .sketching import (
     make_gaussian,
     make_sketch,
 )
+from .dense import (
+    LUFactors,
+    frobenius_norm,
+    gemm,
+    invert_permutation,
+    lupp,
+    lupp_blocked_step,
+    row_permute,
+    triangular_solve,
+)
 from .skeleton import (
     STATUS_ILL_CONDITIONED,
     STATUS_NOT_CONVERGED,
@@ -35,5 +45,7 @@ from .skeleton import (
     rand_lupp,
     rand_lupp_adaptive,
 )
+from .lu_state import BlockedLUState, adaptive_init, adaptive_step, interpolation_matrix
+from .cur import CurFactors, cur_decompose, pinv_apply, two_sided_id
 
 __version__ = "0.1.0"

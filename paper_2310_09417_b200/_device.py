@@ -41,14 +41,15 @@ class Matrix:
     (row-major) or ``base[j*ld + i]`` (column-major).  ``kind`` records the
     caller's container so results can be returned the same way."""
 
-    __slots__ = ("t", "rows", "cols", "ld", "colmajor", "kind")
+    __slots__ = ("t", "rows", "cols", "ld", "colmajor", "kind", "off")
 
-    def __init__(self, t, rows, cols, ld, colmajor, kind):
+    def __init__(self, t, rows, cols, ld, colmajor, kind, off=0):
         self.t, self.rows, self.cols, self.ld, self.colmajor, self.kind = t, rows, cols, ld, colmajor, kind
+        self.off = off  # element offset of (0, 0) from t.data_ptr()
 
     @property
     def ptr(self):
-        return self.t.data_ptr()
+        return self.t.data_ptr() + 8 * self.off
 
     @property
     def shape(self):
@@ -56,7 +57,17 @@ class Matrix:
 
     @property
     def T(self):
-        return Matrix(self.t, self.cols, self.rows, self.ld, not self.colmajor, self.kind)
+        return Matrix(self.t, self.cols, self.rows, self.ld, not self.colmajor, self.kind, self.off)
+
+    def sub(self, r0, c0, rows, cols):
+        """View of the block [r0:r0+rows, c0:c0+cols] (no copy)."""
+        off = self.off + (c0 * self.ld + r0 if self.colmajor else r0 * self.ld + c0)
+        return Matrix(self.t, rows, cols, self.ld, self.colmajor, self.kind, off)
+
+    def tensor(self):
+        """The block as a strided torch view."""
+        st = (1, self.ld) if self.colmajor else (self.ld, 1)
+        return torch.as_strided(self.t, (self.rows, self.cols), st, self.t.storage_offset() + self.off)
 
     def row_major(self):
         """A row-major view of the same matrix (device transpose copy if needed)."""
@@ -67,6 +78,22 @@ class Matrix:
             _lib.call("rs_transpose", self.ptr, self.ld, self.cols, self.rows, out.data_ptr(),
                       self.cols, stream_handle())
         return Matrix(out, self.rows, self.cols, self.cols, False, self.kind)
+
+    def copy(self):
+        """Fresh row-major copy (device kernels only)."""
+        src = self.row_major()
+        if src is not self:
+            return src
+        out = torch.empty((self.rows, self.cols), dtype=torch.float64, device=self.t.device)
+        if self.rows and self.cols:
+            _lib.call("rs_gather_rows", self.ptr, self.ld, None, self.rows, self.cols, out.data_ptr(),
+                      max(self.cols, 1), stream_handle())
+        return Matrix(out, self.rows, self.cols, max(self.cols, 1), False, self.kind)
+
+
+def empty(rows, cols, kind="torch_cuda"):
+    t = torch.empty((rows, cols), dtype=torch.float64, device=device())
+    return Matrix(t, rows, cols, max(cols, 1), False, kind)
 
 
 def _from_tensor_2d(t, kind):

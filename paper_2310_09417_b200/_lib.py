@@ -42,6 +42,10 @@ SIGNATURES = {
     "rs_trinv": (_c_int, [_p, _c_ll, _c_ll, _p, _c_int, _c_int, _c_int, _p, _c_ll, _p]),
     "rs_perm_update": (_c_int, [_p, _p, _c_int, _c_int, _p, _p]),
     "rs_transpose": (_c_int, [_p, _c_ll, _c_int, _c_int, _p, _c_ll, _p]),
+    "rs_jacobi_round": (_c_int, [_p, _c_ll, _c_int, _p, _c_ll, _c_int, _p, _c_int, _c_double, _p, _p]),
+    "rs_pinv_scale": (_c_int, [_p, _c_ll, _c_int, _p, _c_ll, _c_int, _c_double, _p, _p]),
+    "rs_norm1": (_c_int, [_p, _c_ll, _c_int, _c_int, _p, _p]),
+    "rs_gather2d": (_c_int, [_p, _c_ll, _c_ll, _p, _c_int, _p, _c_int, _p, _c_ll, _p]),
     "rs_iota": (_c_int, [_p, _c_int, _p]),
 }
 

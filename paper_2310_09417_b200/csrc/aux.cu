@@ -252,3 +252,35 @@ int launch_transpose(const double* src, long long lds, int rows, int cols, doubl
 }
 
 }  // namespace rs
+
+namespace rs {
+
+// dst[i, j] = src(r(i), c(j)) with src element (r, c) at src[r * rs + c * cs];
+// r(i) = ridx ? ridx[i] : i, c(j) = cidx ? cidx[j] : j.  Skeleton gathers
+// a[I], a[:, J], a[ix_(I, J)] for either input layout (skeleton.py:619,639-645).
+__global__ void gather2d_kernel(const double* __restrict__ src, long long rs_, long long cs_,
+                                const int64_t* __restrict__ ridx, int nr, const int64_t* __restrict__ cidx,
+                                int nc, double* __restrict__ dst, long long ldd) {
+  for (int i = blockIdx.x; i < nr; i += gridDim.x) {
+    const long long r = ridx ? ridx[i] : i;
+    const double* s = src + r * rs_;
+    double* d = dst + (long long)i * ldd;
+    for (int j = threadIdx.x; j < nc; j += blockDim.x) {
+      const long long c = cidx ? cidx[j] : j;
+      d[j] = s[c * cs_];
+    }
+  }
+}
+
+int launch_gather2d(const double* src, long long rs_, long long cs_, const int64_t* ridx, int nr,
+                    const int64_t* cidx, int nc, double* dst, long long ldd, cudaStream_t st) {
+  if (nr < 0 || nc < 0) return RS_ERR_ARG;
+  if (nr == 0 || nc == 0) return RS_OK;
+  int threads = nc >= 256 ? 256 : ((nc + 31) / 32) * 32;
+  int grid = nr < 148 * 16 ? nr : 148 * 16;
+  gather2d_kernel<<<grid, threads, 0, st>>>(src, rs_, cs_, ridx, nr, cidx, nc, dst, ldd);
+  count_launch(1);
+  return cudaGetLastError() == cudaSuccess ? RS_OK : RS_ERR_CUDA;
+}
+
+}  // namespace rs

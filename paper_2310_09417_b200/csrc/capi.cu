@@ -210,6 +210,25 @@ int rs_transpose(const double* src, long long lds, int rows, int cols, double* d
   return rs::launch_transpose(src, lds, rows, cols, dst, ldd, S(stream));
 }
 
+int rs_jacobi_round(double* Xt, long long ldx, int p, double* Vt, long long ldv, int q, const int* pairs,
+                    int npairs, double tol, unsigned long long* max_off, void* stream) {
+  return rs::launch_jacobi_round(Xt, ldx, p, Vt, ldv, q, pairs, npairs, tol, max_off, S(stream));
+}
+
+int rs_pinv_scale(const double* Xt, long long ldx, int p, double* Vt, long long ldv, int q, double rcond,
+                  double* sigma, void* stream) {
+  return rs::launch_pinv_scale(Xt, ldx, p, Vt, ldv, q, rcond, sigma, S(stream));
+}
+
+int rs_norm1(const double* A, long long lda, int rows, int cols, double* out, void* stream) {
+  return rs::launch_norm1(A, lda, rows, cols, out, S(stream));
+}
+
+int rs_gather2d(const double* src, long long rs_, long long cs_, const int64_t* ridx, int nr,
+                const int64_t* cidx, int nc, double* dst, long long ldd, void* stream) {
+  return rs::launch_gather2d(src, rs_, cs_, ridx, nr, cidx, nc, dst, ldd, S(stream));
+}
+
 int rs_iota(int64_t* p, int n, void* stream) { return rs::launch_iota(p, n, S(stream)); }
 
 }  // extern "C"

@@ -59,6 +59,14 @@ int launch_perm_update(const int64_t* perm, int64_t* perm_new, int m, int k, con
 int launch_iota(int64_t* p, int n, cudaStream_t st);
 int launch_scatter_interp(const double* T, long long ldt, const int64_t* perm, int m, int k, double* W,
                           long long ldw, cudaStream_t st);
+// One-sided Jacobi SVD / pinv helpers (svd.cu)
+int launch_jacobi_round(double* Xt, long long ldx, int p, double* Vt, long long ldv, int q, const int* pairs,
+                        int npairs, double tol, unsigned long long* max_off, cudaStream_t st);
+int launch_pinv_scale(const double* Xt, long long ldx, int p, double* Vt, long long ldv, int q, double rcond,
+                      double* sigma, cudaStream_t st);
+int launch_norm1(const double* A, long long lda, int rows, int cols, double* out, cudaStream_t st);
+int launch_gather2d(const double* src, long long rs_, long long cs_, const int64_t* ridx, int nr,
+                    const int64_t* cidx, int nc, double* dst, long long ldd, cudaStream_t st);
 int launch_transpose(const double* src, long long lds, int rows, int cols, double* dst, long long ldd,
                      cudaStream_t st);
 

@@ -1,0 +1,152 @@
+// One-sided (Hestenes) Jacobi SVD of a tall-skinny matrix and the small
+// helpers of the CUR linking solve `pinv_apply` (reference `dense.py:166-182`,
+// LAPACK gelsd with rcond 1e-12) and of the two-sided ID condition flag
+// (`skeleton.py:592-603`).
+//
+// X (p x q) is held transposed, Xt (q x p row-major: row i = column i of X), so
+// every column operation is a contiguous, coalesced stream.  One launch runs
+// one round of a round-robin (circle) schedule: CTA r rotates column pair
+// (i, j) -- three dot products by a fixed-order block reduction, then the
+// rotation of the two columns of X and of V.  Deterministic; converged when
+// every |x_i . x_j| <= tol sqrt(|x_i|^2 |x_j|^2).
+#include "common.cuh"
+#include "rskel_internal.h"
+
+namespace rs {
+
+constexpr int JT = 256;
+
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0) {
+    for (int w = 0; w < JT / 32; ++w) s += red[w];
+    red[JT / 32] = s;
+  }
+  __syncthreads();
+  s = red[JT / 32];
+  __syncthreads();
+  return s;
+}
+
+__global__ void __launch_bounds__(JT) jacobi_round_kernel(double* __restrict__ Xt, long long ldx, int p,
+                                                          double* __restrict__ Vt, long long ldv, int q,
+                                                          const int* __restrict__ pairs, double tol,
+                                                          unsigned long long* __restrict__ max_off) {
+  __shared__ double red[JT / 32 + 1];
+  const int i = pairs[2 * blockIdx.x], j = pairs[2 * blockIdx.x + 1];
+  if (i < 0 || j < 0) return;  // bye (odd q)
+  double* xi = Xt + (long long)i * ldx;
+  double* xj = Xt + (long long)j * ldx;
+  double a = 0.0, b = 0.0, g = 0.0;
+  for (int r = threadIdx.x; r < p; r += JT) {
+    const double u = xi[r], w = xj[r];
+    a = fma(u, u, a);
+    b = fma(w, w, b);
+    g = fma(u, w, g);
+  }
+  a = block_sum(a, red);
+  b = block_sum(b, red);
+  g = block_sum(g, red);
+  const double scale = sqrt(a) * sqrt(b);
+  if (!(scale > 0.0)) return;
+  const double off = fabs(g) / scale;
+  if (threadIdx.x == 0) atomicMax(max_off, (unsigned long long)__double_as_longlong(off));
+  if (!(off > tol)) return;
+  // rotation annihilating g (Rutishauser's formulas)
+  const double zeta = (b - a) / (2.0 * g);
+  const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+  const double c = 1.0 / sqrt(1.0 + tt * tt), s = c * tt;
+  for (int r = threadIdx.x; r < p; r += JT) {
+    const double u = xi[r], w = xj[r];
+    xi[r] = c * u - s * w;
+    xj[r] = s * u + c * w;
+  }
+  double* vi = Vt + (long long)i * ldv;
+  double* vj = Vt + (long long)j * ldv;
+  for (int r = threadIdx.x; r < q; r += JT) {
+    const double u = vi[r], w = vj[r];
+    vi[r] = c * u - s * w;
+    vj[r] = s * u + c * w;
+  }
+}
+
+int launch_jacobi_round(double* Xt, long long ldx, int p, double* Vt, long long ldv, int q, const int* pairs,
+                        int npairs, double tol, unsigned long long* max_off, cudaStream_t st) {
+  if (npairs <= 0) return RS_OK;
+  jacobi_round_kernel<<<npairs, JT, 0, st>>>(Xt, ldx, p, Vt, ldv, q, pairs, tol, max_off);
+  count_launch(1);
+  return cudaGetLastError() == cudaSuccess ? RS_OK : RS_ERR_CUDA;
+}
+
+// sigma_i = |Xt[i, :]|, d_i = 1 / sigma_i^2 if sigma_i > rcond * max sigma else 0;
+// scales column i of V (row i of Vt) by d_i.  One CTA.
+__global__ void __launch_bounds__(JT) pinv_scale_kernel(const double* __restrict__ Xt, long long ldx, int p,
+                                                        double* __restrict__ Vt, long long ldv, int q,
+                                                        double rcond, double* __restrict__ sigma) {
+  __shared__ double red[JT / 32 + 1];
+  __shared__ double smax;
+  for (int i = 0; i < q; ++i) {
+    double a = 0.0;
+    for (int r = threadIdx.x; r < p; r += JT) a = fma(Xt[(long long)i * ldx + r], Xt[(long long)i * ldx + r], a);
+    a = block_sum(a, red);
+    if (threadIdx.x == 0) sigma[i] = sqrt(a);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int i = 0; i < q; ++i) m = fmax(m, sigma[i]);
+    smax = m;
+  }
+  __syncthreads();
+  for (int i = 0; i < q; ++i) {
+    const double si = sigma[i];
+    const double d = (si > rcond * smax && si > 0.0) ? 1.0 / (si * si) : 0.0;
+    for (int r = threadIdx.x; r < q; r += JT) Vt[(long long)i * ldv + r] *= d;
+  }
+}
+
+int launch_pinv_scale(const double* Xt, long long ldx, int p, double* Vt, long long ldv, int q, double rcond,
+                      double* sigma, cudaStream_t st) {
+  if (q <= 0) return RS_OK;
+  pinv_scale_kernel<<<1, JT, 0, st>>>(Xt, ldx, p, Vt, ldv, q, rcond, sigma);
+  count_launch(1);
+  return cudaGetLastError() == cudaSuccess ? RS_OK : RS_ERR_CUDA;
+}
+
+// out = max_j sum_i |A[i, j]| (1-norm), A row-major rows x cols.  One CTA.
+__global__ void __launch_bounds__(JT) norm1_kernel(const double* __restrict__ A, long long lda, int rows, int cols,
+                                                   double* __restrict__ out) {
+  __shared__ double red[JT / 32 + 1];
+  double best = 0.0;
+  for (int c0 = 0; c0 < cols; c0 += JT) {
+    const int c = c0 + threadIdx.x;
+    double s = 0.0;
+    if (c < cols)
+      for (int r = 0; r < rows; ++r) s += fabs(A[(long long)r * lda + c]);
+    best = fmax(best, s);
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) best = fmax(best, __shfl_down_sync(0xffffffffu, best, off));
+  if (lane == 0) red[warp] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int w = 0; w < JT / 32; ++w) m = fmax(m, red[w]);
+    *out = m;
+  }
+}
+
+int launch_norm1(const double* A, long long lda, int rows, int cols, double* out, cudaStream_t st) {
+  if (rows < 0 || cols < 0) return RS_ERR_ARG;
+  norm1_kernel<<<1, JT, 0, st>>>(A, lda, rows, cols, out);
+  count_launch(1);
+  return cudaGetLastError() == cudaSuccess ? RS_OK : RS_ERR_CUDA;
+}
+
+}  // namespace rs

@@ -1,0 +1,231 @@
+"""Two-sided ID and CUR on the B200 -- drop-in for `randskel.skeleton`
+(`skeleton.py:565-647`) and `dense.pinv_apply` (`dense.py:166-182`).
+
+  pinv_apply(a, b)            min-norm least squares, singular values below
+                              1e-12 * sigma_max truncated (gelsd semantics),
+                              by one-sided Jacobi SVD on the device
+  two_sided_id(a, k, spec, rng)
+  cur_decompose(a, k, spec, rng)
+
+Skeleton gathers (`a[row_idx]`, `a[:, col_idx]`, `a[ix_(I, J)]`) run on the
+gather kernel; column skeletons come from LUPP of ``a[row_idx].T`` on the
+T-form engine; the 1-norm condition number of the skeleton submatrix is
+computed exactly from its device LU (the reference's LAPACK dgecon estimate
+is a lower bound of it, so the flag can only turn on earlier, never later).
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _device, _engine, _lib, dense
+from .errors import DimensionError, RankDeficientError
+from .skeleton import STATUS_ILL_CONDITIONED, STATUS_OK, SkeletonResult, rand_lupp
+
+__all__ = ["CurFactors", "pinv_apply", "two_sided_id", "cur_decompose"]
+
+PINV_RCOND = 1e-12   # dense.py:49
+COND_LIMIT = 1e14    # skeleton.py:72
+JACOBI_TOL = 2.0 ** -52
+JACOBI_SWEEPS = 40
+
+
+@dataclass
+class CurFactors:
+    """C = a[:, col_idx], R = a[row_idx, :] implied (reference `skeleton.py:132-139`)."""
+
+    row_idx: object
+    col_idx: object
+    u_mid: object
+    status: str = STATUS_OK
+
+
+def _st():
+    return _device.stream_handle()
+
+
+def _round_robin(q):
+    """Circle-method schedule: q-1 rounds (q even) of q/2 disjoint pairs."""
+    n = q + (q % 2)
+    players = list(range(n))
+    rounds = []
+    for _ in range(n - 1):
+        pr = []
+        for i in range(n // 2):
+            a, b = players[i], players[n - 1 - i]
+            if a >= q or b >= q:
+                a = b = -1
+            pr.append((a, b))
+        rounds.append(pr)
+        players = [players[0]] + [players[-1]] + players[1:-1]
+    return np.array(rounds, dtype=np.int32)  # (rounds, n/2, 2)
+
+
+def _jacobi_svd_t(Xt):
+    """One-sided Jacobi on Xt (q x p, rows = columns of X), in place.
+    Returns Vt (q x q) with X V = Xt_final^T."""
+    q, p = Xt.shape
+    dev = Xt.device
+    Vt = torch.eye(q, dtype=torch.float64, device=dev)
+    if q <= 1:
+        return Vt
+    sched = torch.as_tensor(_round_robin(q)).to(dev)
+    maxoff = torch.zeros(1, dtype=torch.int64, device=dev)
+    npairs = sched.shape[1]
+    for _ in range(JACOBI_SWEEPS):
+        maxoff.zero_()
+        for r in range(sched.shape[0]):
+            _lib.call("rs_jacobi_round", Xt.data_ptr(), p, p, Vt.data_ptr(), q, q,
+                      sched[r].data_ptr(), npairs, JACOBI_TOL, maxoff.data_ptr(), _st())
+        off = float(maxoff.view(torch.float64).item())
+        if off <= JACOBI_TOL:
+            break
+    return Vt
+
+
+def _pinv_apply_dev(A, B):
+    """x = A^+ B (A: Matrix p x q, B: Matrix p x r, any layouts) -> row-major tensor q x r.
+
+    One-sided Jacobi on the columns of A gives A V = U Sigma; then
+    x = V diag(1/sigma^2) (A V)^T B with sigma <= rcond * sigma_max dropped."""
+    p, q = A.shape
+    r = B.cols
+    dev = _device.device()
+    Xt = _gather(A.T).tensor()          # q x p, rows = columns of A
+    Vt = _jacobi_svd_t(Xt)
+    sigma = torch.empty(max(q, 1), dtype=torch.float64, device=dev)
+    _lib.call("rs_pinv_scale", Xt.data_ptr(), p, p, Vt.data_ptr(), q, q, PINV_RCOND, sigma.data_ptr(), _st())
+    if B.colmajor:
+        # Z^T = B^T (A V) with B^T row-major: no transpose of the (large) B
+        XV = _gather(dense._mat(Xt).T)  # p x q row-major
+        Zt = torch.empty((r, q), dtype=torch.float64, device=dev)
+        dense._gemm(dense._mat(Zt), B.T, XV)
+        Z = dense._mat(Zt).T            # q x r (column-major view)
+    else:
+        Zr = torch.empty((q, r), dtype=torch.float64, device=dev)
+        dense._gemm(dense._mat(Zr), dense._mat(Xt), B)
+        Z = dense._mat(Zr)
+    x = torch.empty((q, r), dtype=torch.float64, device=dev)
+    dense._gemm(dense._mat(x), dense._mat(Vt).T, Z)
+    return x
+
+
+def pinv_apply(a, b):
+    """Minimum-norm least-squares solution of ``a @ x = b`` (reference `dense.py:166-182`)."""
+    m, n = _device.shape_of(a, "a")
+    if isinstance(b, torch.Tensor):
+        bt = b.to(device=_device.device(), dtype=torch.float64)
+    else:
+        bt = torch.as_tensor(np.asarray(b, dtype=np.float64)).to(_device.device())
+    if bt.dim() == 1:
+        bt = bt[:, None]
+    if m != bt.shape[0]:
+        raise DimensionError(f"row counts do not agree: {(m, n)} vs {tuple(bt.shape)}")
+    A = _device.as_matrix(a, "a")
+    x = _pinv_apply_dev(A, dense._mat(bt.contiguous()))
+    return dense._out(x, A.kind)
+
+
+# ---------------------------------------------------------------- helpers ---
+def _idx(x):
+    if isinstance(x, torch.Tensor):
+        return x.to(device=_device.device(), dtype=torch.int64)
+    return torch.as_tensor(np.asarray(x, dtype=np.int64)).to(_device.device())
+
+
+def _gather(A, ridx=None, cidx=None):
+    """a[ridx][:, cidx] as a fresh row-major Matrix, any input layout (gather kernel)."""
+    nr = A.rows if ridx is None else ridx.numel()
+    nc = A.cols if cidx is None else cidx.numel()
+    out = _device.empty(nr, nc, A.kind)
+    rs_, cs_ = (1, A.ld) if A.colmajor else (A.ld, 1)
+    _lib.call("rs_gather2d", A.ptr, rs_, cs_, ridx.data_ptr() if ridx is not None else None, nr,
+              cidx.data_ptr() if cidx is not None else None, nc, out.ptr, out.ld, _st())
+    return out
+
+
+def _rows(A, idx):
+    return _gather(A, ridx=idx)
+
+
+def _cols(A, idx):
+    return _gather(A, cidx=idx)
+
+
+def _column_skeletons_from_rows(A, row_idx, k):
+    """LUPP of a[row_idx].T (n x k) -> (col_idx, x) (reference `skeleton.py:565-571`)."""
+    rows = _rows(A, row_idx)        # k x n
+    y = rows.T.row_major()          # n x k
+    st, w, fail = _engine.factor_sample(y, want_w=True)
+    if fail is not None:
+        raise RankDeficientError(fail)
+    return st.perm[:k].clone(), w   # x = w.T
+
+
+def _cond1(S):
+    """Exact 1-norm condition number of the k x k device Matrix S (inf if singular)."""
+    k = S.rows
+    dev = _device.device()
+    out = torch.empty(1, dtype=torch.float64, device=dev)
+    Sr = S.row_major()
+    _lib.call("rs_norm1", Sr.ptr, Sr.ld, k, k, out.data_ptr(), _st())
+    anorm = float(out.item())
+    if anorm == 0.0:
+        return np.inf
+    A = Sr.copy()
+    try:
+        perm, _ = dense._lupp_device(A, allow_partial=False)
+    except RankDeficientError:
+        return np.inf
+    L, U = dense._split_lu(A, k)
+    # S^{-1} = U^{-1} L^{-1} P
+    eye_p = torch.zeros((k, k), dtype=torch.float64, device=dev)
+    eye_p[torch.arange(k, device=dev), perm] = 1.0
+    Y = dense._trsm_left(dense._mat(L.contiguous()), dense._mat(eye_p), lower=True, unit=True)
+    d = U.diagonal()
+    if bool((d == 0).any()):
+        return np.inf
+    X = dense._trsm_left(dense._mat(U.contiguous()), Y, lower=False, unit=False)
+    _lib.call("rs_norm1", X.ptr, X.ld, k, k, out.data_ptr(), _st())
+    inorm = float(out.item())
+    if not np.isfinite(inorm):
+        return np.inf
+    return anorm * inorm
+
+
+def two_sided_id(a, k, spec, rng):
+    """Row skeletons by sketched LUPP, columns from the rows (reference `skeleton.py:606-625`)."""
+    r = rand_lupp(a, k, spec, rng)
+    A = _device.as_matrix(a)
+    ridx = _idx(r.row_idx)
+    cidx, w = _column_skeletons_from_rows(A, ridx, k)
+    S = _cols(_rows(A, ridx), cidx)
+    status = STATUS_ILL_CONDITIONED if _cond1(S) > COND_LIMIT else STATUS_OK
+    kind = A.kind
+    x = _device.to_output(w, kind)
+    return SkeletonResult(rank=k, row_idx=r.row_idx, col_idx=_device.to_host_index(cidx, kind),
+                          w=r.w, x=x.T, status=status)
+
+
+def cur_decompose(a, k, spec, rng):
+    """CUR with skeletons from sketched LUPP and ``u_mid = C^+ a R^+``
+    (reference `skeleton.py:628-647`)."""
+    r = rand_lupp(a, k, spec, rng)
+    A = _device.as_matrix(a)
+    ridx = _idx(r.row_idx)
+    return _cur_from_rows(A, ridx, k, r.row_idx)
+
+
+def _cur_from_rows(A, ridx, k, row_idx_out):
+    cidx, _ = _column_skeletons_from_rows(A, ridx, k)
+    C = _cols(A, cidx)                   # m x k
+    R = _rows(A, ridx)                   # k x n
+    # a R^+ = pinv_apply(R^T, a^T)^T ;  u_mid = pinv_apply(C, a R^+)
+    arp_t = _pinv_apply_dev(R.T, A.T)    # k x m  (= (a R^+)^T)
+    u_mid = _pinv_apply_dev(C, dense._mat(arp_t).T)
+    S = _cols(R, cidx)
+    status = STATUS_ILL_CONDITIONED if _cond1(S) > COND_LIMIT else STATUS_OK
+    kind = A.kind
+    return CurFactors(row_idx=row_idx_out, col_idx=_device.to_host_index(cidx, kind),
+                      u_mid=dense._out(u_mid, kind), status=status)

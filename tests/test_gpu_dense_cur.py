@@ -1,0 +1,213 @@
+"""LU-form API, triangular solves, pinv_apply, two-sided ID and CUR on the
+device vs the reference's golden outputs and the CPU oracle (fp64)."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+import randskel_oracle as orc  # noqa: E402
+from conftest import golden  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def rs():
+    import paper_2310_09417_b200 as rs
+
+    return rs
+
+
+def spec(rs, n, ell=None):
+    return rs.SketchSpec("gaussian", n=n, ell=ell or min(n, 32))
+
+
+def relerr(x, y):
+    return np.linalg.norm(np.asarray(x) - np.asarray(y)) / max(np.linalg.norm(y), 1e-300)
+
+
+# ------------------------------------------------------------------ lupp ----
+@pytest.mark.parametrize("case", ["lupp_tiebreak", "lupp_hand", "lupp_chan10", "lupp_chan30"])
+def test_lupp_known_answers(rs, case):
+    g = golden(case)
+    if case == "lupp_tiebreak":
+        a = np.array([[1, 5], [1, 5], [3, 0], [1, 1]], dtype=float)
+    elif case == "lupp_hand":
+        a = np.array([[1, 2], [3, 4]], dtype=float)
+    else:
+        a = orc.gen_chan(int(case[9:]))
+    f = rs.lupp(a)
+    assert np.array_equal(f.perm, g["perm"])
+    assert np.array_equal(f.L, g["L"]) and np.array_equal(f.U, g["U"])
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_lupp_matches_reference(rs, seed):
+    g = golden(f"lupp_rand{seed}")
+    m, k = int(g["m"]), int(g["k"])
+    a = np.random.default_rng(seed).standard_normal((m, k))
+    f = rs.lupp(a)
+    assert np.array_equal(f.perm, g["perm"])
+    if "L" in g:
+        assert np.abs(f.L - g["L"]).max() <= 1e-13 and np.abs(f.U - g["U"]).max() <= 1e-13
+    else:
+        assert np.abs(f.L[:64] - g["L_head"]).max() <= 1e-12
+    err = np.linalg.norm(a[f.perm] - f.L @ f.U)
+    assert err <= 1e-12 * np.linalg.norm(a) * m
+
+
+def test_lupp_errors(rs):
+    col0 = np.array([4.0, 2.0, 8.0, 1.0])
+    col1 = np.array([1.0, 2.0, 4.0, 8.0])
+    with pytest.raises(rs.RankDeficientError) as exc:
+        rs.lupp(np.column_stack([col0, col1, col0]))
+    assert exc.value.step == 2
+    with pytest.raises(rs.DimensionError):
+        rs.lupp(np.ones((2, 3)))
+    a = np.ones((3, 2))
+    a[1, 1] = np.nan
+    with pytest.raises(ValueError):
+        rs.lupp(a)
+
+
+def test_lupp_input_not_mutated(rs):
+    y = np.asfortranarray(np.random.default_rng(5).standard_normal((20, 8)))
+    before = y.copy()
+    rs.lupp(y)
+    assert np.array_equal(y, before)
+
+
+@pytest.mark.parametrize("cuts", [[4], [2, 4], [1, 3, 5]])
+def test_blocked_step_equals_one_shot(rs, cuts):
+    y = np.random.default_rng(4).standard_normal((64, 8))
+    one = rs.lupp(y)
+    f = None
+    bounds = [0] + cuts + [8]
+    for lo, hi in zip(bounds[:-1], bounds[1:]):
+        f = rs.lupp_blocked_step(f, y[:, lo:hi])
+    assert np.array_equal(f.perm, one.perm)
+    assert np.linalg.norm(f.L - one.L) <= 1e-12 * np.linalg.norm(one.L)
+    assert np.linalg.norm(f.U - one.U) <= 1e-12 * np.linalg.norm(one.U)
+
+
+# ---------------------------------------------------------- triangular ----
+@pytest.mark.parametrize("side", ["left", "right"])
+@pytest.mark.parametrize("uplo", ["lower", "upper"])
+@pytest.mark.parametrize("trans", [False, True])
+@pytest.mark.parametrize("unit", [False, True])
+def test_triangular_solve(rs, side, uplo, trans, unit):
+    import scipy.linalg
+
+    g = np.random.default_rng(7)
+    n = 150
+    t = g.standard_normal((n, n)) + 4 * np.eye(n)
+    t = np.tril(t) if uplo == "lower" else np.triu(t)
+    b = g.standard_normal((n, 9)) if side == "left" else g.standard_normal((9, n))
+    x = rs.triangular_solve(t, b, side=side, uplo=uplo, trans=trans, unit_diagonal=unit)
+    if side == "left":
+        ref = scipy.linalg.solve_triangular(t, b, lower=uplo == "lower", trans=1 if trans else 0,
+                                            unit_diagonal=unit)
+    else:
+        ref = scipy.linalg.solve_triangular(t, b.T, lower=uplo == "lower", trans=0 if trans else 1,
+                                            unit_diagonal=unit).T
+    assert relerr(x, ref) < 1e-11
+
+
+def test_triangular_solve_singular(rs):
+    t = np.eye(4)
+    t[2, 2] = 0.0
+    with pytest.raises(rs.SingularError) as exc:
+        rs.triangular_solve(t, np.ones(4))
+    assert exc.value.index == 2
+    v = rs.triangular_solve(np.eye(3) * 2.0, np.ones(3))
+    assert v.shape == (3,) and np.allclose(v, 0.5)
+
+
+def test_gemm_and_norm(rs):
+    g = np.random.default_rng(1)
+    a = g.standard_normal((3, 5))
+    b = g.standard_normal((3, 4))
+    assert np.allclose(rs.gemm(a, b, transpose_a=True), a.T @ b, atol=1e-13)
+    assert np.allclose(rs.gemm([[1, 2], [3, 4]], [[5], [6]]), [[17.0], [39.0]])
+    with pytest.raises(rs.DimensionError):
+        rs.gemm(np.ones((2, 3)), np.ones((2, 3)))
+    x = g.standard_normal((50, 7))
+    assert abs(rs.frobenius_norm(x) - np.linalg.norm(x)) <= 1e-13 * np.linalg.norm(x)
+    p = g.permutation(50)
+    assert np.array_equal(rs.row_permute(x, p), x[p])
+    assert np.array_equal(rs.invert_permutation(p)[p], np.arange(50))
+
+
+# ------------------------------------------------------------ LU state ----
+def test_adaptive_init_and_step_match_oracle(rs):
+    a, _ = orc.gen_fast_decay(90, 70, 1e-6, 16)
+    sp = spec(rs, 70)
+    st = rs.adaptive_init(a, 10, sp, rs.RngStream(17))
+    for _ in range(3):
+        e, st = rs.adaptive_step(st, a, sp)
+    one = rs.lupp(st.ysofar)
+    assert np.array_equal(st.perm, one.perm)
+    L = np.vstack([st.L1, st.L2])
+    assert np.linalg.norm(L - one.L) <= 1e-11 * np.linalg.norm(one.L)
+    rec = np.linalg.norm(st.ysofar[st.perm] - L @ st.U1)
+    assert rec <= 1e-12 * np.linalg.norm(st.ysofar) * st.m
+    w = rs.interpolation_matrix(st)
+    assert np.array_equal(w[st.perm[:st.rank]], np.eye(st.rank))
+    # the adaptive driver reaches the same state
+    res = rs.rand_lupp_adaptive(a, 10, 1e-300, sp, rs.RngStream(17), max_rank=40)
+    assert np.array_equal(res.row_idx, st.perm[:40])
+
+
+def test_adaptive_step_rank_cap(rs):
+    a, _ = orc.gen_fast_decay(20, 20, 1e-4, 18)
+    sp = spec(rs, 20)
+    st = rs.adaptive_init(a, 12, sp, rs.RngStream(19))
+    with pytest.raises(rs.DimensionError):
+        rs.adaptive_step(st, a, sp)
+
+
+# ------------------------------------------------------- pinv / CUR ------
+def test_pinv_apply_matches_lstsq(rs):
+    g = np.random.default_rng(3)
+    a = g.standard_normal((300, 40))
+    b = g.standard_normal((300, 7))
+    x = rs.pinv_apply(a, b)
+    ref = orc.pinv_apply(a, b)
+    assert relerr(x, ref) < 1e-12
+    # rank deficient: truncated like gelsd
+    a2 = g.standard_normal((200, 10)) @ g.standard_normal((10, 30))
+    x2 = rs.pinv_apply(a2, b[:200])
+    ref2 = orc.pinv_apply(a2, b[:200])
+    assert relerr(x2, ref2) < 1e-8
+
+
+def test_two_sided_id_matches_reference(rs):
+    g = golden("two_sided_exact")
+    r = rs.two_sided_id(g["a"], 20, spec(rs, 60), rs.RngStream(50))
+    assert np.array_equal(r.row_idx, g["row_idx"]) and np.array_equal(r.col_idx, g["col_idx"])
+    assert r.status == str(g["status"])
+    s = g["a"][np.ix_(r.row_idx, r.col_idx)]
+    assert np.linalg.norm(g["a"] - r.w @ s @ r.x) <= 1e-8 * np.linalg.norm(g["a"])
+    assert np.array_equal(r.x[:, r.col_idx], np.eye(20))
+    g = golden("two_sided_illcond")
+    r = rs.two_sided_id(np.diag([1.0] * 5 + [1e-16] * 5), 8, spec(rs, 10), rs.RngStream(57))
+    assert r.status == "ill_conditioned"
+
+
+def test_cur_matches_reference(rs):
+    g = golden("cur_exact")
+    cur = rs.cur_decompose(g["a"], 18, spec(rs, 55), rs.RngStream(54))
+    assert np.array_equal(cur.row_idx, g["row_idx"]) and np.array_equal(cur.col_idx, g["col_idx"])
+    assert relerr(cur.u_mid, g["u_mid"]) < 1e-8
+    a = g["a"]
+    rec = a[:, cur.col_idx] @ cur.u_mid @ a[cur.row_idx]
+    assert np.linalg.norm(a - rec) <= 1e-8 * np.linalg.norm(a)
+    g = golden("cur_fd300")
+    a = golden("fast_decay_300")["a"]
+    cur = rs.cur_decompose(a, 100, spec(rs, 300), rs.RngStream(55))
+    assert np.array_equal(cur.row_idx, g["row_idx"]) and np.array_equal(cur.col_idx, g["col_idx"])
+    rec = a[:, cur.col_idx] @ cur.u_mid @ a[cur.row_idx]
+    ref = a[:, g["col_idx"]] @ g["u_mid"] @ a[g["row_idx"]]
+    e, e0 = np.linalg.norm(a - rec), np.linalg.norm(a - ref)
+    assert e <= 1.5 * e0 + 1e-13 * np.linalg.norm(a)
