@@ -158,6 +158,16 @@ int rs_norm1(const double* A, long long lda, int rows, int cols, double* out, vo
 int rs_gather2d(const double* src, long long rs, long long cs, const int64_t* ridx, int nr,
                 const int64_t* cidx, int nc, double* dst, long long ldd, void* stream);
 
+/* n standard normals of numpy's Generator(Philox(key=[seed, stream_id]))
+ * in generation order, each divided by `scale` (1.0 = none; sqrt(ell) for the
+ * 'inv_sqrt_ell' spec): `make_gaussian` (sketching.py:191-204) on the device.
+ * Workspace: rs_gaussian_workspace_bytes(n).  *status_dev = 1 (never seen)
+ * if the parallel word->normal resolution hit an unsupported chain; the
+ * caller then draws on the host. */
+size_t rs_gaussian_workspace_bytes(long long n);
+int rs_gaussian(unsigned long long seed, unsigned long long stream_id, long long n, double scale, double* out,
+                void* rng_workspace, size_t ws_bytes, int* status_dev, void* stream);
+
 /* p[i] = i. */
 int rs_iota(int64_t* p, int n, void* stream);
 

@@ -46,6 +46,6 @@ from .skeleton import (
     rand_lupp_adaptive,
 )
 from .lu_state import BlockedLUState, adaptive_init, adaptive_step, interpolation_matrix
-from .cur import CurFactors, cur_decompose, pinv_apply, two_sided_id
+from .cur import CurFactors, cur_decompose, cur_decompose_adaptive, pinv_apply, two_sided_id
 
 __version__ = "0.1.0"

@@ -214,9 +214,83 @@ def dgemm(a, b, alpha=1.0, beta=0.0, cin=None, out=None, aidx=None, bidx=None, c
 
 def sketch(a, omega):
     """Y = a @ omega with omega a host (n x ell) float64 array (host-RNG draw)."""
-    m, n = a.shape
-    ell = omega.shape[1]
     om = torch.as_tensor(np.ascontiguousarray(omega, dtype=np.float64)).to(device())
+    return sketch_dev(a, om)
+
+
+# ------------------------------------------------------------ device RNG ----
+_rng_ws = {}
+
+
+def _rng_workspace(n):
+    need = _lib.load().rs_gaussian_workspace_bytes(n)
+    dev = device()
+    ws = _rng_ws.get(dev.index)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(int(need * 1.25) + 4096, dtype=torch.uint8, device=dev)
+        _rng_ws[dev.index] = ws
+    return ws
+
+
+def host_rng():
+    """RSKEL_HOST_RNG=1 draws Omega with numpy on the host (the reference's
+    own generator) and copies it in, instead of the device draw."""
+    import os
+    return os.environ.get("RSKEL_HOST_RNG", "0") == "1"
+
+
+def gaussian(stream, n, ell, unit=False, out=None, status=None):
+    """(n, ell) standard normals of numpy's Generator(Philox(key=[seed, stream]))
+    drawn on the device, divided by sqrt(ell) unless ``unit`` -- bit-identical
+    to `make_gaussian` on the host (rs_gaussian).  ``stream`` is an RngStream.
+
+    With ``status`` (a 1-element int32 device tensor) the launch is fully
+    asynchronous and the caller checks ``status`` later; otherwise a nonzero
+    status (a ziggurat chain longer than the parallel resolver supports, never
+    observed) is repaired at once by the host draw."""
+    dev = device()
+    if out is None:
+        out = torch.empty((n, ell), dtype=torch.float64, device=dev)
+    N = n * ell
+    if N == 0:
+        return out
+    ws = _rng_workspace(N)
+    check = status is None
+    if check:
+        status = torch.empty(1, dtype=torch.int32, device=dev)
+    scale = 1.0 if unit else float(np.sqrt(ell))
+    k0, k1 = stream.philox_key()
+    _lib.call("rs_gaussian", k0, k1, N, scale, out.data_ptr(),
+              ws.data_ptr(), ws.numel(), status.data_ptr(), stream_handle())
+    if check and int(status.item()) != 0:
+        out.copy_(torch.as_tensor(host_gaussian(stream, n, ell, unit)))
+    return out
+
+
+def host_gaussian(stream, n, ell, unit=False):
+    h = stream.generator().standard_normal((n, ell))
+    if not unit:
+        h /= np.sqrt(ell)
+    return h
+
+
+def sketch_omega(a, spec, rng):
+    """Y = a @ Omega for the Gaussian embedding ``spec`` (n x ell) drawn from
+    ``rng``: the device draw by default, the host draw under RSKEL_HOST_RNG=1.
+    Same Omega bit for bit either way."""
+    n, ell = spec.n, spec.ell
+    unit = spec.scale != "inv_sqrt_ell"
+    if host_rng():
+        om = torch.as_tensor(host_gaussian(rng, n, ell, unit)).to(device())
+    else:
+        om = gaussian(rng, n, ell, unit=unit)
+    return sketch_dev(a, om)
+
+
+def sketch_dev(a, om):
+    """Y = a @ om with om a row-major (n x ell) device tensor."""
+    m, n = a.shape
+    ell = om.shape[1]
     y = torch.empty((m, ell), dtype=torch.float64, device=device())
     _lib.call("rs_sketch_gemm", m, n, ell, a.ptr, a.ld, int(a.colmajor), om.data_ptr(),
               max(ell, 1), y.data_ptr(), max(ell, 1), workspace().data_ptr(), stream_handle())

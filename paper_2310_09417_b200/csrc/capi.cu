@@ -229,6 +229,13 @@ int rs_gather2d(const double* src, long long rs_, long long cs_, const int64_t* 
   return rs::launch_gather2d(src, rs_, cs_, ridx, nr, cidx, nc, dst, ldd, S(stream));
 }
 
+size_t rs_gaussian_workspace_bytes(long long n) { return rs::gaussian_workspace_bytes(n); }
+
+int rs_gaussian(unsigned long long seed, unsigned long long stream_id, long long n, double scale, double* out,
+                void* rng_workspace, size_t ws_bytes, int* status_dev, void* stream) {
+  return rs::launch_gaussian(seed, stream_id, n, scale, out, rng_workspace, ws_bytes, status_dev, S(stream));
+}
+
 int rs_iota(int64_t* p, int n, void* stream) { return rs::launch_iota(p, n, S(stream)); }
 
 }  // extern "C"

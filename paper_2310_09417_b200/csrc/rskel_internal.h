@@ -67,6 +67,10 @@ int launch_pinv_scale(const double* Xt, long long ldx, int p, double* Vt, long l
 int launch_norm1(const double* A, long long lda, int rows, int cols, double* out, cudaStream_t st);
 int launch_gather2d(const double* src, long long rs_, long long cs_, const int64_t* ridx, int nr,
                     const int64_t* cidx, int nc, double* dst, long long ldd, cudaStream_t st);
+// numpy Generator(Philox).standard_normal on the device (gaussian_rng.cu)
+size_t gaussian_workspace_bytes(long long N);
+int launch_gaussian(uint64_t seed, uint64_t stream, long long N, double scale, double* out, void* ws,
+                    size_t ws_bytes, int* status_dev, cudaStream_t st);
 int launch_transpose(const double* src, long long lds, int rows, int cols, double* dst, long long ldd,
                      cudaStream_t st);
 

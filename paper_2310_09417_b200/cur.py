@@ -23,7 +23,7 @@ from . import _device, _engine, _lib, dense
 from .errors import DimensionError, RankDeficientError
 from .skeleton import STATUS_ILL_CONDITIONED, STATUS_OK, SkeletonResult, rand_lupp
 
-__all__ = ["CurFactors", "pinv_apply", "two_sided_id", "cur_decompose"]
+__all__ = ["CurFactors", "pinv_apply", "two_sided_id", "cur_decompose", "cur_decompose_adaptive"]
 
 PINV_RCOND = 1e-12   # dense.py:49
 COND_LIMIT = 1e14    # skeleton.py:72
@@ -229,3 +229,21 @@ def _cur_from_rows(A, ridx, k, row_idx_out):
     kind = A.kind
     return CurFactors(row_idx=row_idx_out, col_idx=_device.to_host_index(cidx, kind),
                       u_mid=dense._out(u_mid, kind), status=status)
+
+
+def cur_decompose_adaptive(a, b, tau, spec, rng, max_rank=None):
+    """Adaptive CUR (BASELINE configs[2]): rows by `rand_lupp_adaptive` to
+    tolerance tau, columns from the rows, linking matrix as `cur_decompose`.
+
+    The reference has no adaptive CUR; this is the composition SURVEY.md 8c
+    pins for it (`skeleton.py:391-460` then `skeleton.py:637-647` at the
+    detected rank).  fp32 inputs are upcast to fp64 like the reference
+    (`skeleton.py:200-204`).  Returns ``(CurFactors, SkeletonResult)``.
+    """
+    from .skeleton import rand_lupp_adaptive
+
+    A = _device.as_matrix(a)
+    res = rand_lupp_adaptive(A, b, tau, spec, rng, max_rank=max_rank)
+    ridx = _idx(res.row_idx)
+    cur = _cur_from_rows(A, ridx, res.rank, res.row_idx)
+    return cur, res

@@ -55,8 +55,10 @@ def _block_spec(spec, n, ell):
 
 def _draw_block(A, spec, stream, b):
     """``a @ Omega`` for one block (`skeleton.py:293-295`) -> device tensor (m x b)."""
-    op = make_sketch(_block_spec(spec, A.cols, b), stream)
-    return _device.sketch(A, op.omega)
+    sp = _block_spec(spec, A.cols, b)
+    if sp.kind != "gaussian":
+        make_sketch(sp, stream)  # raises NotImplementedError
+    return _device.sketch_omega(A, sp, stream)
 
 
 def _kind_out(x, kind):

@@ -18,7 +18,7 @@ import torch
 
 from . import _device, _engine, _omega
 from .errors import DimensionError, RankDeficientError
-from .sketching import make_gaussian, make_sketch
+from .sketching import make_sketch
 
 __all__ = [
     "STATUS_OK",
@@ -116,13 +116,21 @@ def _finite_or_raise(y, name="matrix"):
         raise ValueError(f"{name} contains non-finite entries")
 
 
+def _gaussian_spec(spec, rng):
+    """The Gaussian embedding is drawn on the device (`_device.sketch_omega`);
+    other kinds raise like `make_sketch`."""
+    if spec.kind != "gaussian":
+        make_sketch(spec, rng)  # raises NotImplementedError
+    return spec
+
+
 def rand_lupp(a, k, spec, rng):
     """Row skeletons by LUPP of ``a @ Omega`` (fixed rank k)."""
     m, n = _device.shape_of(a)
     _check_rank(k, m, n)
-    op = make_sketch(spec.with_dims(n, k), rng)
+    sp = _gaussian_spec(spec.with_dims(n, k), rng)
     a = _device.as_matrix(a)
-    y = _device.Matrix(_device.sketch(a, op.omega), m, k, k, False, a.kind)
+    y = _device.Matrix(_device.sketch_omega(a, sp, rng), m, k, k, False, a.kind)
     _finite_or_raise(y)
     st, w = _factor_sketch(y, a.kind)
     idx = st.perm[:k].clone()
@@ -134,9 +142,9 @@ def column_id(a, k, spec, rng):
     """Column skeletons by LUPP of ``a.T @ Gamma``; ``x[:, col_idx] = I``."""
     m, n = _device.shape_of(a)
     _check_rank(k, m, n)
-    op = make_sketch(spec.with_dims(m, k), rng)
+    sp = _gaussian_spec(spec.with_dims(m, k), rng)
     a = _device.as_matrix(a)
-    y = _device.Matrix(_device.sketch(a.T, op.omega), n, k, k, False, a.kind)
+    y = _device.Matrix(_device.sketch_omega(a.T, sp, rng), n, k, k, False, a.kind)
     _finite_or_raise(y)
     st, w = _factor_sketch(y, a.kind)
     idx = st.perm[:k].clone()
@@ -219,19 +227,26 @@ class _AdaptiveDriver:
     one pinned readback) while the GPU keeps the next sketch GEMM running.
     """
 
-    def __init__(self, a, b, tau, rng, max_rank):
+    def __init__(self, a, b, tau, rng, max_rank, host=False):
         self.prof = _PHASE_TIMER or _NullTimer()
         self.a, self.b, self.tau, self.rng, self.max_rank = a, b, tau, rng, max_rank
         m, n = a.shape
         self.m, self.n = m, n
         dev = _device.device()
-        self.src = _omega.BlockOmegaSource(n, b, rng)
+        # Omega_t: device draw (rs_gaussian) on the side stream by default,
+        # host thread-pool draw + H2D copy under RSKEL_HOST_RNG=1.
+        self.dev_rng = not (host or _device.host_rng())
+        self.src = None if self.dev_rng else _omega.BlockOmegaSource(n, b, rng)
+        self.rng_status = torch.zeros(max_rank // b + 4, dtype=torch.int32, device=dev)
         self.om = [torch.empty((n, b), dtype=torch.float64, device=dev) for _ in range(2)]
         self.y = [torch.empty((m, b), dtype=torch.float64, device=dev) for _ in range(2)]
         self.om_ready = [torch.cuda.Event() for _ in range(2)]
         self.om_free = [None, None]
         self.copy_stream = torch.cuda.Stream(device=dev)
         self.compute = torch.cuda.current_stream(dev)
+        if self.dev_rng:
+            _device._rng_workspace(n * b)       # allocated on the compute stream
+        self.copy_stream.wait_stream(self.compute)  # prior users of the RNG workspace
         self.e2 = torch.empty(1, dtype=torch.float64, device=dev)
         self.nc = torch.empty(max(1, (b + 63) // 64), dtype=torch.int32, device=dev)
         self.h_e2 = torch.empty(1, dtype=torch.float64, pin_memory=True)
@@ -247,11 +262,17 @@ class _AdaptiveDriver:
             return
         self._issued.add(t)
         slot = t % 2
-        h = self.src.host(t)
+        if t >= self.rng_status.numel():
+            return
+        h = None if self.dev_rng else self.src.host(t)
         with torch.cuda.stream(self.copy_stream):
             if self.om_free[slot] is not None:
                 self.copy_stream.wait_event(self.om_free[slot])
-            self.om[slot].copy_(h, non_blocking=True)
+            if h is None:
+                _device.gaussian(self.rng.child(t), self.n, self.b, out=self.om[slot],
+                                 status=self.rng_status[t:t + 1])
+            else:
+                self.om[slot].copy_(h, non_blocking=True)
             self.om_ready[slot].record(self.copy_stream)
 
     def _sketch(self, t):
@@ -374,7 +395,16 @@ class _AdaptiveDriver:
                     status = STATUS_RANK_EXHAUSTED
                     break
         finally:
-            self.src.close()
+            if self.src is not None:
+                self.src.close()
+            # speculative draws may still be in flight on the side stream
+            self.compute.wait_stream(self.copy_stream)
+        if self.dev_rng and bool(self.rng_status.any()):
+            # a block the parallel ziggurat resolver could not place (never
+            # observed): redo the whole loop with the host draw, same bits
+            self.dev_rng = False
+            self.__init__(self.a, self.b, self.tau, self.rng, self.max_rank, host=True)
+            return self.run()
         k = st.k
         tok = self.prof.start("interp")
         w = st.interpolation()

@@ -13,6 +13,7 @@ are out of the north-star scope).
 """
 
 from dataclasses import dataclass, replace
+from functools import lru_cache
 
 import numpy as np
 
@@ -43,6 +44,12 @@ def _splitmix64(z):
     return z ^ (z >> 31)
 
 
+@lru_cache(maxsize=4096)
+def _philox_key(seed, stream):
+    k = np.random.Philox(key=[seed, stream]).state["state"]["key"]
+    return int(k[0]), int(k[1])
+
+
 @dataclass(frozen=True)
 class RngStream:
     """Reproducible splittable stream: Philox4x64 keyed by ``[seed, stream]``
@@ -53,6 +60,13 @@ class RngStream:
 
     def generator(self):
         return np.random.Generator(np.random.Philox(key=[self.seed & _M64, self.stream & _M64]))
+
+    def philox_key(self):
+        """The two key words numpy's Philox really runs with for
+        ``key=[seed, stream]``: numpy converts the list with np.asarray, which
+        goes through float64 when one word is >= 2**63 and the other is not,
+        rounding that word.  The device draw must use the same words."""
+        return _philox_key(self.seed & _M64, self.stream & _M64)
 
     def child(self, i):
         return RngStream(self.seed, _splitmix64((self.stream & _M64) ^ _splitmix64(i & _M64)))

@@ -211,3 +211,20 @@ def test_cur_matches_reference(rs):
     ref = a[:, g["col_idx"]] @ g["u_mid"] @ a[g["row_idx"]]
     e, e0 = np.linalg.norm(a - rec), np.linalg.norm(a - ref)
     assert e <= 1.5 * e0 + 1e-13 * np.linalg.norm(a)
+
+
+def test_adaptive_cur_fp32_composition(rs):
+    """cfg3 recipe at 1024 x 512: fp32 nonnegative low-rank + noise, adaptive CUR."""
+    g = golden("adaptive_cur_nonneg")
+    rng = np.random.default_rng(0)
+    wmat, hmat = rng.random((1024, 100)), rng.random((100, 512))
+    low = wmat @ hmat
+    noise = rng.random((1024, 512))
+    a32 = (low + 1e-6 * np.linalg.norm(low) / np.linalg.norm(noise) * noise).astype(np.float32)
+    cur, res = rs.cur_decompose_adaptive(a32, 64, float(g["tau"]), spec(rs, 512, 64), rs.RngStream(0))
+    assert res.rank == int(g["rank"]) and res.status == str(g["status"])
+    assert np.array_equal(res.row_idx, g["row_idx"])
+    assert np.array_equal(cur.col_idx, g["col_idx"])
+    a = a32.astype(np.float64)
+    rec = a[:, cur.col_idx] @ cur.u_mid @ a[cur.row_idx]
+    assert np.linalg.norm(a - rec) <= 1e-5 * np.linalg.norm(a)

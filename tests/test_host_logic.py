@@ -83,3 +83,16 @@ def test_error_trace_requires_increasing_ranks():
     tr.append(rs.TraceRecord(k=10, e_schur=1.0))
     with pytest.raises(ValueError):
         tr.append(rs.TraceRecord(k=10, e_schur=0.5))
+
+
+def test_philox_key_matches_numpy_conversion():
+    """RngStream.philox_key() = the key numpy actually uses (float64 rounding
+    of a word >= 2**63 when the other word is small)."""
+    import numpy as np
+    import paper_2310_09417_b200 as rs
+
+    for seed, stream in [(0, 0), (0, 0xa706dd2f4d197e6f), (1 << 63, 1 << 63), (5, (1 << 64) - 1), (2**62, 7)]:
+        s = rs.RngStream(seed, stream)
+        k = np.random.Philox(key=[seed, stream]).state["state"]["key"]
+        assert s.philox_key() == (int(k[0]), int(k[1]))
+    assert rs.RngStream(0, 0xa706dd2f4d197e6f).philox_key()[1] != 0xa706dd2f4d197e6f
