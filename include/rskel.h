@@ -117,7 +117,8 @@ int rs_absorb_schur(int m, int k, int nc, const double* S, long long lds, const 
 int rs_scatter_interp(const double* T, long long ldt, const int64_t* perm, int m, int k, double* W,
                       long long ldw, void* stream);
 
-/* dst[i, :] = src[idx[i], :]  (skeleton gathers `a[row_idx]`, skeleton.py:569,640). */
+/* dst[i, :] = src[idx[i], :]  (skeleton gathers `a[row_idx]`, skeleton.py:569,640);
+ * idx[i] < 0 gives a zero row (owner-masked gathers of the sharded loop). */
 int rs_gather_rows(const double* src, long long lds, const int64_t* idx, int nrows, int ncols,
                    double* dst, long long ldd, void* stream);
 
@@ -170,6 +171,31 @@ int rs_gaussian(unsigned long long seed, unsigned long long stream_id, long long
 
 /* p[i] = i. */
 int rs_iota(int64_t* p, int n, void* stream);
+
+/* ---- column-sharded adaptive loop (no reference counterpart:
+ * the reference is single-process, this shards `rand_lupp_adaptive`,
+ * skeleton.py:391-460, over ranks that own candidate rows [lo, hi)). ------ */
+
+/* Per-block maps from the replicated position order perm (rank k):
+ *   ytop_src[p] (p < k)   local row of skeleton p, or -1 if another rank owns it
+ *   lrow[p]               local T row of position p >= k (or -1), for the next block
+ *   loc[r], spos[r]       local candidate and Schur position of local row r
+ *   *count                number of local remaining rows
+ * With sub != NULL (just after an absorb of nc columns at rank k_old = k - nc,
+ * lrow_old the previous lrow): src_row[r] / wsrc[r] = previous local T row /
+ * Schur row of local row r, tp_src[j] = previous local T row of pivot j or -1. */
+int rs_shard_maps(const int64_t* perm, int m, int k, long long lo, long long hi, const int64_t* lrow_old,
+                  const int64_t* sub, int k_old, int nc, int64_t* lrow, int64_t* loc, int64_t* spos,
+                  int64_t* src_row, int64_t* wsrc, int64_t* tp_src, int64_t* ytop_src, int* count, void* stream);
+
+/* dst[idx[i], :] = src[i, :] for idx[i] >= 0. */
+int rs_scatter_rows(const double* src, long long lds, const int64_t* idx, int nrows, int ncols, double* dst,
+                    long long ldd, void* stream);
+
+/* Local rows [lo, hi) of W (m x k): zero, W[perm[p]-lo, p] = 1 for owned
+ * skeletons, W[loc[r]] = T[r] for the r local remaining rows. */
+int rs_scatter_interp_local(const double* T, long long ldt, const int64_t* perm, int k, const int64_t* loc, int r,
+                            long long lo, long long hi, double* W, long long ldw, void* stream);
 
 #ifdef __cplusplus
 }

@@ -50,6 +50,10 @@ SIGNATURES = {
     "rs_gaussian": (_c_int, [ctypes.c_ulonglong, ctypes.c_ulonglong, _c_ll, _c_double, _p, _p,
                              ctypes.c_size_t, _p, _p]),
     "rs_iota": (_c_int, [_p, _c_int, _p]),
+    "rs_shard_maps": (_c_int, [_p, _c_int, _c_int, _c_ll, _c_ll, _p, _p, _c_int, _c_int, _p, _p, _p, _p, _p,
+                               _p, _p, _p, _p]),
+    "rs_scatter_rows": (_c_int, [_p, _c_ll, _p, _c_int, _c_int, _p, _c_ll, _p]),
+    "rs_scatter_interp_local": (_c_int, [_p, _c_ll, _p, _c_int, _p, _c_int, _c_ll, _c_ll, _p, _c_ll, _p]),
 }
 
 ABI_VERSION = 1

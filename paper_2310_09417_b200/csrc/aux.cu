@@ -8,14 +8,19 @@
 
 namespace rs {
 
-// dst[i, c] = src[idx[i], c] (idx == nullptr: identity), row-major.
+// dst[i, c] = src[idx[i], c] (idx == nullptr: identity; idx[i] < 0: a zero
+// row -- the owner-masked gathers of the sharded loop), row-major.
 __global__ void gather_rows_kernel(const double* __restrict__ src, long long lds,
                                    const int64_t* __restrict__ idx, int nrows, int ncols,
                                    double* __restrict__ dst, long long ldd) {
   for (int i = blockIdx.x; i < nrows; i += gridDim.x) {
     long long r = idx ? idx[i] : i;
-    const double* s = src + r * lds;
     double* d = dst + (long long)i * ldd;
+    if (r < 0) {
+      for (int c = threadIdx.x; c < ncols; c += blockDim.x) d[c] = 0.0;
+      continue;
+    }
+    const double* s = src + r * lds;
     for (int c = threadIdx.x; c < ncols; c += blockDim.x) d[c] = s[c];
   }
 }

@@ -238,4 +238,21 @@ int rs_gaussian(unsigned long long seed, unsigned long long stream_id, long long
 
 int rs_iota(int64_t* p, int n, void* stream) { return rs::launch_iota(p, n, S(stream)); }
 
+int rs_shard_maps(const int64_t* perm, int m, int k, long long lo, long long hi, const int64_t* lrow_old,
+                  const int64_t* sub, int k_old, int nc, int64_t* lrow, int64_t* loc, int64_t* spos,
+                  int64_t* src_row, int64_t* wsrc, int64_t* tp_src, int64_t* ytop_src, int* count, void* stream) {
+  return rs::launch_shard_maps(perm, m, k, lo, hi, lrow_old, sub, k_old, nc, lrow, loc, spos, src_row, wsrc,
+                               tp_src, ytop_src, count, S(stream));
+}
+
+int rs_scatter_rows(const double* src, long long lds, const int64_t* idx, int nrows, int ncols, double* dst,
+                    long long ldd, void* stream) {
+  return rs::launch_scatter_rows(src, lds, idx, nrows, ncols, dst, ldd, S(stream));
+}
+
+int rs_scatter_interp_local(const double* T, long long ldt, const int64_t* perm, int k, const int64_t* loc, int r,
+                            long long lo, long long hi, double* W, long long ldw, void* stream) {
+  return rs::launch_scatter_interp_local(T, ldt, perm, k, loc, r, lo, hi, W, ldw, S(stream));
+}
+
 }  // extern "C"

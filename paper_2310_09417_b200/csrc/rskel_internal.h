@@ -57,6 +57,14 @@ int launch_trinv(const double* T, long long rs_, long long cs_, const int64_t* r
 int launch_perm_update(const int64_t* perm, int64_t* perm_new, int m, int k, const int64_t* sub,
                        cudaStream_t st);
 int launch_iota(int64_t* p, int n, cudaStream_t st);
+int launch_shard_maps(const int64_t* perm, int m, int k, long long lo, long long hi, const int64_t* lrow_old,
+                      const int64_t* sub, int k_old, int nc, int64_t* lrow, int64_t* loc, int64_t* spos,
+                      int64_t* src_row, int64_t* wsrc, int64_t* tp_src, int64_t* ytop_src, int* count,
+                      cudaStream_t st);
+int launch_scatter_rows(const double* src, long long lds, const int64_t* idx, int nrows, int ncols, double* dst,
+                        long long ldd, cudaStream_t st);
+int launch_scatter_interp_local(const double* T, long long ldt, const int64_t* perm, int k, const int64_t* loc,
+                                int r, long long lo, long long hi, double* W, long long ldw, cudaStream_t st);
 int launch_scatter_interp(const double* T, long long ldt, const int64_t* perm, int m, int k, double* W,
                           long long ldw, cudaStream_t st);
 // One-sided Jacobi SVD / pinv helpers (svd.cu)

@@ -1,0 +1,291 @@
+"""Column-sharded adaptive skeleton loop over ranks.
+
+The reference is single-process; its north-star multi-GPU form is the
+column ID of an A that is column-sharded across the GPUs of one box: rank g
+holds the contiguous candidate rows ``a[lo:hi]`` of ``a = A.T`` (so A's
+columns J_g) and the loop of `rand_lupp_adaptive` (`skeleton.py:391-460`)
+runs with
+
+  * the sketch ``Y_g = a[lo:hi] @ Omega_t`` fully local -- every rank draws
+    the same Omega_t = rng.child(t) on its own device (no broadcast);
+  * ONE exchange of the pivot candidates per block: the Schur block
+    ``S = Y[perm[k:]] - T Y[perm[:k]]`` is formed row-parallel (each rank its
+    own remaining candidates, against the all-reduced skeleton rows Y_top)
+    and all-reduced into position order, so every rank runs the SAME exact
+    partial-pivoting panel on the same S (no tournament pivoting; pivots,
+    e_schur and the stop decision are identical on all ranks);
+  * the pivots' interpolation rows T[P_hat] all-reduced once per block for
+    the rank-nc update of the local rows T_g.
+
+The all-reduces carry one nonzero contribution per element (owners write,
+the others write zeros), so they are exact: the result does not depend on
+the reduction order or on the world size.  The position order ``perm`` is
+replicated; T_g stays local and compact (rows = the rank's remaining
+candidates in position order).  At the end ``row_idx = perm[:k]`` is
+global and W stays row-sharded: the rank gets ``W[lo:hi]``.
+
+The per-rank arithmetic is behind a small ops object: `DeviceShardOps`
+(librskel.so kernels, the product path) or a test double.
+"""
+
+import math
+
+import torch
+import torch.distributed as dist
+
+from . import _device, _lib
+from .errors import DimensionError, RankDeficientError
+from .skeleton import (
+    STATUS_NOT_CONVERGED,
+    STATUS_OK,
+    STATUS_RANK_EXHAUSTED,
+    ErrorTrace,
+    SkeletonResult,
+    TraceRecord,
+)
+
+__all__ = ["DeviceShardOps", "rand_lupp_adaptive_sharded", "shard_bounds"]
+
+MAX_BLOCK = 64
+
+
+def shard_bounds(m, world, rank):
+    """Contiguous near-equal split of m candidates: rank -> [lo, hi)."""
+    base, extra = divmod(m, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+class DeviceShardOps:
+    """Per-rank primitives on librskel.so (all on the current stream)."""
+
+    def __init__(self, a_local):
+        self.a = a_local
+        self.dev = _device.device()
+        self.ws = _device.workspace()
+        self.st = _device.stream_handle()
+
+    def f64(self, n):
+        return torch.empty(max(int(n), 1), dtype=torch.float64, device=self.dev)
+
+    def i64(self, n):
+        return torch.empty(max(int(n), 1), dtype=torch.int64, device=self.dev)
+
+    def i32(self, n):
+        return torch.empty(max(int(n), 1), dtype=torch.int32, device=self.dev)
+
+    def sketch(self, rng, t, b, out):
+        m, n = self.a.shape
+        om = _device.gaussian(rng.child(t), n, b)
+        _lib.call("rs_sketch_gemm", m, n, b, self.a.ptr, self.a.ld, int(self.a.colmajor), om.data_ptr(), b,
+                  out.data_ptr(), b, self.ws.data_ptr(), self.st)
+
+    def iota(self, p, n):
+        _lib.call("rs_iota", p.data_ptr(), n, self.st)
+
+    def gather_rows(self, src, lds, idx, n, cols, dst, ldd):
+        _lib.call("rs_gather_rows", src.data_ptr(), lds, idx.data_ptr(), n, cols, dst.data_ptr(), ldd, self.st)
+
+    def scatter_rows(self, src, lds, idx, n, cols, dst, ldd):
+        _lib.call("rs_scatter_rows", src.data_ptr(), lds, idx.data_ptr(), n, cols, dst.data_ptr(), ldd, self.st)
+
+    def schur(self, r, k, b, Tg, Ytop, Y, loc, out):
+        """out (r x b) = Y[loc] - Tg (r x k) @ Ytop (k x b)."""
+        if k == 0:
+            return self.gather_rows(Y, b, loc, r, b, out, b)
+        _lib.call("rs_dgemm", r, b, k, -1.0, Tg.data_ptr(), k, 0, None, Ytop.data_ptr(), b, None, 1.0,
+                  Y.data_ptr(), b, loc.data_ptr(), out.data_ptr(), b, self.ws.data_ptr(), self.st)
+
+    def sumsq(self, X, R, w, out):
+        _lib.call("rs_sumsq", X.data_ptr(), w, R, w, out.data_ptr(), self.ws.data_ptr(), self.st)
+
+    def panel(self, S, R, w, sub, ncols):
+        _lib.call("rs_panel_lupp", S.data_ptr(), w, R, w, sub.data_ptr(), ncols.data_ptr(), self.ws.data_ptr(),
+                  self.st)
+
+    def perm_update(self, perm, perm_new, m, k, sub):
+        _lib.call("rs_perm_update", perm.data_ptr(), perm_new.data_ptr(), m, k, sub.data_ptr(), self.st)
+
+    def maps(self, perm, m, k, lo, hi, lrow_old, sub, k_old, nc, lrow, loc, spos, src_row, wsrc, tp_src,
+             ytop_src, count):
+        p = (lambda x: x.data_ptr() if x is not None else None)
+        _lib.call("rs_shard_maps", perm.data_ptr(), m, k, lo, hi, p(lrow_old), p(sub), k_old, nc, lrow.data_ptr(),
+                  loc.data_ptr(), spos.data_ptr(), p(src_row), p(wsrc), p(tp_src), ytop_src.data_ptr(),
+                  count.data_ptr(), self.st)
+
+    def what(self, S, lds, sub, nc, wsrc, r, linv, out, ldo):
+        """out[i, :nc] = S[wsrc[i]] L1^{-1}, L1 = unit lower part of rows S[sub[:nc]]."""
+        _lib.call("rs_trinv", S.data_ptr(), lds, 1, sub.data_ptr(), nc, 1, 1, linv.data_ptr(), MAX_BLOCK,
+                  self.st)
+        if r > 0:
+            _lib.call("rs_dgemm", r, nc, nc, 1.0, S.data_ptr(), lds, 0, wsrc.data_ptr(), linv.data_ptr(),
+                      MAX_BLOCK, None, 0.0, None, 0, None, out.data_ptr(), ldo, self.ws.data_ptr(), self.st)
+
+    def t_update(self, r, k, nc, Tn, ldn, TP, iota, Tg, src_row):
+        """Tn[:, :k] = Tg[src_row] - Tn[:, k:k+nc] @ TP (nc x k)."""
+        if r == 0:
+            return
+        _lib.call("rs_rank_update", r, k, nc, Tn.data_ptr() + 8 * k, ldn, TP.data_ptr(), k, iota.data_ptr(),
+                  Tg.data_ptr(), k, src_row.data_ptr(), Tn.data_ptr(), ldn, self.st)
+
+    def scatter_interp_local(self, Tg, k, perm, loc, r, lo, hi, W):
+        _lib.call("rs_scatter_interp_local", Tg.data_ptr(), max(k, 1), perm.data_ptr(), k, loc.data_ptr(), r,
+                  lo, hi, W.data_ptr(), max(k, 1), self.st)
+
+    def read(self, *xs):
+        """Host values of small device scalars (one sync)."""
+        return [x.item() for x in xs]
+
+    def output(self, row_idx, w):
+        """Results in the caller's container (numpy in -> numpy out, ...)."""
+        return _device.to_host_index(row_idx, self.a.kind), _device.to_output(w, self.a.kind)
+
+
+def _allreduce(x, group):
+    if dist.get_world_size(group) > 1:
+        dist.all_reduce(x, op=dist.ReduceOp.SUM, group=group)
+
+
+def _row_counts(m_local, group, dev):
+    world = dist.get_world_size(group)
+    mine = torch.tensor([m_local], dtype=torch.int64, device=dev)
+    allc = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
+    dist.all_gather(allc, mine, group=group)
+    return [int(c.item()) for c in allc]
+
+
+def rand_lupp_adaptive_sharded(a_local, b, tau, spec, rng, max_rank=None, group=None, ops=None):
+    """`rand_lupp_adaptive` over ranks that each hold a contiguous block of
+    the candidate rows (rank order = row order).  Same stopping rule, trace
+    and statuses; returns a SkeletonResult whose ``row_idx``/``rank``/
+    ``trace``/``status`` are global (identical on every rank) and whose ``w``
+    holds this rank's rows of W.  Block width b <= 64 (one panel per block).
+    """
+    if ops is None:
+        a_local = _device.as_matrix(a_local)
+        ops = DeviceShardOps(a_local)
+    m_loc, n = ops.a.shape
+    counts = _row_counts(m_loc, group, ops.dev)
+    rank = dist.get_rank(group)
+    lo = sum(counts[:rank])
+    hi = lo + m_loc
+    m = sum(counts)
+    if tau <= 0:
+        raise ValueError(f"tau must be positive, got {tau}")
+    if not 1 <= b <= min(m, n):
+        raise DimensionError(f"block size must be in [1, {min(m, n)}], got {b}")
+    if b > MAX_BLOCK:
+        raise NotImplementedError("the sharded loop factors one panel per block: b <= 64")
+    if spec.kind != "gaussian":
+        raise NotImplementedError(f"sketch kind {spec.kind!r} is outside the B200 hot path (Gaussian only)")
+    if max_rank is None:
+        max_rank = max(b, min(m, n) - b)
+    max_rank = min(max_rank, min(m, n))
+    return _ShardedLoop(ops, group, m, n, lo, hi, b, tau, rng, max_rank).run()
+
+
+class _ShardedLoop:
+    def __init__(self, ops, group, m, n, lo, hi, b, tau, rng, max_rank):
+        self.ops, self.group = ops, group
+        self.m, self.n, self.lo, self.hi = m, n, lo, hi
+        self.b, self.tau, self.rng, self.max_rank = b, tau, rng, max_rank
+        mg = hi - lo
+        kcap = min(max_rank + b, m)
+        o = ops
+        self.perm = [o.i64(m), o.i64(m)]
+        self.lrow = [o.i64(m), o.i64(m)]
+        self.loc, self.spos, self.src_row, self.wsrc = o.i64(mg), o.i64(mg), o.i64(mg), o.i64(mg)
+        self.tp_src, self.ytop_src = o.i64(b), o.i64(kcap)
+        self.count, self.ncols = o.i32(1), o.i32(1)
+        self.sub = o.i64(m)
+        self.iota_b = o.i64(b)
+        o.iota(self.iota_b, b)
+        self.Y = o.f64(mg * b)
+        self.Ytop = o.f64(kcap * b)
+        self.Sg = o.f64(mg * b)
+        self.S = o.f64(m * b)
+        self.TP = o.f64(b * kcap)
+        self.linv = o.f64(MAX_BLOCK * MAX_BLOCK)
+        self.e2 = o.f64(1)
+        pts = {kcap, min(kcap, max(0, m - mg)), min(kcap, m // 2), min(kcap, (m + 1) // 2)}
+        cap = max(1, max(min(mg, m - kk) * kk for kk in pts))
+        self.T = [o.f64(cap), o.f64(cap)]
+        self.cur = 0
+        self.k = 0
+        self.r = mg
+
+    def _schur(self):
+        o, b, k = self.ops, self.b, self.k
+        Tg = self.T[self.cur]
+        if k > 0:
+            o.gather_rows(self.Y, b, self.ytop_src, k, b, self.Ytop, b)
+            _allreduce(self.Ytop[: k * b], self.group)
+        o.schur(self.r, k, b, Tg, self.Ytop, self.Y, self.loc, self.Sg)
+        R = self.m - k
+        S = self.S[: R * b]
+        S.zero_()
+        o.scatter_rows(self.Sg, b, self.spos, self.r, b, S, b)
+        _allreduce(S, self.group)
+        o.sumsq(S, R, b, self.e2)
+
+    def _absorb(self, nc):
+        o, b, m = self.ops, self.b, self.m
+        k_old, cur = self.k, self.cur
+        k_new = k_old + nc
+        nxt = 1 - cur
+        o.perm_update(self.perm[cur], self.perm[nxt], m, k_old, self.sub)
+        o.maps(self.perm[nxt], m, k_new, self.lo, self.hi, self.lrow[cur], self.sub, k_old, nc, self.lrow[nxt],
+               self.loc, self.spos, self.src_row, self.wsrc, self.tp_src, self.ytop_src, self.count)
+        (r_new,) = o.read(self.count)
+        Tg, Tn = self.T[cur], self.T[nxt]
+        if k_old > 0 and nc > 0:
+            o.gather_rows(Tg, k_old, self.tp_src, nc, k_old, self.TP, k_old)
+            _allreduce(self.TP[: nc * k_old], self.group)
+        if nc > 0:
+            o.what(self.S, b, self.sub, nc, self.wsrc, r_new, self.linv, Tn[k_old:], k_new)
+            if k_old > 0:
+                o.t_update(r_new, k_old, nc, Tn, k_new, self.TP, self.iota_b, Tg, self.src_row)
+        self.cur, self.k, self.r = nxt, k_new, r_new
+
+    def run(self):
+        o, b, m, tau = self.ops, self.b, self.m, self.tau
+        o.iota(self.perm[0], m)
+        o.maps(self.perm[0], m, 0, self.lo, self.hi, None, None, 0, 0, self.lrow[0], self.loc, self.spos, None,
+               None, None, self.ytop_src, self.count)
+        trace = ErrorTrace()
+        status = STATUS_NOT_CONVERGED
+        t = 0
+        while True:
+            o.sketch(self.rng, t, b, self.Y)
+            self._schur()
+            (e2,) = o.read(self.e2)
+            if t == 0:
+                # adaptive_init (`skeleton.py:298-314`): full lupp of block 0
+                if not math.isfinite(e2):
+                    raise ValueError("matrix contains non-finite entries")
+            else:
+                e_schur = math.sqrt(e2) if e2 >= 0 else float("nan")
+                trace.append(TraceRecord(k=self.k, e_schur=e_schur))
+                if e_schur <= tau:
+                    status = STATUS_OK
+                    break
+                if self.k + b > self.max_rank:
+                    break
+                if not math.isfinite(e2):
+                    raise ValueError("matrix contains non-finite entries")
+            R = m - self.k
+            o.panel(self.S, R, b, self.sub, self.ncols)
+            (nc,) = o.read(self.ncols)
+            if t == 0 and nc < b:
+                raise RankDeficientError(nc)
+            self._absorb(nc)
+            t += 1
+            if nc < b:
+                status = STATUS_RANK_EXHAUSTED
+                break
+        k = self.k
+        mg = self.hi - self.lo
+        W = o.f64(mg * k)
+        o.scatter_interp_local(self.T[self.cur], k, self.perm[self.cur], self.loc, self.r, self.lo, self.hi, W)
+        row_idx, w = o.output(self.perm[self.cur][:k].clone(), W[: mg * k].view(mg, k))
+        return SkeletonResult(rank=k, row_idx=row_idx, w=w, trace=trace, status=status)
