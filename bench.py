@@ -48,6 +48,8 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--cpu-blocks", type=int, default=8)
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--sharded", action="store_true",
+                   help="column-sharded loop even at 1 GPU (always used when WORLD_SIZE > 1)")
     return p.parse_args()
 
 
@@ -201,14 +203,24 @@ def main():
 
     import paper_2310_09417_b200 as rs
     from paper_2310_09417_b200 import _lib, skeleton
+    from paper_2310_09417_b200.sharded import rand_lupp_adaptive_sharded, shard_bounds
 
     lib = _lib.load()
     n, b, tau = args.n, args.b, args.tau
-    seed = args.seed + rank
+    seed = args.seed
+    sharded = world > 1 or args.sharded
+    # Every rank builds the same matrix and keeps its own column block A[:, lo:hi]
+    # (the column ID's candidates), i.e. A is column-sharded.
     a = gen_fast_decay_device(n, 1e-16, seed, dev)
+    lo, hi = shard_bounds(n, world, rank)
+    if sharded and world > 1:
+        a = a[:, lo:hi].contiguous()
+        torch.cuda.empty_cache()
     spec = rs.SketchSpec("gaussian", n, b)
 
     def step():
+        if sharded:
+            return rand_lupp_adaptive_sharded(a.T, b, tau, spec, rs.RngStream(seed))
         return rs.rand_lupp_adaptive(a.T, b, tau, spec, rs.RngStream(seed))
 
     for _ in range(args.warmup):
@@ -241,12 +253,13 @@ def main():
     ms_max = float(ms_t.item())
     k = res.rank
     f = algo_flops(n, n, k, b)
-    value = world * f / (ms_max * 1e-3) / 1e12
+    value = f / (ms_max * 1e-3) / 1e12  # one n x n problem split over the ranks
 
     phases = timer.totals()
     counts = timer.launches()
     blocks = counts.get("sketch_gemm", 0)
-    sketch_flops = blocks * 2.0 * n * n * b
+    n_loc = a.shape[1]  # candidate columns on this rank
+    sketch_flops = blocks * 2.0 * n * n_loc * b
     sketch_ms = phases.get("sketch_gemm", float("nan"))
     achieved = sketch_flops / (sketch_ms * 1e-3) / 1e12 if sketch_ms else float("nan")
     roofline = {
@@ -254,7 +267,7 @@ def main():
         "achieved": achieved, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
         "frac": achieved / FP64_DMMA_PEAK_TFLOPS, "traffic": None,
         "peak_source": FP64_PEAK_SOURCE,
-        "per_launch_flops": 2.0 * n * n * b,
+        "per_launch_flops": 2.0 * n * n_loc * b,
         "launches": blocks,
         "avg_launch_ms": sketch_ms / max(blocks, 1),
         "share_of_step": sketch_ms / (ms * args.steps),
@@ -262,7 +275,7 @@ def main():
     phase_ms = {kk: v / args.steps for kk, v in phases.items()}
 
     # ---------------- e2e: host numpy in, host numpy out -----------------------
-    a_host_t = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+    a_host_t = torch.empty(tuple(a.shape), dtype=torch.float64, pin_memory=True)
     a_host_t.copy_(a)
     a_host = a_host_t.numpy()
     torch.cuda.synchronize()
@@ -273,7 +286,10 @@ def main():
         res_h = None  # the caller consumed the previous result: its pinned block is reused
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        res_h = rs.rand_lupp_adaptive(a_host.T, b, tau, spec, rs.RngStream(seed))
+        if sharded:
+            res_h = rand_lupp_adaptive_sharded(a_host.T, b, tau, spec, rs.RngStream(seed))
+        else:
+            res_h = rs.rand_lupp_adaptive(a_host.T, b, tau, spec, rs.RngStream(seed))
         torch.cuda.synchronize()
         if i > 0:
             e2e_ms.append(1e3 * (time.perf_counter() - t0))
@@ -283,12 +299,15 @@ def main():
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_ms_max = float(e2e_t.item())
     nblk = len(res_h.trace) + 1
-    h2d = n * n * 8 + nblk * n * b * 8
-    d2h = n * res_h.rank * 8 + res_h.rank * 8 + nblk * 12
-    e2e = {"value": world * algo_flops(n, n, res_h.rank, b) / (e2e_ms_max * 1e-3) / 1e12,
+    # Omega is drawn on the device (no H2D); per-block readbacks: e2 + ncols
+    # (+ the local row count on the sharded loop)
+    h2d = n * n_loc * 8
+    d2h = n_loc * res_h.rank * 8 + res_h.rank * 8 + nblk * (16 if sharded else 12)
+    e2e = {"value": algo_flops(n, n, res_h.rank, b) / (e2e_ms_max * 1e-3) / 1e12,
            "unit": "TFLOP/s", "ms_per_step": e2e_ms_max,
            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-           "path": "rand_lupp_adaptive(numpy pinned A.T) -> numpy W, row_idx"}
+           "path": ("rand_lupp_adaptive_sharded(numpy pinned A[:, J_g].T) -> numpy W[J_g], row_idx" if sharded
+                    else "rand_lupp_adaptive(numpy pinned A.T) -> numpy W, row_idx")}
 
     # ---------------- CPU baseline (rank 0, N = 1 only) -----------------------
     cpu = None
@@ -304,12 +323,14 @@ def main():
             "metric": "adaptive column-ID throughput (algorithmic TFLOP/s)",
             "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
             "config": {
                 "workload": f"cfg2: rand_lupp_adaptive(A.T, b={b}, tau={tau:g} abs) on a {n}x{n} "
                             f"fp64 fast-decay matrix (beta=1e-16, Haar bases), seed {args.seed}",
                 "n": n, "b": b, "tau": tau, "rank": k, "status": res.status,
-                "blocks": len(res.trace) + 1, "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                "blocks": len(res.trace) + 1, "parallelism": (f"A column-sharded over {world} GPUs (NCCL all-reduce of Y_top, S, T_P per block)"
+                                if sharded else "1 GPU"),
                 "l2": "inputs (A: %.1f GB) larger than L2 between steps" % (n * n * 8 / 1e9),
             },
             "seconds_per_step": ms_max / 1e3,

@@ -74,9 +74,12 @@ class DeviceShardOps:
     def i32(self, n):
         return torch.empty(max(int(n), 1), dtype=torch.int32, device=self.dev)
 
-    def sketch(self, rng, t, b, out):
+    def omega(self, rng, t, b):
+        """Omega_t = rng.child(t) Gaussian block (n x b), drawn on this device."""
+        return _device.gaussian(rng.child(t), self.a.shape[1], b)
+
+    def sketch(self, om, b, out):
         m, n = self.a.shape
-        om = _device.gaussian(rng.child(t), n, b)
         _lib.call("rs_sketch_gemm", m, n, b, self.a.ptr, self.a.ld, int(self.a.colmajor), om.data_ptr(), b,
                   out.data_ptr(), b, self.ws.data_ptr(), self.st)
 
@@ -141,13 +144,22 @@ class DeviceShardOps:
         return _device.to_host_index(row_idx, self.a.kind), _device.to_output(w, self.a.kind)
 
 
+def _world(group):
+    """(world size, rank); a process without a process group is rank 0 of 1."""
+    if not dist.is_available() or not dist.is_initialized():
+        return 1, 0
+    return dist.get_world_size(group), dist.get_rank(group)
+
+
 def _allreduce(x, group):
-    if dist.get_world_size(group) > 1:
+    if _world(group)[0] > 1:
         dist.all_reduce(x, op=dist.ReduceOp.SUM, group=group)
 
 
 def _row_counts(m_local, group, dev):
-    world = dist.get_world_size(group)
+    world = _world(group)[0]
+    if world == 1:
+        return [m_local]
     mine = torch.tensor([m_local], dtype=torch.int64, device=dev)
     allc = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
     dist.all_gather(allc, mine, group=group)
@@ -166,7 +178,7 @@ def rand_lupp_adaptive_sharded(a_local, b, tau, spec, rng, max_rank=None, group=
         ops = DeviceShardOps(a_local)
     m_loc, n = ops.a.shape
     counts = _row_counts(m_loc, group, ops.dev)
-    rank = dist.get_rank(group)
+    rank = _world(group)[1]
     lo = sum(counts[:rank])
     hi = lo + m_loc
     m = sum(counts)
@@ -255,9 +267,17 @@ class _ShardedLoop:
         trace = ErrorTrace()
         status = STATUS_NOT_CONVERGED
         t = 0
+        from . import skeleton
+
+        prof = skeleton._PHASE_TIMER or skeleton._NullTimer()
         while True:
-            o.sketch(self.rng, t, b, self.Y)
+            om = o.omega(self.rng, t, b)
+            tok = prof.start("sketch_gemm")
+            o.sketch(om, b, self.Y)
+            prof.stop(tok)
+            tok = prof.start("schur_exchange")
             self._schur()
+            prof.stop(tok)
             (e2,) = o.read(self.e2)
             if t == 0:
                 # adaptive_init (`skeleton.py:298-314`): full lupp of block 0
@@ -274,11 +294,15 @@ class _ShardedLoop:
                 if not math.isfinite(e2):
                     raise ValueError("matrix contains non-finite entries")
             R = m - self.k
+            tok = prof.start("panel")
             o.panel(self.S, R, b, self.sub, self.ncols)
+            prof.stop(tok)
             (nc,) = o.read(self.ncols)
             if t == 0 and nc < b:
                 raise RankDeficientError(nc)
+            tok = prof.start("absorb")
             self._absorb(nc)
+            prof.stop(tok)
             t += 1
             if nc < b:
                 status = STATUS_RANK_EXHAUSTED

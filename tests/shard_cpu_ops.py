@@ -36,9 +36,11 @@ class CpuShardOps:
     def i32(self, n):
         return torch.zeros(max(int(n), 1), dtype=torch.int32)
 
-    def sketch(self, rng, t, b, out):
+    def omega(self, rng, t, b):
+        return orc.gaussian(self.seed, orc.child_stream(self.stream, t), self.a.shape[1], b)
+
+    def sketch(self, om, b, out):
         m, n = self.a.shape
-        om = orc.gaussian(self.seed, orc.child_stream(self.stream, t), n, b)
         _np(out)[: m * b] = (self.a @ om).ravel()
 
     def iota(self, p, n):
