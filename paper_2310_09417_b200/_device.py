@@ -130,24 +130,89 @@ def as_matrix(a, name="matrix"):
         if a.dim() != 2:
             raise DimensionError(f"{name} must be 2-dimensional, got shape {tuple(a.shape)}")
         kind = "torch_cuda" if a.is_cuda else "torch_cpu"
+        if not a.is_cuda:
+            if a.dtype not in (torch.float32, torch.float64):
+                a = a.to(torch.float64)
+            if a.t().is_contiguous() and not a.is_contiguous():
+                a = h2d(a.t().numpy()).t()
+            else:
+                a = h2d(a.contiguous().numpy())
         if a.dtype != torch.float64:
             a = a.to(torch.float64)
-        if not a.is_cuda:
-            a = a.contiguous() if not (a.is_contiguous() or a.t().is_contiguous()) else a
-            a = a.to(dev)
         return _from_tensor_2d(a, kind)
-    arr = np.asarray(a, dtype=np.float64)
+    arr = np.asarray(a)
+    if arr.dtype not in (np.float32, np.float64):
+        arr = arr.astype(np.float64)
     if arr.ndim != 2:
         raise DimensionError(f"{name} must be 2-dimensional, got shape {arr.shape}")
-    if arr.flags.c_contiguous:
-        t = torch.as_tensor(arr).to(dev)
-        return Matrix(t, arr.shape[0], arr.shape[1], max(arr.shape[1], 1), False, "numpy")
-    if arr.flags.f_contiguous:
-        t = torch.as_tensor(arr.T).to(dev)
-        return Matrix(t, arr.shape[0], arr.shape[1], max(arr.shape[0], 1), True, "numpy")
-    arr = np.ascontiguousarray(arr)
-    t = torch.as_tensor(arr).to(dev)
-    return Matrix(t, arr.shape[0], arr.shape[1], max(arr.shape[1], 1), False, "numpy")
+    if not (arr.flags.c_contiguous or arr.flags.f_contiguous):
+        arr = np.ascontiguousarray(arr)
+    colmajor = not arr.flags.c_contiguous
+    t = h2d(arr.T if colmajor else arr)
+    if t.dtype != torch.float64:  # fp32 input: upcast on the device (half the H2D bytes)
+        t = t.to(torch.float64)
+    rows, cols = arr.shape
+    return Matrix(t, rows, cols, max(rows if colmajor else cols, 1), colmajor, "numpy")
+
+
+# ------------------------------------------------------------- host -> device --
+_STAGE_BYTES = 32 << 20
+_STAGE_DEPTH = 4
+_stage = {}
+
+
+def _stage_ring(dev):
+    ring = _stage.get(dev.index)
+    if ring is None:
+        ring = {
+            "bufs": [torch.empty(_STAGE_BYTES, dtype=torch.uint8, pin_memory=True) for _ in range(_STAGE_DEPTH)],
+            "events": [None] * _STAGE_DEPTH,
+            "stream": torch.cuda.Stream(device=dev),
+        }
+        _stage[dev.index] = ring
+    return ring
+
+
+def _copy_pool():
+    from . import _omega
+    return _omega._pool()
+
+
+def h2d(arr):
+    """Device copy of a C-contiguous host array.  Page-locked memory goes
+    straight to DMA; pageable memory (a user's numpy array) is staged through
+    a ring of pinned 32 MB chunks that host threads fill while earlier chunks
+    are in flight, instead of the driver's synchronous pageable path."""
+    dev = device()
+    host = torch.from_numpy(arr)
+    nbytes = arr.nbytes
+    if nbytes < (8 << 20) or host.is_pinned():
+        return host.to(dev, non_blocking=host.is_pinned())
+    out = torch.empty(arr.shape, dtype=host.dtype, device=dev)
+    src = arr.reshape(-1).view(np.uint8)
+    dst = out.view(-1).view(torch.uint8)
+    ring = _stage_ring(dev)
+    pool = _copy_pool()
+    nthr = max(1, min(8, pool._max_workers))
+    cs = ring["stream"]
+    cs.wait_stream(torch.cuda.current_stream(dev))  # `out` was allocated on the compute stream
+    for i, c0 in enumerate(range(0, nbytes, _STAGE_BYTES)):
+        c1 = min(nbytes, c0 + _STAGE_BYTES)
+        slot = i % _STAGE_DEPTH
+        ev = ring["events"][slot]
+        if ev is not None:
+            ev.synchronize()
+        buf = ring["bufs"][slot].numpy()
+        step = -(-(c1 - c0) // nthr)
+        parts = [(p0, min(c1 - c0, p0 + step)) for p0 in range(0, c1 - c0, step)]
+        list(pool.map(lambda pr: np.copyto(buf[pr[0]:pr[1]], src[c0 + pr[0]:c0 + pr[1]]), parts))
+        with torch.cuda.stream(cs):
+            dst[c0:c1].copy_(ring["bufs"][slot][: c1 - c0], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(cs)
+        ring["events"][slot] = ev
+    torch.cuda.current_stream(dev).wait_stream(cs)
+    return out
 
 
 def as_index(idx, kind):
