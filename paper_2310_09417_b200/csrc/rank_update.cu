@@ -230,7 +230,7 @@ constexpr int UTHREADS = 256;                       // 8 warps: 2 (M) x 4 (N), w
 constexpr int UWM = 2, UWN = 4, UWTM = UBM / UWM, UWTN = UBN / UWN;
 constexpr int UMT = UWTM / 16, UNT = UWTN / 8;      // 2 x 2 m16n8 tiles per warp
 constexpr int UA_LD = UK + 4, UB_LD = UBN + 4;      // = 4 (mod 16): conflict-free fragment loads
-constexpr size_t U_SMEM = sizeof(double) * (UBM * UA_LD + 2 * UK * UB_LD);
+constexpr size_t U_SMEM = sizeof(double) * (UBM * UA_LD + 2 * UK * UB_LD) + sizeof(long long) * UK;
 
 template <bool VEC2>
 __device__ __forceinline__ void ru_copy(double* dst, const double* src, int valid) {
@@ -261,6 +261,9 @@ __global__ void __launch_bounds__(UTHREADS, 2) rank_update_kernel(RankUpdatePara
   extern __shared__ __align__(16) double usm[];
   double* As = usm;                  // [UBM][UA_LD]
   double* Bs = usm + UBM * UA_LD;    // [2][UK][UB_LD]
+  // B row offsets (bidx is fixed for the launch): one global load per row per
+  // CTA instead of one dependent load per copied element.
+  long long* brow = reinterpret_cast<long long*>(Bs + 2 * UK * UB_LD);  // [UK]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int wm = (warp % UWM) * UWTM, wn = (warp / UWM) * UWTN;
@@ -268,6 +271,8 @@ __global__ void __launch_bounds__(UTHREADS, 2) rank_update_kernel(RankUpdatePara
   const int t0 = (int)((long long)c * p.tiles / G), t1 = (int)((long long)(c + 1) * p.tiles / G);
   if (t0 >= t1) return;
   constexpr int V = VEC2 ? 2 : 1;
+  for (int r = tid; r < UK; r += UTHREADS) brow[r] = r < p.K ? p.bidx[r] * p.ldb : 0;
+  __syncthreads();
 
   auto load_A = [&](int m0) {
     for (int e = tid; e < UBM * (UK / V); e += UTHREADS) {
@@ -283,11 +288,24 @@ __global__ void __launch_bounds__(UTHREADS, 2) rank_update_kernel(RankUpdatePara
       const int r = e / (UBN / V), nc = (e % (UBN / V)) * V;
       const int gn = n0 + nc;
       const int valid = (r < p.K && gn < p.N) ? min(V, p.N - gn) : 0;
-      ru_copy<VEC2>(bs + r * UB_LD + nc, valid ? p.B + p.bidx[r] * p.ldb + gn : p.B, valid);
+      ru_copy<VEC2>(bs + r * UB_LD + nc, valid ? p.B + brow[r] + gn : p.B, valid);
     }
+  };
+  // Cin row pointers of this thread's 2 x UMT accumulator rows: they change
+  // only with the strip, so the gathered-index loads leave the tile loop.
+  const double* crow[UMT][2];
+  auto set_rows = [&](int m0) {
+#pragma unroll
+    for (int i = 0; i < UMT; ++i)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int gm = m0 + wm + 16 * i + g + 8 * h;
+        crow[i][h] = gm < p.M ? p.Cin + p.cidx[gm] * p.ldcin : nullptr;
+      }
   };
 
   int strip = t0 / p.tiles_n;
+  set_rows(strip * UBM);
   load_A(strip * UBM);
   load_B((t0 % p.tiles_n) * UBN, 0);
   cp_async_commit();
@@ -298,6 +316,7 @@ __global__ void __launch_bounds__(UTHREADS, 2) rank_update_kernel(RankUpdatePara
     if (tstrip != strip) {
       __syncthreads();
       strip = tstrip;
+      set_rows(m0);
       load_A(m0);
       cp_async_commit();
     }
@@ -306,18 +325,17 @@ __global__ void __launch_bounds__(UTHREADS, 2) rank_update_kernel(RankUpdatePara
     for (int i = 0; i < UMT; ++i)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int gm = m0 + wm + 16 * i + g + 8 * h;
-        const double* crow = gm < p.M ? p.Cin + p.cidx[gm] * p.ldcin : nullptr;
+        const double* cr = crow[i][h];
 #pragma unroll
         for (int j = 0; j < UNT; ++j) {
           const int gn = n0 + wn + 8 * j + 2 * t;
-          if (VEC2 && crow != nullptr && gn + 1 < p.N) {
-            const double2 v = ldnc2(crow + gn);
+          if (VEC2 && cr != nullptr && gn + 1 < p.N) {
+            const double2 v = ldnc2(cr + gn);
             cin[i][h][j][0] = v.x;
             cin[i][h][j][1] = v.y;
           } else {
-            cin[i][h][j][0] = (crow != nullptr && gn < p.N) ? ldnc1(crow + gn) : 0.0;
-            cin[i][h][j][1] = (crow != nullptr && gn + 1 < p.N) ? ldnc1(crow + gn + 1) : 0.0;
+            cin[i][h][j][0] = (cr != nullptr && gn < p.N) ? ldnc1(cr + gn) : 0.0;
+            cin[i][h][j][1] = (cr != nullptr && gn + 1 < p.N) ? ldnc1(cr + gn + 1) : 0.0;
           }
         }
       }
@@ -355,21 +373,152 @@ __global__ void __launch_bounds__(UTHREADS, 2) rank_update_kernel(RankUpdatePara
       for (int h = 0; h < 2; ++h) {
         const int gm = m0 + wm + 16 * i + g + 8 * h;
         if (gm >= p.M) continue;
-        double* crow = p.C + (long long)gm * p.ldc;
+        double* cw = p.C + (long long)gm * p.ldc;
 #pragma unroll
         for (int j = 0; j < UNT; ++j) {
           const int gn = n0 + wn + 8 * j + 2 * t;
           const double v0 = cin[i][h][j][0] - acc[i][j][2 * h];
           const double v1 = cin[i][h][j][1] - acc[i][j][2 * h + 1];
           if (VEC2 && gn + 1 < p.N) {
-            *reinterpret_cast<double2*>(crow + gn) = make_double2(v0, v1);
+            *reinterpret_cast<double2*>(cw + gn) = make_double2(v0, v1);
           } else {
-            if (gn < p.N) crow[gn] = v0;
-            if (gn + 1 < p.N) crow[gn + 1] = v1;
+            if (gn < p.N) cw[gn] = v0;
+            if (gn + 1 < p.N) cw[gn + 1] = v1;
           }
         }
       }
     __syncthreads();
+  }
+  cp_async_wait<0>();
+}
+
+// ------------------------------------------------- streaming kernel (v3) --
+// One CTA per SM walks its contiguous range of 64 x 64 output tiles
+// (strip-major).  The A strip (64 x K, W_hat) lives in registers as DMMA
+// fragments for the whole strip; the B chunk (K x 64, gathered rows of
+// T[P_hat]) and the Cin chunk (64 x 64, gathered rows of T[Q_hat]) stream
+// through a 3-stage cp.async ring, so the HBM reads of tile i+2 are in flight
+// while tile i is multiplied; C = Cin - A B leaves from registers with 16-byte
+// stores.  8 warps: 4 (M, 16 rows) x 2 (N, 32 cols); 4 independent
+// accumulators per warp.  B rows at ld 68 (= 4 mod 16: conflict-free 64-bit
+// fragment loads), Cin rows at ld 72 (= 8 mod 16: conflict-free 128-bit
+// epilogue loads).
+constexpr int R3_BM = 64, R3_BN = 64, R3_K = 64, R3_STAGES = 3, R3_THREADS = 256;
+constexpr int R3_BLD = R3_BN + 4, R3_CLD = R3_BN + 8;
+constexpr int R3_STAGE = R3_K * R3_BLD + R3_BM * R3_CLD;  // doubles
+constexpr size_t R3_SMEM = sizeof(double) * R3_STAGES * R3_STAGE;
+constexpr int R3_CHUNKS = R3_BM * R3_BN / 2 / R3_THREADS;  // 16-byte chunks per thread per operand (8)
+
+__global__ void __launch_bounds__(R3_THREADS, 1) rank_update_stream_kernel(RankUpdateParams p) {
+  extern __shared__ __align__(16) double r3sm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp & 3) * 16, wn = (warp >> 2) * 32;
+  const int G = gridDim.x, c = blockIdx.x;
+  const int t0 = (int)((long long)c * p.tiles / G), t1 = (int)((long long)(c + 1) * p.tiles / G);
+  if (t0 >= t1) return;
+  const int ntile = t1 - t0;
+
+  // copy geometry: chunk q = tid + 256 i -> row q / 32 (32 chunks = 64 doubles
+  // per row), 16-byte column (q % 32) * 2
+  const int crow0 = tid >> 5, ccol = (tid & 31) * 2;
+  long long boff[R3_CHUNKS];  // B row offsets: bidx is fixed for the launch
+#pragma unroll
+  for (int i = 0; i < R3_CHUNKS; ++i) {
+    const int r = crow0 + 8 * i;
+    boff[i] = r < p.K ? p.bidx[r] * p.ldb : -1;
+  }
+  long long coff[R3_CHUNKS];  // Cin row offsets of the prefetch strip
+  int pf_strip = -1;
+
+  auto issue = [&](int li) {  // loads of local tile li into stage li % S
+    const int tile = t0 + li;
+    const int strip = tile / p.tiles_n;
+    const int m0 = strip * R3_BM, n0 = (tile - strip * p.tiles_n) * R3_BN;
+    if (strip != pf_strip) {
+      pf_strip = strip;
+#pragma unroll
+      for (int i = 0; i < R3_CHUNKS; ++i) {
+        const int gm = m0 + crow0 + 8 * i;
+        coff[i] = gm < p.M ? p.cidx[gm] * p.ldcin : -1;
+      }
+    }
+    double* st = r3sm + (li % R3_STAGES) * R3_STAGE;
+    double* bs = st;
+    double* cs = st + R3_K * R3_BLD;
+    const int gn = n0 + ccol;
+    const int nv = gn < p.N ? min(2, p.N - gn) : 0;
+#pragma unroll
+    for (int i = 0; i < R3_CHUNKS; ++i) {
+      const int r = crow0 + 8 * i;
+      const bool bv = boff[i] >= 0 && nv > 0;
+      cp_async16(bs + r * R3_BLD + ccol, bv ? p.B + boff[i] + gn : p.B, bv ? nv * 8 : 0);
+      const bool cv = coff[i] >= 0 && nv > 0;
+      cp_async16(cs + r * R3_CLD + ccol, cv ? p.Cin + coff[i] + gn : p.Cin, cv ? nv * 8 : 0);
+    }
+  };
+
+  double af[16][2];  // A fragments of this warp's 16 rows, all K/4 k-steps
+  int a_strip = -1;
+
+#pragma unroll
+  for (int s = 0; s < R3_STAGES - 1; ++s) {
+    if (s < ntile) issue(s);
+    cp_async_commit();
+  }
+  for (int li = 0; li < ntile; ++li) {
+    const int tile = t0 + li;
+    const int strip = tile / p.tiles_n;
+    const int m0 = strip * R3_BM, n0 = (tile - strip * p.tiles_n) * R3_BN;
+    if (strip != a_strip) {  // new strip: A fragments straight from global
+      a_strip = strip;
+      const int r0 = m0 + wm + g, r1 = r0 + 8;
+#pragma unroll
+      for (int ks = 0; ks < 16; ++ks) {
+        const int kc = 4 * ks + t;
+        af[ks][0] = (r0 < p.M && kc < p.K) ? p.A[(long long)r0 * p.lda + kc] : 0.0;
+        af[ks][1] = (r1 < p.M && kc < p.K) ? p.A[(long long)r1 * p.lda + kc] : 0.0;
+      }
+    }
+    cp_async_wait<R3_STAGES - 2>();
+    __syncthreads();
+    if (li + R3_STAGES - 1 < ntile) issue(li + R3_STAGES - 1);
+    cp_async_commit();
+    const double* st = r3sm + (li % R3_STAGES) * R3_STAGE;
+    const double* bs = st;
+    const double* cs = st + R3_K * R3_BLD;
+    double acc[4][4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[j][e] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < 16; ++ks) {
+      double b[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = bs[(4 * ks + t) * R3_BLD + wn + 8 * j + g];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma_16x8x4(acc[j], af[ks][0], af[ks][1], b[j]);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int lr = wm + g + 8 * h;
+      const int gm = m0 + lr;
+      if (gm >= p.M) continue;
+      double* cw = p.C + (long long)gm * p.ldc;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int ln = wn + 8 * j + 2 * t;
+        const int gn = n0 + ln;
+        const double2 ci = *reinterpret_cast<const double2*>(cs + lr * R3_CLD + ln);
+        const double v0 = ci.x - acc[j][2 * h], v1 = ci.y - acc[j][2 * h + 1];
+        if (gn + 1 < p.N) {
+          *reinterpret_cast<double2*>(cw + gn) = make_double2(v0, v1);
+        } else if (gn < p.N) {
+          cw[gn] = v0;
+        }
+      }
+    }
   }
   cp_async_wait<0>();
 }
@@ -392,7 +541,22 @@ int launch_rank_update(int M, int N, int K, const double* A, long long lda, cons
     const char* e = getenv("RSKEL_RU_BULK");
     return e != nullptr && e[0] == '1';
   }();
-  if (bulk_ok && prefer_bulk) {
+  static const int ru_kernel = [] {
+    const char* e = getenv("RSKEL_RU_KERNEL");  // 0: 2-CTA cp.async, 1: bulk, 3: streaming (default)
+    return e != nullptr ? atoi(e) : 3;
+  }();
+  const bool stream_ok = bulk_ok && K <= R3_K && ldb % 2 == 0;
+  if (stream_ok && ru_kernel == 3 && !prefer_bulk) {
+    p.tiles_n = (N + R3_BN - 1) / R3_BN;
+    p.tiles = p.tiles_n * ((M + R3_BM - 1) / R3_BM);
+    const int G = p.tiles < nsm ? p.tiles : nsm;
+    static bool configured3 = false;
+    if (!configured3) {
+      cudaFuncSetAttribute(rank_update_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)R3_SMEM);
+      configured3 = true;
+    }
+    rank_update_stream_kernel<<<G, R3_THREADS, R3_SMEM, st>>>(p);
+  } else if (bulk_ok && (prefer_bulk || ru_kernel == 1)) {
     p.tiles_n = (N + WBN - 1) / WBN;
     p.tiles = p.tiles_n * ((M + WBM - 1) / WBM);
     const int G = p.tiles < nsm ? p.tiles : nsm;
