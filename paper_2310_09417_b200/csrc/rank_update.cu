@@ -403,17 +403,26 @@ __global__ void __launch_bounds__(UTHREADS, 2) rank_update_kernel(RankUpdatePara
 // accumulators per warp.  B rows at ld 68 (= 4 mod 16: conflict-free 64-bit
 // fragment loads), Cin rows at ld 72 (= 8 mod 16: conflict-free 128-bit
 // epilogue loads).
-constexpr int R3_BM = 64, R3_BN = 64, R3_K = 64, R3_STAGES = 3, R3_THREADS = 256;
-constexpr int R3_BLD = R3_BN + 4, R3_CLD = R3_BN + 8;
-constexpr int R3_STAGE = R3_K * R3_BLD + R3_BM * R3_CLD;  // doubles
-constexpr size_t R3_SMEM = sizeof(double) * R3_STAGES * R3_STAGE;
-constexpr int R3_CHUNKS = R3_BM * R3_BN / 2 / R3_THREADS;  // 16-byte chunks per thread per operand (8)
+template <int BM, int WARPS_N, int STAGES>
+struct R3Cfg {
+  static constexpr int BN = 64, K = 64, THREADS = 256;
+  static constexpr int WARPS_M = 8 / WARPS_N;
+  static_assert(WARPS_M * 16 == BM, "8 warps: BM = 16 * warps along M");
+  static constexpr int NT = BN / 8 / WARPS_N;  // n8 accumulators per warp
+  static constexpr int BLD = BN + 4, CLD = BN + 8;
+  static constexpr int STAGE = K * BLD + BM * CLD;  // doubles
+  static constexpr size_t SMEM = sizeof(double) * STAGES * STAGE;
+  static constexpr int BCH = K * BN / 2 / THREADS;   // 16-byte B chunks per thread (8)
+  static constexpr int CCH = BM * BN / 2 / THREADS;  // 16-byte Cin chunks per thread
+};
 
-__global__ void __launch_bounds__(R3_THREADS, 1) rank_update_stream_kernel(RankUpdateParams p) {
+template <int BM, int WARPS_N, int STAGES>
+__global__ void __launch_bounds__(256, 1) rank_update_stream_kernel(RankUpdateParams p) {
+  using C = R3Cfg<BM, WARPS_N, STAGES>;
   extern __shared__ __align__(16) double r3sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int wm = (warp & 3) * 16, wn = (warp >> 2) * 32;
+  const int wm = (warp % C::WARPS_M) * 16, wn = (warp / C::WARPS_M) * (C::BN / WARPS_N);
   const int G = gridDim.x, c = blockIdx.x;
   const int t0 = (int)((long long)c * p.tiles / G), t1 = (int)((long long)(c + 1) * p.tiles / G);
   if (t0 >= t1) return;
@@ -422,39 +431,41 @@ __global__ void __launch_bounds__(R3_THREADS, 1) rank_update_stream_kernel(RankU
   // copy geometry: chunk q = tid + 256 i -> row q / 32 (32 chunks = 64 doubles
   // per row), 16-byte column (q % 32) * 2
   const int crow0 = tid >> 5, ccol = (tid & 31) * 2;
-  long long boff[R3_CHUNKS];  // B row offsets: bidx is fixed for the launch
+  long long boff[C::BCH];  // B row offsets: bidx is fixed for the launch
 #pragma unroll
-  for (int i = 0; i < R3_CHUNKS; ++i) {
+  for (int i = 0; i < C::BCH; ++i) {
     const int r = crow0 + 8 * i;
     boff[i] = r < p.K ? p.bidx[r] * p.ldb : -1;
   }
-  long long coff[R3_CHUNKS];  // Cin row offsets of the prefetch strip
+  long long coff[C::CCH];  // Cin row offsets of the prefetch strip
   int pf_strip = -1;
 
-  auto issue = [&](int li) {  // loads of local tile li into stage li % S
+  auto issue = [&](int li) {  // loads of local tile li into stage li % STAGES
     const int tile = t0 + li;
     const int strip = tile / p.tiles_n;
-    const int m0 = strip * R3_BM, n0 = (tile - strip * p.tiles_n) * R3_BN;
+    const int m0 = strip * BM, n0 = (tile - strip * p.tiles_n) * C::BN;
     if (strip != pf_strip) {
       pf_strip = strip;
 #pragma unroll
-      for (int i = 0; i < R3_CHUNKS; ++i) {
+      for (int i = 0; i < C::CCH; ++i) {
         const int gm = m0 + crow0 + 8 * i;
         coff[i] = gm < p.M ? p.cidx[gm] * p.ldcin : -1;
       }
     }
-    double* st = r3sm + (li % R3_STAGES) * R3_STAGE;
+    double* st = r3sm + (li % STAGES) * C::STAGE;
     double* bs = st;
-    double* cs = st + R3_K * R3_BLD;
+    double* cs = st + C::K * C::BLD;
     const int gn = n0 + ccol;
     const int nv = gn < p.N ? min(2, p.N - gn) : 0;
 #pragma unroll
-    for (int i = 0; i < R3_CHUNKS; ++i) {
-      const int r = crow0 + 8 * i;
+    for (int i = 0; i < C::BCH; ++i) {
       const bool bv = boff[i] >= 0 && nv > 0;
-      cp_async16(bs + r * R3_BLD + ccol, bv ? p.B + boff[i] + gn : p.B, bv ? nv * 8 : 0);
+      cp_async16(bs + (crow0 + 8 * i) * C::BLD + ccol, bv ? p.B + boff[i] + gn : p.B, bv ? nv * 8 : 0);
+    }
+#pragma unroll
+    for (int i = 0; i < C::CCH; ++i) {
       const bool cv = coff[i] >= 0 && nv > 0;
-      cp_async16(cs + r * R3_CLD + ccol, cv ? p.Cin + coff[i] + gn : p.Cin, cv ? nv * 8 : 0);
+      cp_async16(cs + (crow0 + 8 * i) * C::CLD + ccol, cv ? p.Cin + coff[i] + gn : p.Cin, cv ? nv * 8 : 0);
     }
   };
 
@@ -462,14 +473,14 @@ __global__ void __launch_bounds__(R3_THREADS, 1) rank_update_stream_kernel(RankU
   int a_strip = -1;
 
 #pragma unroll
-  for (int s = 0; s < R3_STAGES - 1; ++s) {
+  for (int s = 0; s < STAGES - 1; ++s) {
     if (s < ntile) issue(s);
     cp_async_commit();
   }
   for (int li = 0; li < ntile; ++li) {
     const int tile = t0 + li;
     const int strip = tile / p.tiles_n;
-    const int m0 = strip * R3_BM, n0 = (tile - strip * p.tiles_n) * R3_BN;
+    const int m0 = strip * BM, n0 = (tile - strip * p.tiles_n) * C::BN;
     if (strip != a_strip) {  // new strip: A fragments straight from global
       a_strip = strip;
       const int r0 = m0 + wm + g, r1 = r0 + 8;
@@ -480,25 +491,25 @@ __global__ void __launch_bounds__(R3_THREADS, 1) rank_update_stream_kernel(RankU
         af[ks][1] = (r1 < p.M && kc < p.K) ? p.A[(long long)r1 * p.lda + kc] : 0.0;
       }
     }
-    cp_async_wait<R3_STAGES - 2>();
+    cp_async_wait<STAGES - 2>();
     __syncthreads();
-    if (li + R3_STAGES - 1 < ntile) issue(li + R3_STAGES - 1);
+    if (li + STAGES - 1 < ntile) issue(li + STAGES - 1);
     cp_async_commit();
-    const double* st = r3sm + (li % R3_STAGES) * R3_STAGE;
+    const double* st = r3sm + (li % STAGES) * C::STAGE;
     const double* bs = st;
-    const double* cs = st + R3_K * R3_BLD;
-    double acc[4][4];
+    const double* cs = st + C::K * C::BLD;
+    double acc[C::NT][4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < C::NT; ++j)
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[j][e] = 0.0;
 #pragma unroll
     for (int ks = 0; ks < 16; ++ks) {
-      double b[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = bs[(4 * ks + t) * R3_BLD + wn + 8 * j + g];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) dmma_16x8x4(acc[j], af[ks][0], af[ks][1], b[j]);
+      for (int j = 0; j < C::NT; ++j) {
+        const double b = bs[(4 * ks + t) * C::BLD + wn + 8 * j + g];
+        dmma_16x8x4(acc[j], af[ks][0], af[ks][1], b);
+      }
     }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -507,10 +518,10 @@ __global__ void __launch_bounds__(R3_THREADS, 1) rank_update_stream_kernel(RankU
       if (gm >= p.M) continue;
       double* cw = p.C + (long long)gm * p.ldc;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < C::NT; ++j) {
         const int ln = wn + 8 * j + 2 * t;
         const int gn = n0 + ln;
-        const double2 ci = *reinterpret_cast<const double2*>(cs + lr * R3_CLD + ln);
+        const double2 ci = *reinterpret_cast<const double2*>(cs + lr * C::CLD + ln);
         const double v0 = ci.x - acc[j][2 * h], v1 = ci.y - acc[j][2 * h + 1];
         if (gn + 1 < p.N) {
           *reinterpret_cast<double2*>(cw + gn) = make_double2(v0, v1);
@@ -521,6 +532,21 @@ __global__ void __launch_bounds__(R3_THREADS, 1) rank_update_stream_kernel(RankU
     }
   }
   cp_async_wait<0>();
+}
+
+template <int BM, int WARPS_N, int STAGES>
+static void launch_stream(RankUpdateParams p, int nsm, cudaStream_t st) {
+  using C = R3Cfg<BM, WARPS_N, STAGES>;
+  p.tiles_n = (p.N + C::BN - 1) / C::BN;
+  p.tiles = p.tiles_n * ((p.M + BM - 1) / BM);
+  const int G = p.tiles < nsm ? p.tiles : nsm;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(rank_update_stream_kernel<BM, WARPS_N, STAGES>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    configured = true;
+  }
+  rank_update_stream_kernel<BM, WARPS_N, STAGES><<<G, 256, C::SMEM, st>>>(p);
 }
 
 int launch_rank_update(int M, int N, int K, const double* A, long long lda, const double* B,
@@ -542,20 +568,16 @@ int launch_rank_update(int M, int N, int K, const double* A, long long lda, cons
     return e != nullptr && e[0] == '1';
   }();
   static const int ru_kernel = [] {
-    const char* e = getenv("RSKEL_RU_KERNEL");  // 0: 2-CTA cp.async, 1: bulk, 3: streaming (default)
+    // 0: 2-CTA cp.async, 1: bulk, 3: streaming 128 x 64 tiles (default), 4: streaming 64 x 64
+    const char* e = getenv("RSKEL_RU_KERNEL");
     return e != nullptr ? atoi(e) : 3;
   }();
-  const bool stream_ok = bulk_ok && K <= R3_K && ldb % 2 == 0;
-  if (stream_ok && ru_kernel == 3 && !prefer_bulk) {
-    p.tiles_n = (N + R3_BN - 1) / R3_BN;
-    p.tiles = p.tiles_n * ((M + R3_BM - 1) / R3_BM);
-    const int G = p.tiles < nsm ? p.tiles : nsm;
-    static bool configured3 = false;
-    if (!configured3) {
-      cudaFuncSetAttribute(rank_update_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)R3_SMEM);
-      configured3 = true;
-    }
-    rank_update_stream_kernel<<<G, R3_THREADS, R3_SMEM, st>>>(p);
+  const bool stream_ok = bulk_ok && K <= 64;
+  if (stream_ok && (ru_kernel == 3 || ru_kernel == 4) && !prefer_bulk) {
+    if (ru_kernel == 4)
+      launch_stream<64, 2, 3>(p, nsm, st);
+    else
+      launch_stream<128, 1, 2>(p, nsm, st);
   } else if (bulk_ok && (prefer_bulk || ru_kernel == 1)) {
     p.tiles_n = (N + WBN - 1) / WBN;
     p.tiles = p.tiles_n * ((M + WBM - 1) / WBM);
