@@ -60,6 +60,9 @@ using Cfg5 = GemmCfg<64, 64, 16, 2, 2, 4, 4>;    // 4 warps of 32x32, 4 CTAs/SM
 using Cfg6 = GemmCfg<128, 64, 16, 2, 2, 3, 2>;   // 4 warps of 64x32, 3 stages
 using Cfg7 = GemmCfg<256, 64, 16, 4, 2, 3, 1>;   // 8 warps of 64x32, 1 CTA/SM
 using Cfg8 = GemmCfg<128, 64, 32, 2, 2, 2, 2>;   // 4 warps of 64x32, BK 32
+using Cfg9 = GemmCfg<64, 32, 16, 2, 2, 4, 4>;    // 4 warps of 32x16, 4 stages, 4 CTAs/SM
+using Cfg10 = GemmCfg<64, 64, 32, 2, 2, 3, 2>;   // 4 warps of 32x32, BK 32
+using Cfg11 = GemmCfg<128, 32, 16, 4, 1, 4, 3>;  // 4 warps of 32x32 along M, 4 stages
 // Stream-K partial slots: 2 per CTA, THREADS * ACC doubles each; every config
 // has MINB * THREADS * ACC <= 16384 doubles per SM.
 constexpr int SK_SLOT_DOUBLES_PER_SM = 16384;
@@ -369,6 +372,9 @@ int launch_dgemm(const DGemmParams& p, bool a_col, cudaStream_t st) {
     case 6: return launch_cfg<Cfg6>(p, a_col, vec2, st);
     case 7: return launch_cfg<Cfg7>(p, a_col, vec2, st);
     case 8: return launch_cfg<Cfg8>(p, a_col, vec2, st);
+    case 9: return launch_cfg<Cfg9>(p, a_col, vec2, st);
+    case 10: return launch_cfg<Cfg10>(p, a_col, vec2, st);
+    case 11: return launch_cfg<Cfg11>(p, a_col, vec2, st);
     default:
       // Measured on B200 (tools/tune_gemm.sh): the column-major sketch operand
       // prefers 64x32 warp tiles (31.4 TF/s vs 28.2), the gathered row-major

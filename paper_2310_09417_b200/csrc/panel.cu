@@ -32,14 +32,14 @@
 #include "rskel_internal.h"
 
 // Optional per-phase timestamps (build with -DRS_PANEL_PROBE_ON; read with
-// rs_panel_probe): clock64 of CTA 0 and CTA 1, lane 0, per column.
+// rs_panel_probe): clock64 of thread 0 per phase and column, kept in shared
+// memory during the run and written out by CTAs 0 and 1 at the end (global
+// stores inside the step loop perturb the exchange they are timing).
 #ifdef RS_PANEL_PROBE_ON
-__device__ unsigned long long g_panel_probe[8][64][2];
-#define RS_PANEL_PROBE(k)                                                            \
-  do {                                                                               \
-    if (cta < 2 && (threadIdx.x & 31) == 0 && threadIdx.x < 32) {                    \
-      g_panel_probe[k][j][cta] = clock64();                                          \
-    }                                                                                \
+__device__ unsigned long long g_panel_probe[2][8][64];
+#define RS_PANEL_PROBE(k)                          \
+  do {                                             \
+    if (threadIdx.x == 0) s_probe[k][j] = clock64(); \
   } while (0)
 extern "C" void rs_panel_probe(unsigned long long* out) {
   cudaMemcpyFromSymbol(out, g_panel_probe, sizeof(g_panel_probe));
@@ -70,9 +70,13 @@ struct PanelScratch {
 };
 
 RS_DEV void st_v4(uint4* p, unsigned a, unsigned b, unsigned c, unsigned d) {
+#ifdef RS_PANEL_WEAK_ST
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};\n" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+#else
   // gpu-scope relaxed: .volatile (= relaxed.sys) stores were serialised (~150 ns each)
   asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1,%2,%3,%4};\n" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d)
                : "memory");
+#endif
 }
 RS_DEV uint4 ld_v4(const uint4* p) {
   uint4 v;
@@ -114,6 +118,7 @@ RS_DEV void block_best(double& v, int& p, int& r, double* red_v, int* red_p, int
   __syncthreads();
 }
 
+template <int QMAX>
 __global__ void __launch_bounds__(PTHREADS, 1)
     panel_kernel(double* __restrict__ S, long long lds, int R, int w, int rows_per,
                  int64_t* __restrict__ perm_out, int* __restrict__ ncols_out, PanelScratch* ws,
@@ -132,6 +137,9 @@ __global__ void __launch_bounds__(PTHREADS, 1)
   __shared__ int red_p[PWARPS], red_r[PWARPS];
   __shared__ double s_val;
   __shared__ int s_pos, s_row;
+#ifdef RS_PANEL_PROBE_ON
+  __shared__ unsigned long long s_probe[8][PMAXW];
+#endif
 
   for (int idx = tid; idx < nloc * w; idx += PTHREADS) {
     int i = idx / w, c = idx - i * w;
@@ -157,18 +165,20 @@ __global__ void __launch_bounds__(PTHREADS, 1)
     RS_PANEL_PROBE(0);
     if (warp == 0) {
       const unsigned f = flag_base + (unsigned)j + 1u;
-      // ---- publish this CTA's candidate for column j (no fence needed) ----
-      if (br >= 0) {
-        for (int c = lane; c < w; c += 32) {
-          const unsigned long long x = (unsigned long long)__double_as_longlong(Ss[swz(br, c)]);
-          st_v4(&ws->rowdata[par][cta][c], (unsigned)x, f, (unsigned)(x >> 32), f);
-        }
-      }
+      // ---- publish this CTA's candidate for column j (no fence needed).
+      // The record goes first: it is what every CTA polls; the row values are
+      // read only by the winner's readers, one exchange hop later. ----
       if (lane == 0) {
         const double v = br >= 0 ? bv : -1.0;
         const unsigned long long x = (unsigned long long)__double_as_longlong(v);
         st_v4(&ws->rec[par][cta][0], (unsigned)x, f, (unsigned)(x >> 32), f);
         st_v4(&ws->rec[par][cta][1], (unsigned)bp, f, br >= 0 ? (unsigned)(r0 + br + 1) : 0u, f);
+      }
+      if (br >= 0) {
+        for (int c = lane; c < w; c += 32) {
+          const unsigned long long x = (unsigned long long)__double_as_longlong(Ss[swz(br, c)]);
+          st_v4(&ws->rowdata[par][cta][c], (unsigned)x, f, (unsigned)(x >> 32), f);
+        }
       }
       RS_PANEL_PROBE(1);
       // ---- reduce the G candidates: every CTA polls all records itself
@@ -179,7 +189,6 @@ __global__ void __launch_bounds__(PTHREADS, 1)
       if (cta == 0 || !central) {
         // Poll all of this lane's records in one pass (loads issued back to
         // back, then checked), repeat only for the ones not yet published.
-        constexpr int QMAX = (PMAXG + 31) / 32;
         const int nq = (G - lane + 31) / 32;
         unsigned pending = nq >= 32 ? 0xffffffffu : ((1u << nq) - 1u);
         while (pending) {
@@ -250,13 +259,40 @@ __global__ void __launch_bounds__(PTHREADS, 1)
       RS_PANEL_PROBE(3);
     } else if (late_j >= 0) {
       // ---- late update of the previous step (off the critical path) ----
+      // Rank-1 update of columns jl+2.. of every live row; each lane owns at
+      // most two columns (u0, u1 in registers) and walks 4 rows per trip so
+      // the smem load -> dmul -> dsub -> store chains overlap.
       const int jl = late_j;
-      for (int i = warp - 1; i < nloc; i += PWARPS - 1) {
-        if (pos[i] <= jl || i == late_skip) continue;
-        const double l = Ss[swz(i, jl)];
-        for (int c = jl + 2 + lane; c < w; c += 32) {
-          const int a = swz(i, c);
-          Ss[a] = __dsub_rn(Ss[a], __dmul_rn(l, Urow2[jl & 1][c]));
+      const int c0 = jl + 2 + lane, c1 = c0 + 32;
+      if (c0 < w) {
+        const bool h1 = c1 < w;
+        const double u0 = Urow2[jl & 1][c0], u1 = h1 ? Urow2[jl & 1][c1] : 0.0;
+        constexpr int WS = PWARPS - 1;
+        int i = warp - 1;
+        for (; i + 3 * WS < nloc; i += 4 * WS) {
+          int rr4[4];
+          bool ok[4];
+          double l[4], a[4], b[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            rr4[q] = i + q * WS;
+            ok[q] = pos[rr4[q]] > jl && rr4[q] != late_skip;
+            l[q] = Ss[swz(rr4[q], jl)];
+            a[q] = Ss[swz(rr4[q], c0)];
+            b[q] = h1 ? Ss[swz(rr4[q], c1)] : 0.0;
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (!ok[q]) continue;
+            Ss[swz(rr4[q], c0)] = __dsub_rn(a[q], __dmul_rn(l[q], u0));
+            if (h1) Ss[swz(rr4[q], c1)] = __dsub_rn(b[q], __dmul_rn(l[q], u1));
+          }
+        }
+        for (; i < nloc; i += WS) {
+          if (pos[i] <= jl || i == late_skip) continue;
+          const double l = Ss[swz(i, jl)];
+          Ss[swz(i, c0)] = __dsub_rn(Ss[swz(i, c0)], __dmul_rn(l, u0));
+          if (h1) Ss[swz(i, c1)] = __dsub_rn(Ss[swz(i, c1)], __dmul_rn(l, u1));
         }
       }
     }
@@ -286,6 +322,7 @@ __global__ void __launch_bounds__(PTHREADS, 1)
     }
     RS_PANEL_PROBE(6);
     block_best(bv, bp, br, red_v, red_p, red_r);
+    RS_PANEL_PROBE(4);
     // The new local best row is published next step: bring it fully up to date.
     if (warp == 0 && br >= 0) {
       const double l = Ss[swz(br, j)];
@@ -308,6 +345,10 @@ __global__ void __launch_bounds__(PTHREADS, 1)
   }
   for (int i = tid; i < nloc; i += PTHREADS) perm_out[pos[i]] = r0 + i;
   if (cta == 0 && tid == 0) *ncols_out = ncols;
+#ifdef RS_PANEL_PROBE_ON
+  if (cta < 2)
+    for (int e = tid; e < 8 * PMAXW; e += PTHREADS) g_panel_probe[cta][e / PMAXW][e % PMAXW] = s_probe[e / PMAXW][e % PMAXW];
+#endif
 }
 
 int launch_panel(double* S, long long lds, int R, int w, int64_t* perm_out, int* ncols_dev,
@@ -335,9 +376,14 @@ int launch_panel(double* S, long long lds, int R, int w, int64_t* perm_out, int*
   size_t smem = (size_t)rows_per * PMAXW * sizeof(double) + (size_t)rows_per * sizeof(int);
   smem = (smem + 15) & ~size_t(15);
   if (smem + static_smem > (size_t)max_smem) return RS_ERR_CAPACITY;
-  cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // Polled record slots per lane: G <= 32 * QMAX (a small QMAX keeps the
+  // exchange loop short).
+  const void* kern = G <= 32 ? (const void*)panel_kernel<1>
+                   : G <= 64 ? (const void*)panel_kernel<2>
+                   : G <= 128 ? (const void*)panel_kernel<4> : (const void*)panel_kernel<8>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, panel_kernel, PTHREADS, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, PTHREADS, smem);
   if (occ * nsm < G || G > PMAXG) return RS_ERR_CAPACITY;
   PanelScratch* ws = static_cast<PanelScratch*>(workspace);
   // Flags of launch e are e*128 + j + 1: stale words of earlier launches never match.
@@ -346,7 +392,7 @@ int launch_panel(double* S, long long lds, int R, int w, int64_t* perm_out, int*
   int central = 0;
   if (const char* e = getenv("RSKEL_PANEL_CENTRAL")) central = atoi(e);
   void* args[] = {&S, &lds, &R, &w, &rows_per, &perm_out, &ncols_dev, &ws, &flag_base, &central};
-  cudaError_t e = cudaLaunchCooperativeKernel((void*)panel_kernel, dim3(G), dim3(PTHREADS), args, smem, st);
+  cudaError_t e = cudaLaunchCooperativeKernel(kern, dim3(G), dim3(PTHREADS), args, smem, st);
   count_launch(1);
   return e == cudaSuccess ? RS_OK : RS_ERR_CUDA;
 }

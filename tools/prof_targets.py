@@ -56,7 +56,7 @@ elif what in ("schur", "rank_update", "absorb"):
             _lib.call("rs_absorb_block", n, k, 64, S.data_ptr(), 64, sub.data_ptr(), T.data_ptr(), k,
                       Tn.data_ptr(), perm.data_ptr(), pn.data_ptr(), ws.data_ptr(), st)
 elif what == "panel":
-    Rp = 20000
+    Rp = int(sys.argv[3]) if len(sys.argv) > 3 else 20000
     s0 = torch.randn(Rp, 64, dtype=torch.float64, device="cuda")
     perm = torch.empty(Rp, dtype=torch.int64, device="cuda")
     nc = torch.empty(1, dtype=torch.int32, device="cuda")
