@@ -129,6 +129,20 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def sketch_traffic(m, n_loc, b):
+    """DRAM bytes per sketch launch from the committed ncu --set full capture
+    (profiles/r01_roofline_traffic.json), valid for the cfg2 single-GPU shape
+    it was measured on; None for other shapes."""
+    path = os.path.join(REPO, "profiles", "r01_roofline_traffic.json")
+    if not os.path.exists(path) or (m, n_loc, b) != (20000, 20000, 64):
+        return None
+    with open(path) as f:
+        d = json.load(f)
+    return {"bytes_per_launch": d["dram_bytes_per_launch"],
+            "algorithmic_bytes_per_launch": d["algorithmic_bytes_per_launch"],
+            "ratio": d["dram_bytes_per_launch"] / d["algorithmic_bytes_per_launch"], "source": d["source"]}
+
+
 def cpu_sample(a_host, b, tau, seed, blocks):
     """Reference algorithm (oracle port) on the host cores: first `blocks`
     blocks of the adaptive loop.  Returns (seconds, rank, flops, cores)."""
@@ -265,7 +279,7 @@ def main():
     roofline = {
         "bound": "tensor", "kernel": "dgemm_kernel (sketch Y = A^T Omega_t, DMMA fp64)",
         "achieved": achieved, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-        "frac": achieved / FP64_DMMA_PEAK_TFLOPS, "traffic": None,
+        "frac": achieved / FP64_DMMA_PEAK_TFLOPS, "traffic": sketch_traffic(n, n_loc, b),
         "peak_source": FP64_PEAK_SOURCE,
         "per_launch_flops": 2.0 * n * n_loc * b,
         "launches": blocks,

@@ -22,4 +22,4 @@ echo "full ru rc=$?" >> gpurun_out/ncu_full_ru.log
 for r in prof_bench_sketch prof_bench_ru; do
   ncu -i gpurun_out/$r.ncu-rep --page raw --csv > gpurun_out/${r}_raw.csv 2>/dev/null
 done
-tail -3 gpurun_out/*.log
+tail -n 3 gpurun_out/*.log
