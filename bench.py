@@ -279,7 +279,9 @@ def main():
     roofline = {
         "bound": "tensor", "kernel": "dgemm_kernel (sketch Y = A^T Omega_t, DMMA fp64)",
         "achieved": achieved, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-        "frac": achieved / FP64_DMMA_PEAK_TFLOPS, "traffic": sketch_traffic(n, n_loc, b),
+        "frac": achieved / FP64_DMMA_PEAK_TFLOPS,
+        "traffic": (sketch_traffic(n, n_loc, b) or {}).get("bytes_per_launch"),
+        "traffic_detail": sketch_traffic(n, n_loc, b),
         "peak_source": FP64_PEAK_SOURCE,
         "per_launch_flops": 2.0 * n * n_loc * b,
         "launches": blocks,
