@@ -50,13 +50,26 @@ class TFormState:
         self._T = [torch.empty(cap, dtype=torch.float64, device=dev) for _ in range(2)]
         self._perm = [torch.empty(max(m, 1), dtype=torch.int64, device=dev) for _ in range(2)]
         self._cur = 0
-        self.S = torch.empty(max(m * bmax, 1), dtype=torch.float64, device=dev)
+        # Schur block S (factored in place by the panel).  absorb_schur writes
+        # the next block's S into the other buffer, so a rollback can still
+        # re-absorb the previous block from its own factored S.
+        self._S = [torch.empty(max(m * bmax, 1), dtype=torch.float64, device=dev)]
+        self._scur = 0
         self.sub = torch.empty(max(m, 1), dtype=torch.int64, device=dev)
         self.ws = _device.workspace()
         self.stream = _device.stream_handle()
         _lib.call("rs_iota", self.perm.data_ptr(), m, self.stream)
 
     # -- views ---------------------------------------------------------------
+    @property
+    def S(self):
+        return self._S[self._scur]
+
+    def _s_next(self):
+        if len(self._S) == 1:
+            self._S.append(torch.empty_like(self._S[0]))
+        return self._S[1 - self._scur]
+
     @property
     def perm(self):
         return self._perm[self._cur]
@@ -95,7 +108,7 @@ class TFormState:
             self.T.data_ptr(), max(self.k, 1), self._T[nxt].data_ptr(), self.perm.data_ptr(),
             self._perm[nxt].data_ptr(), self.ws.data_ptr(), self.stream,
         )
-        self._prev = (self._cur, self.k)
+        self._prev = (self._cur, self.k, self._scur)
         self._cur = nxt
         self.k += nc
 
@@ -103,20 +116,22 @@ class TFormState:
         """absorb(w, nc) fused with the Schur block of the next sketch block
         (m x 64 at y_next_ptr) into S, e2_out = ||S||^2 (rs_absorb_schur)."""
         nxt = 1 - self._cur
+        s_next = self._s_next()
         _lib.call(
             "rs_absorb_schur", self.m, self.k, nc, self.S.data_ptr(), w, self.sub.data_ptr(),
             self.T.data_ptr(), max(self.k, 1), self._T[nxt].data_ptr(), self.perm.data_ptr(),
-            self._perm[nxt].data_ptr(), y_next_ptr, 64, self.S.data_ptr(),
+            self._perm[nxt].data_ptr(), y_next_ptr, 64, s_next.data_ptr(),
             e2_out.data_ptr() if e2_out is not None else None, self.ws.data_ptr(), self.stream,
         )
-        self._prev = (self._cur, self.k)
+        self._prev = (self._cur, self.k, self._scur)
         self._cur = nxt
+        self._scur = 1 - self._scur
         self.k += nc
 
     def rollback(self):
         """Undo the last absorb (its inputs are intact in the other buffers):
         used when a speculative absorb assumed a full-width elimination."""
-        self._cur, self.k = self._prev
+        self._cur, self.k, self._scur = self._prev
 
     def interpolation(self, out=None):
         """Dense W (m x k) with W[perm[:k]] = I, W[perm[k:]] = T."""

@@ -17,7 +17,7 @@ namespace {
 constexpr int kMaxB = 64;
 
 struct WorkspaceLayout {
-  size_t panel_off, sumsq_off, linv_off, gemm_off, fused_off, total;
+  size_t panel_off, sumsq_off, linv_off, gemm_off, fused_off, zp_off, total;
 };
 
 WorkspaceLayout layout() {
@@ -34,7 +34,8 @@ WorkspaceLayout layout() {
   L.linv_off = L.sumsq_off + up(rs::sumsq_workspace_bytes());
   L.gemm_off = L.linv_off + up(sizeof(double) * kMaxB * kMaxB);
   L.fused_off = L.gemm_off + up(rs::gemm_partials_bytes(nsm));
-  L.total = L.fused_off + up(rs::fused_partials_bytes(nsm));
+  L.zp_off = L.fused_off + up(rs::absorb_schur_slots_bytes(nsm));
+  L.total = L.zp_off + up(sizeof(double) * kMaxB * kMaxB);
   return L;
 }
 
@@ -146,15 +147,16 @@ int rs_absorb_schur(int m, int k, int nc, const double* S_, long long lds, const
   const int R = m - k, Rn = R - nc;
   const long long ldn = k + nc;
   auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
-  // The fused kernel is correct but not yet faster than the two tuned kernels
-  // on B200 (DMMA 41% busy: too few independent accumulators per warp); it is
-  // opt-in (RSKEL_FUSED=1) until that is fixed.
+  // One pass over T (absorb_schur.cu) with RSKEL_FUSED=1: correct, but on
+  // B200 it is not yet faster than the two tuned kernels (rank update at 64%
+  // and Schur GEMM at 70% DMMA vs 68% for the fused pass), so the default is
+  // the two-pass path.
   static const bool fused_enabled = [] {
     const char* e = getenv("RSKEL_FUSED");
     return e != nullptr && e[0] == '1';
   }();
-  const bool fused = fused_enabled && nc == kMaxB && k % 32 == 0 && ldy == 64 && (k == 0 || ldt == k) &&
-                     al16(T) && al16(T_new) && al16(Y_next) && al16(S_next);
+  const bool fused = fused_enabled && nc >= 1 && k >= 1 && k % 2 == 0 && nc % 2 == 0 && ldy == 64 &&
+                     ldt == k && al16(T) && al16(T_new) && al16(Y_next) && al16(S_next) && S_next != S_;
   if (!fused) {
     int rc = rs_absorb_block(m, k, nc, S_, lds, sub_perm, T, ldt, T_new, perm, perm_new, workspace, stream);
     if (rc != RS_OK) return rc;
@@ -162,6 +164,8 @@ int rs_absorb_schur(int m, int k, int nc, const double* S_, long long lds, const
                           nc > 0 ? ldy : 1, e2_dev, workspace, stream);
   }
   double* linv = reinterpret_cast<double*>(W(workspace, layout().linv_off));
+  double* zp = reinterpret_cast<double*>(W(workspace, layout().zp_off));
+  // L_1^{-1}, W_hat = L_r L_1^{-1} -> T_new[:, k:k+nc], perm' (as rs_absorb_block)
   int rc = rs::launch_trinv(S_, lds, 1, sub_perm, nc, 1, 1, linv, kMaxB, S(stream));
   if (rc != RS_OK) return rc;
   rs::DGemmParams pw{Rn, nc, nc, S_, lds, sub_perm + nc, linv, kMaxB, nullptr, nullptr, 0,
@@ -170,11 +174,15 @@ int rs_absorb_schur(int m, int k, int nc, const double* S_, long long lds, const
   if (rc != RS_OK) return rc;
   rc = rs::launch_perm_update(perm, perm_new, m, k, sub_perm, S(stream));
   if (rc != RS_OK) return rc;
-  rc = rs::launch_fused_absorb_schur(Rn, k, nc, T, sub_perm, T_new, Y_next, perm_new, S_next,
-                                     reinterpret_cast<double*>(W(workspace, layout().fused_off)),
-                                     S(stream));
+  // Z[P] = Y[perm'[k:k+nc]] - T[P] Y[perm'[:k]]
+  rs::DGemmParams pz{nc, (int)ldy, k, T, ldt, sub_perm, Y_next, ldy, perm_new, Y_next, ldy,
+                     perm_new + k, zp, ldy, -1.0, 1.0, gemm_ws(workspace)};
+  rc = rs::launch_dgemm(pz, false, S(stream));
   if (rc != RS_OK) return rc;
-  if (e2_dev) rc = rs_sumsq(S_next, 64, Rn, 64, e2_dev, workspace, stream);
+  rc = rs::launch_absorb_schur(Rn, k, nc, T, sub_perm, T_new, Y_next, ldy, perm_new, zp, S_next, S_next,
+                               reinterpret_cast<double*>(W(workspace, layout().fused_off)), S(stream));
+  if (rc != RS_OK) return rc;
+  if (e2_dev) rc = rs_sumsq(S_next, ldy, Rn, (int)ldy, e2_dev, workspace, stream);
   return rc;
 }
 

@@ -20,6 +20,7 @@
 // units.  Tiles split between CTAs write fragment-ordered partials; a fixup
 // kernel adds them in k order (CTA order) and applies the epilogue.  The
 // split depends only on (M, N, K, G), so results are bitwise reproducible.
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -307,6 +308,39 @@ __global__ void __launch_bounds__(C::THREADS) dgemm_fixup_kernel(DGemmParams p, 
   epilogue_store<C>(p, m0, n0, wm, wn, g, t, acc);
 }
 
+// Fixup for skinny splits (many CTAs per tile): CTA (tile, e) sums element e
+// of every thread's partial over the contributors (in CTA order) and stores it.
+template <class C>
+__global__ void __launch_bounds__(C::THREADS) dgemm_fixup_elem_kernel(DGemmParams p, SkPlan sk) {
+  const int tile = blockIdx.x, e = blockIdx.y;
+  const long long ub = (long long)tile * sk.KT, ue = ub + sk.KT;
+  auto owner = [&](long long u) {
+    int c = (int)((u * sk.G) / sk.U);
+    while (c + 1 < sk.G && sk_u0(sk, c + 1) <= u) ++c;
+    while (c > 0 && sk_u0(sk, c) > u) --c;
+    return c;
+  };
+  const int clo = owner(ub), chi = owner(ue - 1);
+  if (clo == chi) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp % C::WARPS_M) * C::WTM, wn = (warp / C::WARPS_M) * C::WTN;
+  double acc = p.partials[(size_t)(2 * clo + 1) * C::THREADS * C::ACC + (size_t)e * C::THREADS + tid];
+  for (int c = clo + 1; c <= chi; ++c)
+    acc += p.partials[(size_t)(2 * c) * C::THREADS * C::ACC + (size_t)e * C::THREADS + tid];
+  // e = ((i * NT + j) * 4 + 2h + ee): fragment row/column of this element
+  const int ee = e & 1, h = (e >> 1) & 1, ij = e >> 2, i = ij / C::NT, j = ij % C::NT;
+  const int m0 = (tile / sk.tiles_n) * C::BM, n0 = (tile % sk.tiles_n) * C::BN;
+  const int row = m0 + wm + 16 * i + g + 8 * h, col = n0 + wn + 8 * j + 2 * t + ee;
+  if (row >= p.M || col >= p.N) return;
+  double v = p.alpha * acc;
+  if (p.beta != 0.0) {
+    const long long r = p.cidx ? p.cidx[row] : row;
+    v = fma(p.alpha, acc, p.beta * p.Cin[r * p.ldcin + col]);
+  }
+  p.C[(long long)row * p.ldc + col] = v;
+}
+
 template <class C, bool A_COL, bool VEC2>
 static int launch_dgemm_t(const DGemmParams& p, cudaStream_t st) {
   static_assert(C::MINB * C::THREADS * C::ACC <= SK_SLOT_DOUBLES_PER_SM, "partials workspace");
@@ -329,10 +363,20 @@ static int launch_dgemm_t(const DGemmParams& p, cudaStream_t st) {
   const int slots = nsm * C::MINB;
   // Stream-K when a plain grid would run fewer than ~4 waves and each CTA
   // still gets a few k-tiles of work.
-  if (p.partials != nullptr && sk.tiles < 4 * slots && sk.U >= 4LL * slots && sk.KT >= 8) {
-    sk.G = slots;
+  // Skinny products (fewer tiles than CTA slots, long K) split K over up to
+  // `slots` CTAs with at least 4 k-tiles each.
+  int G = 0;
+  if (p.partials != nullptr && sk.tiles < 4 * slots && sk.KT >= 8) {
+    if (sk.U >= 4LL * slots) G = slots;
+    else if (sk.tiles < slots && sk.KT >= 64) G = (int)std::max<long long>(sk.tiles, std::min<long long>(slots, sk.U / 4));
+  }
+  if (G > 0) {
+    sk.G = G;
     dgemm_kernel<C, A_COL, VEC2><<<sk.G, C::THREADS, smem, st>>>(p, sk);
-    dgemm_fixup_kernel<C><<<sk.tiles, C::THREADS, 0, st>>>(p, sk);
+    if (sk.G > 8 * sk.tiles)  // many contributors per tile: element-parallel sum
+      dgemm_fixup_elem_kernel<C><<<dim3(sk.tiles, C::ACC), C::THREADS, 0, st>>>(p, sk);
+    else
+      dgemm_fixup_kernel<C><<<sk.tiles, C::THREADS, 0, st>>>(p, sk);
     count_launch(2);
   } else {
     dim3 grid(sk.tiles_n, tiles_m);

@@ -32,11 +32,11 @@ int launch_rank_update(int M, int N, int K, const double* A, long long lda, cons
                        long long ldb, const int64_t* bidx, const double* Cin, long long ldcin,
                        const int64_t* cidx, double* C, long long ldc, cudaStream_t st);
 size_t gemm_partials_bytes(int nsm);
-// Fused absorb(t) + Schur(t+1) pass over T (fused_update.cu); nc must be 64, k % 32 == 0.
-size_t fused_partials_bytes(int nsm);
-int launch_fused_absorb_schur(int Rn, int k, int nc, const double* T, const int64_t* sub, double* Tn,
-                              const double* Y, const int64_t* perm, double* S, double* partials,
-                              cudaStream_t st);
+// Absorb(t) + Schur(t+1) with one read of T (absorb_schur.cu).
+size_t absorb_schur_slots_bytes(int nsm);
+int launch_absorb_schur(int Rn, int k, int nc, const double* T, const int64_t* sub, double* Tn,
+                        const double* Y, long long ldy, const int64_t* perm_new, const double* ZP, double* X,
+                        double* S, double* slots, cudaStream_t st);
 
 // Panel LUPP (cooperative grid).  Factors the R x w row-major block S in
 // place with partial pivoting (first maximum in the current position wins,

@@ -7,6 +7,8 @@ differs from OpenBLAS/LAPACK, indices may not).
 """
 
 import ctypes
+import os
+import sys
 
 import numpy as np
 import pytest
@@ -295,3 +297,44 @@ def test_adaptive_nonfinite_rejected(rs):
     a[3, 4] = np.nan
     with pytest.raises(ValueError):
         rs.rand_lupp_adaptive(a, 8, 1e-3, spec(rs, 30), rs.RngStream(0))
+
+
+@pytest.mark.parametrize("b", [64, 32])
+def test_adaptive_rank_exhausted_full_width_block(b):
+    """Zero pivot in the middle of a b-wide block on the speculative
+    (absorb-ahead) path: the block is re-absorbed truncated from its own
+    factored Schur block (`skeleton.py:439-454`, `dense.py:195-198`)."""
+    import paper_2310_09417_b200 as rs
+
+    g = np.random.default_rng(41)
+    a = np.zeros((500, 400))
+    rows = np.sort(g.choice(500, 100, replace=False))
+    a[rows] = g.standard_normal((100, 400))
+    spec = rs.SketchSpec("gaussian", 400, b)
+    res = rs.rand_lupp_adaptive(a, b, 1e-30, spec, rs.RngStream(3))
+    ref = orc.rand_lupp_adaptive(a, b, 1e-30, 3)
+    assert res.status == ref["status"] == "rank_exhausted"
+    assert res.rank == ref["rank"] == 100
+    assert np.array_equal(np.sort(res.row_idx), rows)
+    assert np.array_equal(res.row_idx, ref["row_idx"])
+    err = np.linalg.norm(a - res.w @ a[res.row_idx]) / np.linalg.norm(a)
+    assert err <= 1e-12
+
+
+def test_absorb_schur_one_pass_matches_two_pass():
+    """RSKEL_FUSED=1 (one pass over T: Schur of the next block against the
+    old factorisation + rank-nc correction) agrees with the two-pass kernels:
+    T' bitwise, S' and e2 to rounding (tools/check_absorb_schur.py)."""
+    import subprocess
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, RSKEL_FUSED="1", PYTHONPATH=repo)
+    out = subprocess.run([sys.executable, os.path.join(repo, "tools", "check_absorb_schur.py")], env=env,
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("n=")]
+    assert len(lines) == 3
+    for ln in lines:
+        assert "perm equal True" in ln and "T' max diff 0.000e+00" in ln, ln
+        rel = float(ln.split("S' max rel diff ")[1].split(",")[0])
+        assert rel < 1e-13, ln

@@ -97,6 +97,14 @@ def bench_gemm():
         print(f"  rank_update only: {ms:.3f} ms {fl / ms / 1e9:.1f} TF/s {by / ms / 1e6:.0f} GB/s")
         Tref = T[sub[64:]] - What @ T[sub[:64]]
         print("  rank_update max err:", float((Tn[: (R - 64) * k].view(R - 64, k) - Tref).abs().max()))
+        # absorb(t) + Schur(t+1): one call (rs_absorb_schur; RSKEL_FUSED=0 -> two passes)
+        Sn = torch.empty(R, 64, dtype=torch.float64, device="cuda")
+        y2 = torch.randn(n, 64, dtype=torch.float64, device="cuda")
+        ms = timeit(lambda: _lib.call("rs_absorb_schur", n, k, 64, Sx.data_ptr(), 64, sub.data_ptr(),
+                                      T.data_ptr(), k, Tn.data_ptr(), perm.data_ptr(), pn.data_ptr(),
+                                      y2.data_ptr(), 64, Sn.data_ptr(), e2.data_ptr(), ws.data_ptr(), st),
+                    reps=10)
+        print(f"  absorb+schur k={k:5d}: {ms:.3f} ms {2 * fl / ms / 1e9:.1f} TF/s")
         linv = torch.empty(64, 64, dtype=torch.float64, device="cuda")
         ms = timeit(lambda: _lib.call("rs_trinv", Sx.data_ptr(), 64, 1, sub.data_ptr(), 64, 1, 1,
                                       linv.data_ptr(), 64, st), reps=10)

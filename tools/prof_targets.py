@@ -31,9 +31,10 @@ elif what == "fused":
     Tn = torch.empty((R - 64) * (k + 64), dtype=torch.float64, device="cuda")
     pn = torch.empty(n, dtype=torch.int64, device="cuda")
     e2 = torch.empty(1, dtype=torch.float64, device="cuda")
+    Sn = torch.empty(R, 64, dtype=torch.float64, device="cuda")
     for _ in range(reps):
         _lib.call("rs_absorb_schur", n, k, 64, S.data_ptr(), 64, sub.data_ptr(), T.data_ptr(), k,
-                  Tn.data_ptr(), perm.data_ptr(), pn.data_ptr(), y.data_ptr(), 64, S.data_ptr(),
+                  Tn.data_ptr(), perm.data_ptr(), pn.data_ptr(), y.data_ptr(), 64, Sn.data_ptr(),
                   e2.data_ptr(), ws.data_ptr(), st)
 elif what in ("schur", "rank_update", "absorb"):
     y = torch.randn(n, 64, dtype=torch.float64, device="cuda")
