@@ -154,6 +154,18 @@ int rs_pinv_scale(const double* Xt, long long ldx, int p, double* Vt, long long 
 /* *out = max_j sum_i |A[i,j]| (matrix 1-norm, for the cond_1 flag, skeleton.py:592-603). */
 int rs_norm1(const double* A, long long lda, int rows, int cols, double* out, void* stream);
 
+/* All nrounds rounds of a Jacobi sweep (sched: nrounds x npairs pairs) in one
+ * cooperative launch of npairs CTAs with a grid barrier between rounds;
+ * barrier: one caller-owned device unsigned (reset by the call). */
+int rs_jacobi_sweep(double* Xt, long long ldx, int p, double* Vt, long long ldv, int q, const int* sched,
+                    int nrounds, int npairs, double tol, unsigned long long* max_off, unsigned* barrier,
+                    void* stream);
+
+/* Cholesky G = R^T R of a small SPD matrix (n <= 1024) in place (upper R,
+ * strict lower part zeroed); *status_dev = 0 or j + 1 for a non-positive
+ * pivot j.  The Gram step of pinv_apply (dense.py:166-182). */
+int rs_cholesky(double* G, long long ldg, int n, int* status_dev, void* stream);
+
 /* dst[i, j] = src[r(i)*rs + c(j)*cs], r/c via optional index vectors: the
  * skeleton gathers a[I], a[:, J], a[ix_(I, J)] (skeleton.py:619,639-645). */
 int rs_gather2d(const double* src, long long rs, long long cs, const int64_t* ridx, int nr,

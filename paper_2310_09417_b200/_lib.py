@@ -45,6 +45,8 @@ SIGNATURES = {
     "rs_jacobi_round": (_c_int, [_p, _c_ll, _c_int, _p, _c_ll, _c_int, _p, _c_int, _c_double, _p, _p]),
     "rs_pinv_scale": (_c_int, [_p, _c_ll, _c_int, _p, _c_ll, _c_int, _c_double, _p, _p]),
     "rs_norm1": (_c_int, [_p, _c_ll, _c_int, _c_int, _p, _p]),
+    "rs_cholesky": (_c_int, [_p, _c_ll, _c_int, _p, _p]),
+    "rs_jacobi_sweep": (_c_int, [_p, _c_ll, _c_int, _p, _c_ll, _c_int, _p, _c_int, _c_int, _c_double, _p, _p, _p]),
     "rs_gather2d": (_c_int, [_p, _c_ll, _c_ll, _p, _c_int, _p, _c_int, _p, _c_ll, _p]),
     "rs_gaussian_workspace_bytes": (ctypes.c_size_t, [_c_ll]),
     "rs_gaussian": (_c_int, [ctypes.c_ulonglong, ctypes.c_ulonglong, _c_ll, _c_double, _p, _p,

@@ -228,6 +228,16 @@ int rs_pinv_scale(const double* Xt, long long ldx, int p, double* Vt, long long 
   return rs::launch_pinv_scale(Xt, ldx, p, Vt, ldv, q, rcond, sigma, S(stream));
 }
 
+int rs_jacobi_sweep(double* Xt, long long ldx, int p, double* Vt, long long ldv, int q, const int* sched,
+                    int nrounds, int npairs, double tol, unsigned long long* max_off, unsigned* barrier,
+                    void* stream) {
+  return rs::launch_jacobi_sweep(Xt, ldx, p, Vt, ldv, q, sched, nrounds, npairs, tol, max_off, barrier, S(stream));
+}
+
+int rs_cholesky(double* G, long long ldg, int n, int* status_dev, void* stream) {
+  return rs::launch_cholesky(G, ldg, n, status_dev, S(stream));
+}
+
 int rs_norm1(const double* A, long long lda, int rows, int cols, double* out, void* stream) {
   return rs::launch_norm1(A, lda, rows, cols, out, S(stream));
 }

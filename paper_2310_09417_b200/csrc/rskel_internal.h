@@ -72,6 +72,10 @@ int launch_jacobi_round(double* Xt, long long ldx, int p, double* Vt, long long 
                         int npairs, double tol, unsigned long long* max_off, cudaStream_t st);
 int launch_pinv_scale(const double* Xt, long long ldx, int p, double* Vt, long long ldv, int q, double rcond,
                       double* sigma, cudaStream_t st);
+int launch_jacobi_sweep(double* Xt, long long ldx, int p, double* Vt, long long ldv, int q, const int* sched,
+                        int nrounds, int npairs, double tol, unsigned long long* max_off, unsigned* bar,
+                        cudaStream_t st);
+int launch_cholesky(double* G, long long ldg, int n, int* status, cudaStream_t st);
 int launch_norm1(const double* A, long long lda, int rows, int cols, double* out, cudaStream_t st);
 int launch_gather2d(const double* src, long long rs_, long long cs_, const int64_t* ridx, int nr,
                     const int64_t* cidx, int nc, double* dst, long long ldd, cudaStream_t st);

@@ -83,6 +83,74 @@ int launch_jacobi_round(double* Xt, long long ldx, int p, double* Vt, long long 
   return cudaGetLastError() == cudaSuccess ? RS_OK : RS_ERR_CUDA;
 }
 
+// A whole sweep in one cooperative launch: CTA c rotates pair c of every
+// round, a grid barrier between rounds (the per-round launches of a small
+// q x q problem were host-launch bound).  Same arithmetic as the round kernel.
+__global__ void __launch_bounds__(JT) jacobi_sweep_kernel(double* __restrict__ Xt, long long ldx, int p,
+                                                          double* __restrict__ Vt, long long ldv, int q,
+                                                          const int* __restrict__ sched, int nrounds, double tol,
+                                                          unsigned long long* __restrict__ max_off,
+                                                          unsigned* __restrict__ bar) {
+  __shared__ double red[JT / 32 + 1];
+  const int G = gridDim.x;
+  for (int rd = 0; rd < nrounds; ++rd) {
+    const int* pairs = sched + (size_t)rd * 2 * G;
+    const int i = pairs[2 * blockIdx.x], j = pairs[2 * blockIdx.x + 1];
+    if (i >= 0 && j >= 0) {
+      double* xi = Xt + (long long)i * ldx;
+      double* xj = Xt + (long long)j * ldx;
+      double a = 0.0, b = 0.0, g = 0.0;
+      for (int r = threadIdx.x; r < p; r += JT) {
+        const double u = xi[r], w = xj[r];
+        a = fma(u, u, a);
+        b = fma(w, w, b);
+        g = fma(u, w, g);
+      }
+      a = block_sum(a, red);
+      b = block_sum(b, red);
+      g = block_sum(g, red);
+      const double scale = sqrt(a) * sqrt(b);
+      const double off = scale > 0.0 ? fabs(g) / scale : 0.0;
+      if (threadIdx.x == 0 && scale > 0.0) atomicMax(max_off, (unsigned long long)__double_as_longlong(off));
+      if (scale > 0.0 && off > tol) {
+        const double zeta = (b - a) / (2.0 * g);
+        const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / sqrt(1.0 + tt * tt), s = c * tt;
+        for (int r = threadIdx.x; r < p; r += JT) {
+          const double u = xi[r], w = xj[r];
+          xi[r] = c * u - s * w;
+          xj[r] = s * u + c * w;
+        }
+        double* vi = Vt + (long long)i * ldv;
+        double* vj = Vt + (long long)j * ldv;
+        for (int r = threadIdx.x; r < q; r += JT) {
+          const double u = vi[r], w = vj[r];
+          vi[r] = c * u - s * w;
+          vj[r] = s * u + c * w;
+        }
+      }
+    }
+    __threadfence();
+    grid_barrier(bar, (unsigned)((rd + 1) * G));
+  }
+}
+
+int launch_jacobi_sweep(double* Xt, long long ldx, int p, double* Vt, long long ldv, int q, const int* sched,
+                        int nrounds, int npairs, double tol, unsigned long long* max_off, unsigned* bar,
+                        cudaStream_t st) {
+  if (npairs <= 0 || nrounds <= 0) return RS_OK;
+  int dev = 0, nsm = 148, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, jacobi_sweep_kernel, JT, 0);
+  if (npairs > occ * nsm) return RS_ERR_CAPACITY;
+  if (cudaMemsetAsync(bar, 0, sizeof(unsigned), st) != cudaSuccess) return RS_ERR_CUDA;
+  void* args[] = {&Xt, &ldx, &p, &Vt, &ldv, &q, &sched, &nrounds, &tol, &max_off, &bar};
+  cudaError_t e = cudaLaunchCooperativeKernel((void*)jacobi_sweep_kernel, dim3(npairs), dim3(JT), args, 0, st);
+  count_launch(1);
+  return e == cudaSuccess ? RS_OK : RS_ERR_CUDA;
+}
+
 // sigma_i = |Xt[i, :]|, d_i = 1 / sigma_i^2 if sigma_i > rcond * max sigma else 0;
 // scales column i of V (row i of Vt) by d_i.  One CTA.
 __global__ void __launch_bounds__(JT) pinv_scale_kernel(const double* __restrict__ Xt, long long ldx, int p,
@@ -145,6 +213,53 @@ __global__ void __launch_bounds__(JT) norm1_kernel(const double* __restrict__ A,
 int launch_norm1(const double* A, long long lda, int rows, int cols, double* out, cudaStream_t st) {
   if (rows < 0 || cols < 0) return RS_ERR_ARG;
   norm1_kernel<<<1, JT, 0, st>>>(A, lda, rows, cols, out);
+  count_launch(1);
+  return cudaGetLastError() == cudaSuccess ? RS_OK : RS_ERR_CUDA;
+}
+
+// Cholesky G = R^T R of a small SPD matrix (n <= 1024), in place: the upper
+// triangle of G becomes R, the strict lower triangle is zeroed.  One CTA,
+// right-looking by columns (the Gram matrix of a well-conditioned
+// interpolation matrix in the pinv path, cur.py).  *status = 0, or j + 1 if
+// pivot j is not positive.
+__global__ void __launch_bounds__(1024) cholesky_kernel(double* __restrict__ G, long long ldg, int n,
+                                                        int* __restrict__ status) {
+  __shared__ double s_d;
+  __shared__ int s_bad;
+  if (threadIdx.x == 0) s_bad = 0;
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    if (threadIdx.x == 0) {
+      const double d = G[(long long)j * ldg + j];
+      if (!(d > 0.0)) s_bad = j + 1;
+      s_d = d > 0.0 ? sqrt(d) : 1.0;
+    }
+    __syncthreads();
+    if (s_bad) break;
+    const double d = s_d;
+    for (int c = j + threadIdx.x; c < n; c += blockDim.x)
+      G[(long long)j * ldg + c] = c == j ? d : G[(long long)j * ldg + c] / d;
+    __syncthreads();
+    // trailing update of the upper triangle: G[r][c] -= R[j][r] R[j][c], j < r <= c
+    const int m = n - j - 1;
+    for (long long e = threadIdx.x; e < (long long)m * m; e += blockDim.x) {
+      const int r = j + 1 + (int)(e / m), c = j + 1 + (int)(e % m);
+      if (c < r) continue;
+      G[(long long)r * ldg + c] -= G[(long long)j * ldg + r] * G[(long long)j * ldg + c];
+    }
+    __syncthreads();
+  }
+  for (long long e = threadIdx.x; e < (long long)n * n; e += blockDim.x) {
+    const int r = (int)(e / n), c = (int)(e % n);
+    if (c < r) G[(long long)r * ldg + c] = 0.0;
+  }
+  if (threadIdx.x == 0) *status = s_bad;
+}
+
+int launch_cholesky(double* G, long long ldg, int n, int* status, cudaStream_t st) {
+  if (n < 0 || n > 1024 || ldg < n) return RS_ERR_ARG;
+  if (n == 0) return cudaMemsetAsync(status, 0, sizeof(int), st) == cudaSuccess ? RS_OK : RS_ERR_CUDA;
+  cholesky_kernel<<<1, 1024, 0, st>>>(G, ldg, n, status);
   count_launch(1);
   return cudaGetLastError() == cudaSuccess ? RS_OK : RS_ERR_CUDA;
 }

@@ -72,12 +72,18 @@ def _jacobi_svd_t(Xt):
         return Vt
     sched = torch.as_tensor(_round_robin(q)).to(dev)
     maxoff = torch.zeros(1, dtype=torch.int64, device=dev)
-    npairs = sched.shape[1]
+    bar = torch.zeros(1, dtype=torch.int32, device=dev)
+    nrounds, npairs = sched.shape[0], sched.shape[1]
     for _ in range(JACOBI_SWEEPS):
         maxoff.zero_()
-        for r in range(sched.shape[0]):
-            _lib.call("rs_jacobi_round", Xt.data_ptr(), p, p, Vt.data_ptr(), q, q,
-                      sched[r].data_ptr(), npairs, JACOBI_TOL, maxoff.data_ptr(), _st())
+        # one cooperative launch per sweep; per-round launches if the pairs
+        # do not fit co-resident (RS_ERR_CAPACITY)
+        rc = _lib.load().rs_jacobi_sweep(Xt.data_ptr(), p, p, Vt.data_ptr(), q, q, sched.data_ptr(), nrounds,
+                                         npairs, JACOBI_TOL, maxoff.data_ptr(), bar.data_ptr(), _st())
+        if rc != 0:
+            for r in range(nrounds):
+                _lib.call("rs_jacobi_round", Xt.data_ptr(), p, p, Vt.data_ptr(), q, q,
+                          sched[r].data_ptr(), npairs, JACOBI_TOL, maxoff.data_ptr(), _st())
         off = float(maxoff.view(torch.float64).item())
         if off <= JACOBI_TOL:
             break
@@ -87,7 +93,55 @@ def _jacobi_svd_t(Xt):
 def _pinv_apply_dev(A, B):
     """x = A^+ B (A: Matrix p x q, B: Matrix p x r, any layouts) -> row-major tensor q x r.
 
-    One-sided Jacobi on the columns of A gives A V = U Sigma; then
+    Tall A (p > 2q, q <= 1024) is first compressed to q x q: LUPP of A gives the
+    interpolative form A = W A[I] (W = P [I; T], so sigma_min(W) >= 1 and W is
+    well conditioned), CholeskyQR of W gives W = Q_W R_W, hence
+    A = Q_W M with M = R_W A[I] (q x q) and A^+ B = M^+ (R_W^-T W^T B): the
+    same singular values, so the rcond truncation is unchanged, and the
+    Jacobi sweeps run on q x q instead of p x q.  Exactly rank-deficient or
+    badly conditioned W falls back to Jacobi on A itself."""
+    p, q = A.shape
+    if p > 2 * q and 2 <= q <= 1024:
+        x = _pinv_apply_compressed(A, B)
+        if x is not None:
+            return x
+    return _pinv_apply_jacobi(A, B)
+
+
+def _pinv_apply_compressed(A, B):
+    p, q = A.shape
+    r = B.cols
+    dev = _device.device()
+    Ar = A.row_major()
+    st, W, fail = _engine.factor_sample(Ar, want_w=True)
+    if fail is not None:
+        return None
+    Wm = dense._mat(W)                                   # p x q row-major
+    A_I = _rows(Ar, st.perm[:q].clone())                 # q x q
+    G = torch.empty((q, q), dtype=torch.float64, device=dev)
+    dense._gemm(dense._mat(G), Wm.T, Wm)                 # W^T W = I + T^T T
+    status = torch.empty(1, dtype=torch.int32, device=dev)
+    _lib.call("rs_cholesky", G.data_ptr(), q, q, status.data_ptr(), _st())
+    if int(status.item()) != 0:
+        return None
+    Rw = dense._mat(G)                                   # upper R_W, W = Q_W R_W
+    M = torch.empty((q, q), dtype=torch.float64, device=dev)
+    dense._gemm(dense._mat(M), Rw, A_I)                  # M = R_W A[I]
+    # H = W^T B (q x r) without transposing a large column-major B
+    if B.colmajor:
+        Ht = torch.empty((r, q), dtype=torch.float64, device=dev)
+        dense._gemm(dense._mat(Ht), B.T, Wm)             # H^T = B^T W
+        H = dense._mat(Ht).T.row_major()
+    else:
+        Hr = torch.empty((q, r), dtype=torch.float64, device=dev)
+        dense._gemm(dense._mat(Hr), Wm.T, B)
+        H = dense._mat(Hr)
+    H2 = dense._trsm_left(Rw.T, H, lower=True, unit=False)   # Q_W^T B = R_W^-T W^T B
+    return _pinv_apply_jacobi(dense._mat(M), H2)
+
+
+def _pinv_apply_jacobi(A, B):
+    """x = A^+ B by one-sided Jacobi on the columns of A: A V = U Sigma, then
     x = V diag(1/sigma^2) (A V)^T B with sigma <= rcond * sigma_max dropped."""
     p, q = A.shape
     r = B.cols
