@@ -72,6 +72,14 @@ constexpr double ZIG_INV_R = 0.27366123732975828;
 // Pass A: one attempt starting at every position.
 __global__ void rng_attempt_kernel(uint64_t k0, uint64_t k1, long long P, uint8_t* __restrict__ next,
                                    uint8_t* __restrict__ ends, double* __restrict__ val) {
+  // ki / wi looked up per word with 32 different indices per warp: from
+  // shared memory (constant memory serialises divergent indices)
+  __shared__ uint64_t s_ki[256], s_wi[256];
+  for (int e = threadIdx.x; e < 256; e += blockDim.x) {
+    s_ki[e] = zig_ki[e];
+    s_wi[e] = zig_wi_bits[e];
+  }
+  __syncthreads();
   const long long base = 4LL * (blockIdx.x * (long long)blockDim.x + threadIdx.x);
   if (base >= P) return;
   uint64_t w[4];
@@ -85,10 +93,10 @@ __global__ void rng_attempt_kernel(uint64_t k0, uint64_t k1, long long P, uint8_
     r >>= 8;
     const bool neg = r & 1;
     const uint64_t rabs = (r >> 1) & 0x000fffffffffffffull;
-    double x = (double)rabs * __longlong_as_double((long long)zig_wi_bits[idx]);
+    double x = (double)rabs * __longlong_as_double((long long)s_wi[idx]);
     if (neg) x = -x;
     uint8_t nx = 1, en = 1;
-    if (rabs >= zig_ki[idx]) {
+    if (rabs >= s_ki[idx]) {
       if (idx == 0) {  // tail: pairs of doubles until accepted
         long long s = p + 1;
         double xx, yy;
