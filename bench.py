@@ -32,7 +32,7 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 FP64_DMMA_PEAK_TFLOPS = 37.1  # tools/dmma_peak.cu on this pool (profiles/r01_probe_box.log)
-FP64_PEAK_SOURCE = "measured DMMA m16n8k16 register-only peak (tools/dmma_peak.cu); MEASURED_PEAKS.json has no fp64 entry"
+FP64_PEAK_SOURCE = "measured FP64 tensor-core peak, register-only mma.sync f64 (SASS DMMA.8x8x4) microbenchmark (tools/dmma_peak.cu, profiles/r01_probe_box.log); MEASURED_PEAKS.json has no fp64 entry"
 
 
 def parse():
