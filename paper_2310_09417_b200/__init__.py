@@ -47,5 +47,6 @@ from .skeleton import (
 )
 from .lu_state import BlockedLUState, adaptive_init, adaptive_step, interpolation_matrix
 from .cur import CurFactors, cur_decompose, cur_decompose_adaptive, pinv_apply, two_sided_id
+from .evaluate import row_id_error, stable_row_id_error
 
 __version__ = "0.1.0"

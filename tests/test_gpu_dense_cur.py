@@ -228,3 +228,29 @@ def test_adaptive_cur_fp32_composition(rs):
     a = a32.astype(np.float64)
     rec = a[:, cur.col_idx] @ cur.u_mid @ a[cur.row_idx]
     assert np.linalg.norm(a - rec) <= 1e-5 * np.linalg.norm(a)
+
+
+@pytest.mark.parametrize("kind", ["decay", "exact", "decay_T"])
+def test_row_id_error_evaluators(kind):
+    """row_id_error / stable_row_id_error on the device vs the oracle
+    (`skeleton.py:542-562`)."""
+    import paper_2310_09417_b200 as rs
+
+    g = np.random.default_rng(7)
+    if kind == "exact":
+        a = g.standard_normal((600, 40)) @ g.standard_normal((40, 300))
+    else:
+        a, _ = orc.gen_fast_decay(600, 300, 1e-10, 11)
+    if kind == "decay_T":
+        a = np.asfortranarray(a)  # column-major input path
+    spec = rs.SketchSpec("gaussian", 300, 64)
+    res = rs.rand_lupp(a, 64, spec, rs.RngStream(2))
+    e1 = rs.row_id_error(a, res)
+    e2 = rs.stable_row_id_error(a, res)
+    r1 = orc.row_id_error(a, res.row_idx, res.w)
+    r2 = orc.stable_row_id_error(a, res.row_idx)
+    na = np.linalg.norm(a)
+    assert abs(e1 - r1) <= 1e-9 * r1 + 1e-13 * na, (e1, r1)
+    assert abs(e2 - r2) <= 1e-7 * r2 + 1e-13 * na, (e2, r2)
+    with pytest.raises(ValueError):
+        rs.row_id_error(a, rs.SkeletonResult(rank=0))
