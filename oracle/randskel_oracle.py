@@ -185,6 +185,38 @@ def adaptive_init(a, b, seed, stream=0):
     return LUState(L[:b].copy(), L[b:].copy(), U, perm, y)
 
 
+RESIDUAL_STREAM = 1 << 40  # `skeleton.py:75`
+
+
+def adaptive_step(state, a, b, seed, stream, t):
+    """`skeleton.py:354-388` for block t: (e_schur, new state)."""
+    y = block(a, seed, stream, t, b)
+    u2, s = schur(state, y)
+    e = float(np.linalg.norm(s))
+    L, U, sperm, nc = lupp(s, allow_partial=True)
+    return e, extend(state, y, u2, L, U, sperm, nc)
+
+
+def draw_residual_sample(a, p, seed, stream=0):
+    """`skeleton.py:527-539` (Gaussian): a @ Omega_r, unit-variance Omega_r from
+    the stream's child(1 << 40)."""
+    return a @ gaussian(seed, child_stream(stream, RESIDUAL_STREAM), a.shape[1], p, unit=True)
+
+
+def residual_ur_estimates(state, a, p, seed, stream=0):
+    """`skeleton.py:463-524` (Gaussian): norms of the trailing p x p factor of
+    the dedicated sample, scaled by (4 log k / k) sqrt(m - k)."""
+    m = a.shape[0]
+    k = state.rank
+    y_r = draw_residual_sample(a, p, seed, stream)
+    _, s_r = schur(state, y_r)
+    L, U, _, nc = lupp(s_r, allow_partial=True)
+    norm_ur = float(np.linalg.norm(U)) if nc else 0.0
+    max_ur = float(np.abs(U).max()) if nc else 0.0
+    factor = (4.0 * np.log(k) / k) * np.sqrt(m - k)
+    return dict(norm_ur=norm_ur, max_ur=max_ur, est_norm=factor * norm_ur, est_max=factor * max_ur)
+
+
 def rand_lupp_adaptive(a, b, tau, seed, stream=0, max_rank=None, want_w=True, max_blocks=None):
     """`skeleton.py:391-460`: returns dict(rank, row_idx, w, trace, status).
 

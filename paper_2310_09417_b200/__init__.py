@@ -45,7 +45,15 @@ from .skeleton import (
     rand_lupp,
     rand_lupp_adaptive,
 )
-from .lu_state import BlockedLUState, adaptive_init, adaptive_step, interpolation_matrix
+from .lu_state import (
+    BlockedLUState,
+    ResidualEstimates,
+    adaptive_init,
+    adaptive_step,
+    draw_residual_sample,
+    interpolation_matrix,
+    residual_ur_estimates,
+)
 from .cur import CurFactors, cur_decompose, cur_decompose_adaptive, pinv_apply, two_sided_id
 from .evaluate import row_id_error, stable_row_id_error
 

@@ -8,7 +8,8 @@ for callers that drive the loop themselves.  Every product, solve and
 factorisation runs on the device kernels (`dense.py` here).
 """
 
-from dataclasses import dataclass
+import math
+from dataclasses import dataclass, replace
 
 import numpy as np
 import torch
@@ -17,7 +18,10 @@ from . import _device, dense
 from .errors import DimensionError
 from .sketching import make_sketch
 
-__all__ = ["BlockedLUState", "adaptive_init", "adaptive_step", "interpolation_matrix"]
+__all__ = ["BlockedLUState", "adaptive_init", "adaptive_step", "interpolation_matrix", "ResidualEstimates",
+           "draw_residual_sample", "residual_ur_estimates"]
+
+_RESIDUAL_STREAM = 1 << 40  # reference `skeleton.py:75`
 
 
 @dataclass
@@ -163,3 +167,59 @@ def interpolation_matrix(state):
               max(k, 1), _device.stream_handle())
     kind = "torch_cuda" if isinstance(state.L1, torch.Tensor) and state.L1.is_cuda else "numpy"
     return _kind_out(W, kind)
+
+
+@dataclass
+class ResidualEstimates:
+    """Error proxies from the trailing p x p factor of a dedicated sample
+    (reference `skeleton.py:142-149`)."""
+
+    norm_ur: float
+    max_ur: float
+    est_norm: float
+    est_max: float
+
+
+def draw_residual_sample(a, p, spec, rng):
+    """Dedicated sample ``a @ Omega_r`` (m x p) from ``rng.child(1 << 40)``,
+    unit-variance Gaussian Omega_r drawn on the device (reference
+    `skeleton.py:527-539`)."""
+    m, n = _device.shape_of(a)
+    A = _device.as_matrix(a)
+    stream = rng.child(_RESIDUAL_STREAM)
+    if spec.kind != "gaussian":
+        make_sketch(replace(spec, n=n, ell=p), stream)  # raises NotImplementedError
+    y = _device.sketch_omega(A, replace(spec, n=n, ell=p, scale="unit"), stream)
+    return _kind_out(y, A.kind)
+
+
+def residual_ur_estimates(state, a, p, spec, rng, sample_r=None):
+    """Norms of the trailing p x p LU factor of a dedicated sample reduced
+    against the state, scaled by ``(4 log k / k) sqrt(m - k)`` (reference
+    `skeleton.py:463-524`)."""
+    m, n = _device.shape_of(a)
+    if not 1 <= p < state.b:
+        raise DimensionError(f"oversample count must satisfy 1 <= p < b = {state.b}")
+    k = state.rank
+    if m - k < p:
+        raise DimensionError(f"need at least p = {p} rows beyond rank {k}")
+    if sample_r is None:
+        y_r = _dev(draw_residual_sample(a, p, spec, rng))
+    else:
+        shp = tuple(sample_r.shape)
+        if shp != (m, p):
+            raise DimensionError(f"sample_r must have shape {(m, p)}, got {shp}")
+        y_r = _dev(sample_r)
+    L1, L2 = _dev(state.L1), _dev(state.L2)
+    perm = _devi(state.perm)
+    _, s_r = _schur(L1, L2, perm, y_r)
+    _, U, _, nc = dense._lupp_partial_device(dense._mat(s_r.contiguous()))
+    if nc == 0:
+        norm_ur = max_ur = 0.0
+    else:
+        norm_ur = dense.frobenius_norm(U)
+        max_ur = float(U.abs().max().item())
+    factor = (4.0 * math.log(k) / k) * math.sqrt(m - k)
+    if spec.kind != "gaussian":
+        factor *= math.sqrt(p)
+    return ResidualEstimates(norm_ur=norm_ur, max_ur=max_ur, est_norm=factor * norm_ur, est_max=factor * max_ur)

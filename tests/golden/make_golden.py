@@ -157,6 +157,21 @@ def main():
         row_idx=res.row_idx, col_idx=col_idx, status=res.status,
         trace=np.array([[rec.k, rec.e_schur] for rec in res.trace]))
 
+    # ---- residual-U_r certificates and error evaluators --
+    a, _ = rs.gen_fast_decay(400, 300, 1e-12, rs.RngStream(70))
+    st = rs.adaptive_init(a, 16, spec(300, 16), rs.RngStream(71))
+    for _ in range(3):
+        _, st = rs.adaptive_step(st, a, spec(300, 16))
+    for p in (4, 15):
+        y_r = rs.draw_residual_sample(a, p, spec(300, 16), rs.RngStream(72))
+        est = rs.residual_ur_estimates(st, a, p, spec(300, 16), rs.RngStream(72))
+        put(f"resid_ur_p{p}", gen_seed=70, b=16, steps=3, seed=71, rseed=72, p=p, rank=st.rank,
+            perm=st.perm, y_r_sum=y_r.sum(), norm_ur=est.norm_ur, max_ur=est.max_ur,
+            est_norm=est.est_norm, est_max=est.est_max)
+    r = rs.rand_lupp(a, 48, spec(300, 48), rs.RngStream(73))
+    put("row_id_errors", gen_seed=70, k=48, seed=73, row_idx=r.row_idx,
+        err=rs.row_id_error(a, r), stable_err=rs.stable_row_id_error(a, r))
+
     path = os.path.join(OUT, "reference_golden.npz")
     flat = {}
     for name, arrays in cases.items():

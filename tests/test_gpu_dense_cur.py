@@ -254,3 +254,40 @@ def test_row_id_error_evaluators(kind):
     assert abs(e2 - r2) <= 1e-7 * r2 + 1e-13 * na, (e2, r2)
     with pytest.raises(ValueError):
         rs.row_id_error(a, rs.SkeletonResult(rank=0))
+
+
+@pytest.mark.parametrize("p", [4, 15])
+def test_residual_ur_estimates_vs_reference(p):
+    """Residual-U_r certificates on the LU-form state (`skeleton.py:463-539`)
+    against the reference's values (golden)."""
+    import paper_2310_09417_b200 as rs
+
+    g = golden(f"resid_ur_p{p}")
+    a, _ = orc.gen_fast_decay(400, 300, 1e-12, int(g["gen_seed"]))
+    spec = rs.SketchSpec("gaussian", 300, 16)
+    st = rs.adaptive_init(a, int(g["b"]), spec, rs.RngStream(int(g["seed"])))
+    for _ in range(int(g["steps"])):
+        _, st = rs.adaptive_step(st, a, spec)
+    assert st.rank == int(g["rank"])
+    assert np.array_equal(np.asarray(st.perm), g["perm"])
+    y_r = rs.draw_residual_sample(a, p, spec, rs.RngStream(int(g["rseed"])))
+    assert abs(y_r.sum() - float(g["y_r_sum"])) <= 1e-9 * np.abs(y_r).sum()
+    est = rs.residual_ur_estimates(st, a, p, spec, rs.RngStream(int(g["rseed"])))
+    for key in ("norm_ur", "max_ur", "est_norm", "est_max"):
+        ref = float(g[key])
+        assert abs(getattr(est, key) - ref) <= 1e-6 * abs(ref) + 1e-300, (key, getattr(est, key), ref)
+    est2 = rs.residual_ur_estimates(st, a, p, spec, None, sample_r=y_r)
+    assert est2 == est
+    with pytest.raises(rs.DimensionError):
+        rs.residual_ur_estimates(st, a, 16, spec, rs.RngStream(0))
+
+
+def test_row_id_errors_vs_reference():
+    import paper_2310_09417_b200 as rs
+
+    g = golden("row_id_errors")
+    a, _ = orc.gen_fast_decay(400, 300, 1e-12, int(g["gen_seed"]))
+    r = rs.rand_lupp(a, int(g["k"]), rs.SketchSpec("gaussian", 300, 48), rs.RngStream(int(g["seed"])))
+    assert np.array_equal(r.row_idx, g["row_idx"])
+    assert abs(rs.row_id_error(a, r) - float(g["err"])) <= 1e-6 * float(g["err"])
+    assert abs(rs.stable_row_id_error(a, r) - float(g["stable_err"])) <= 1e-6 * float(g["stable_err"])

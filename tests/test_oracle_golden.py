@@ -167,3 +167,31 @@ def test_adaptive_cfg2_recipe_n2000():
     assert np.array_equal(out["row_idx"], g["row_idx"])
     resid = np.linalg.norm(a.T - out["w"] @ a.T[out["row_idx"]]) / np.linalg.norm(a)
     assert abs(resid - float(g["resid"])) <= 1e-2 * float(g["resid"])
+
+
+@pytest.mark.parametrize("p", [4, 15])
+def test_oracle_residual_ur_estimates(p):
+    """Residual-U_r certificates (`skeleton.py:463-539`) vs the reference."""
+    g = golden(f"resid_ur_p{p}")
+    a, _ = orc.gen_fast_decay(400, 300, 1e-12, int(g["gen_seed"]))
+    st = orc.adaptive_init(a, int(g["b"]), int(g["seed"]))
+    for t in range(1, int(g["steps"]) + 1):
+        _, st = orc.adaptive_step(st, a, int(g["b"]), int(g["seed"]), 0, t)
+    assert st.rank == int(g["rank"])
+    assert np.array_equal(st.perm, g["perm"])
+    y_r = orc.draw_residual_sample(a, p, int(g["rseed"]))
+    assert abs(y_r.sum() - float(g["y_r_sum"])) <= 1e-9 * np.abs(y_r).sum()
+    est = orc.residual_ur_estimates(st, a, p, int(g["rseed"]))
+    for key in ("norm_ur", "max_ur", "est_norm", "est_max"):
+        assert abs(est[key] - float(g[key])) <= 1e-9 * abs(float(g[key])) + 1e-300, key
+
+
+def test_oracle_row_id_errors():
+    g = golden("row_id_errors")
+    a, _ = orc.gen_fast_decay(400, 300, 1e-12, int(g["gen_seed"]))
+    r = orc.rand_lupp(a, int(g["k"]), int(g["seed"]))
+    assert np.array_equal(r[0], g["row_idx"])
+    e = orc.row_id_error(a, r[0], r[1])
+    s = orc.stable_row_id_error(a, r[0])
+    assert abs(e - float(g["err"])) <= 1e-8 * float(g["err"])
+    assert abs(s - float(g["stable_err"])) <= 1e-8 * float(g["stable_err"])
