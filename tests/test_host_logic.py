@@ -96,3 +96,28 @@ def test_philox_key_matches_numpy_conversion():
         k = np.random.Philox(key=[seed, stream]).state["state"]["key"]
         assert s.philox_key() == (int(k[0]), int(k[1]))
     assert rs.RngStream(0, 0xa706dd2f4d197e6f).philox_key()[1] != 0xa706dd2f4d197e6f
+
+
+def test_zoo_generators_match_reference_construction():
+    """gen_fast_decay / gen_kahan / gen_chan build the reference's matrices
+    bit for bit (the oracle restates `zoo.py:36-104`)."""
+    import os
+    import sys
+
+    import numpy as np
+    import paper_2310_09417_b200 as rs
+
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle"))
+    import randskel_oracle as orc
+
+    a, d = rs.gen_fast_decay(60, 40, 1e-6, rs.RngStream(7, 3))
+    a2, d2 = orc.gen_fast_decay(60, 40, 1e-6, 7, 3)
+    assert np.array_equal(a, a2) and np.array_equal(d, d2)
+    assert np.array_equal(rs.gen_kahan(30, 0.9), orc.gen_kahan(30, 0.9))
+    assert np.array_equal(rs.gen_chan(12), orc.gen_chan(12))
+    import pytest
+
+    with pytest.raises(rs.DimensionError):
+        rs.gen_fast_decay(3, 5, 0.5, rs.RngStream(0))
+    with pytest.raises(ValueError):
+        rs.gen_kahan(4, 1.5)
