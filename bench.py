@@ -41,7 +41,7 @@ def parse():
     p.add_argument("--steps", type=int, default=3)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--n", type=int, default=20000)
+    p.add_argument("--size", "--n", dest="n", type=int, default=20000)
     p.add_argument("--b", type=int, default=64)
     p.add_argument("--tau", type=float, default=1e-8)
     p.add_argument("--seed", type=int, default=0)
@@ -210,10 +210,18 @@ def main():
     import torch
     import torch.distributed as dist
 
+    # BENCH_BACKEND=gloo runs the N > 1 plumbing on a box with fewer GPUs than
+    # ranks (ranks share devices; host-staged collectives) -- a functional
+    # check only, the numbers are not multi-GPU numbers.
+    backend = os.environ.get("BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     import paper_2310_09417_b200 as rs
     from paper_2310_09417_b200 import _lib, skeleton
@@ -345,7 +353,7 @@ def main():
                 "workload": f"cfg2: rand_lupp_adaptive(A.T, b={b}, tau={tau:g} abs) on a {n}x{n} "
                             f"fp64 fast-decay matrix (beta=1e-16, Haar bases), seed {args.seed}",
                 "n": n, "b": b, "tau": tau, "rank": k, "status": res.status,
-                "blocks": len(res.trace) + 1, "parallelism": (f"A column-sharded over {world} GPUs (NCCL all-reduce of Y_top, S, T_P per block)"
+                "blocks": len(res.trace) + 1, "parallelism": (f"A column-sharded over {world} GPUs ({backend} all-reduce of Y_top, S, T_P per block)"
                                 if sharded else "1 GPU"),
                 "l2": "inputs (A: %.1f GB) larger than L2 between steps" % (n * n * 8 / 1e9),
             },

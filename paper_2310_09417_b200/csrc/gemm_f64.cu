@@ -64,6 +64,8 @@ using Cfg8 = GemmCfg<128, 64, 32, 2, 2, 2, 2>;   // 4 warps of 64x32, BK 32
 using Cfg9 = GemmCfg<64, 32, 16, 2, 2, 4, 4>;    // 4 warps of 32x16, 4 stages, 4 CTAs/SM
 using Cfg10 = GemmCfg<64, 64, 32, 2, 2, 3, 2>;   // 4 warps of 32x32, BK 32
 using Cfg11 = GemmCfg<128, 32, 16, 4, 1, 4, 3>;  // 4 warps of 32x32 along M, 4 stages
+using Cfg12 = GemmCfg<128, 64, 32, 4, 2, 2, 2>;  // 8 warps of 32x32, BK 32
+using Cfg13 = GemmCfg<256, 64, 32, 4, 2, 2, 1>;  // 8 warps of 64x32, BK 32, 1 CTA/SM
 // Stream-K partial slots: 2 per CTA, THREADS * ACC doubles each; every config
 // has MINB * THREADS * ACC <= 16384 doubles per SM.
 constexpr int SK_SLOT_DOUBLES_PER_SM = 16384;
@@ -419,6 +421,8 @@ int launch_dgemm(const DGemmParams& p, bool a_col, cudaStream_t st) {
     case 9: return launch_cfg<Cfg9>(p, a_col, vec2, st);
     case 10: return launch_cfg<Cfg10>(p, a_col, vec2, st);
     case 11: return launch_cfg<Cfg11>(p, a_col, vec2, st);
+    case 12: return launch_cfg<Cfg12>(p, a_col, vec2, st);
+    case 13: return launch_cfg<Cfg13>(p, a_col, vec2, st);
     default:
       // Measured on B200 (tools/tune_gemm.sh): the column-major sketch operand
       // prefers 64x32 warp tiles (31.4 TF/s vs 28.2), the gathered row-major
