@@ -277,6 +277,10 @@ def main():
     f = algo_flops(n, n, k, b)
     value = f / (ms_max * 1e-3) / 1e12  # one n x n problem split over the ranks
 
+    # accuracy of the timed result (outside the timed region): ||A.T - W A.T[I]||_F / ||A||_F
+    resid = None
+    if not sharded:
+        resid = rs.row_id_error(a.T, res) / rs.frobenius_norm(a)
     phases = timer.totals()
     counts = timer.launches()
     blocks = counts.get("sketch_gemm", 0)
@@ -353,6 +357,7 @@ def main():
                 "workload": f"cfg2: rand_lupp_adaptive(A.T, b={b}, tau={tau:g} abs) on a {n}x{n} "
                             f"fp64 fast-decay matrix (beta=1e-16, Haar bases), seed {args.seed}",
                 "n": n, "b": b, "tau": tau, "rank": k, "status": res.status,
+                "row_id_error_rel": resid,
                 "blocks": len(res.trace) + 1, "parallelism": (f"A column-sharded over {world} GPUs ({backend} all-reduce of Y_top, S, T_P per block)"
                                 if sharded else "1 GPU"),
                 "l2": "inputs (A: %.1f GB) larger than L2 between steps" % (n * n * 8 / 1e9),

@@ -193,7 +193,7 @@ def h2d(arr):
     dst = out.view(-1).view(torch.uint8)
     ring = _stage_ring(dev)
     pool = _copy_pool()
-    nthr = max(1, min(8, pool._max_workers))
+    nthr = max(1, min(16, pool._max_workers))
     cs = ring["stream"]
     cs.wait_stream(torch.cuda.current_stream(dev))  # `out` was allocated on the compute stream
     for i, c0 in enumerate(range(0, nbytes, _STAGE_BYTES)):

@@ -4,6 +4,7 @@ mkdir -p gpurun_out
 python -m pytest tests -m gpu -q --timeout 900 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
+python bench_configs.py --cpu > gpurun_out/configs.jsonl 2> gpurun_out/configs.err; echo "configs rc=$?" >> gpurun_out/configs.err
 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.log 2>&1; echo "ref rc=$?" >> gpurun_out/bench_ref.log
 KRE='regex:dgemm|panel|rank_update|sumsq|trinv|gather|perm_update|scatter|fixup|iota|transpose|rng_'
 python bench.py --steps 1 --warmup 1 --e2e-steps 0 --no-cpu > gpurun_out/plain_bench.log 2>&1 && \
