@@ -133,6 +133,63 @@ def cfg4(do_cpu):
     return line
 
 
+def _fwht_rows_(x, chunk=4096):
+    """x <- H x / sqrt(n) in place (H the n x n Walsh-Hadamard matrix, n a
+    power of two), column chunk by column chunk."""
+    n = x.shape[0]
+    for c0 in range(0, x.shape[1], chunk):
+        y = x[:, c0:c0 + chunk].contiguous()
+        cw = y.shape[1]
+        h = 1
+        while h < n:
+            v = y.view(n // (2 * h), 2, h, cw)
+            a, b = v[:, 0].clone(), v[:, 1]
+            v[:, 0].add_(b)
+            v[:, 1].neg_().add_(a)
+            h *= 2
+        y.mul_(1.0 / np.sqrt(n))
+        x[:, c0:c0 + chunk] = y
+
+
+def gen_fast_decay_hadamard(n, beta, seed):
+    """cfg5 input (device generator with an exact spectrum):
+    A = U diag(d) V^T, d_i = beta^((i-1)/(n-1)), with orthogonal
+    U = H S1 H S2 and V = H S3 H S4 (H Walsh-Hadamard, S random signs)."""
+    g = torch.Generator(device="cuda")
+    g.manual_seed(seed)
+    signs = [torch.randint(0, 2, (n, 1), generator=g, device="cuda").double() * 2 - 1 for _ in range(4)]
+    d = beta ** (torch.arange(n, dtype=torch.float64, device="cuda") / (n - 1))
+    x = torch.eye(n, dtype=torch.float64, device="cuda")   # V^T = S4 H S3 H
+    _fwht_rows_(x)
+    x.mul_(signs[2])
+    _fwht_rows_(x)
+    x.mul_(signs[3])
+    x.mul_(d[:, None])                                     # D V^T
+    x.mul_(signs[1])                                       # U = H S1 H S2
+    _fwht_rows_(x)
+    x.mul_(signs[0])
+    _fwht_rows_(x)
+    return x
+
+
+def cfg5(do_cpu):
+    """cfg5 at one GPU (the sharded form runs this loop split over ranks):
+    adaptive column ID of a 65536^2 fp64 fast-decay matrix, b=64, tau=1e-8."""
+    n, b, tau = int(os.environ.get("CFG5_N", 65536)), 64, 1e-8
+    a = gen_fast_decay_hadamard(n, 1e-16, 0)
+    torch.cuda.synchronize()
+    spec = rs.SketchSpec("gaussian", n, b)
+    ms, res = dev_time(lambda: rs.rand_lupp_adaptive(a.T, b, tau, spec, rs.RngStream(0)), reps=1)
+    k = res.rank
+    f = algo_flops(n, n, k, b)
+    line = {"config": f"cfg5 adaptive column ID {n}^2 fp64 fast-decay (Hadamard bases) b=64 tau=1e-8, 1 GPU",
+            "rank": k, "status": res.status, "blocks": len(res.trace) + 1, "gpu_ms": ms,
+            "tflops": f / ms / 1e9, "frac_fp64_dmma": f / ms / 1e9 / FP64_DMMA_PEAK_TFLOPS,
+            "cpu": "infeasible here (SURVEY 8d: ~2-4 h on the host cores)"}
+    del res
+    return line
+
+
 if __name__ == "__main__":
     do_cpu = "--cpu" in sys.argv
     which = [a for a in sys.argv[1:] if a.startswith("cfg")] or ["cfg1", "cfg3", "cfg4"]

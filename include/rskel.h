@@ -195,10 +195,13 @@ int rs_iota(int64_t* p, int n, void* stream);
  *   *count                number of local remaining rows
  * With sub != NULL (just after an absorb of nc columns at rank k_old = k - nc,
  * lrow_old the previous lrow): src_row[r] / wsrc[r] = previous local T row /
- * Schur row of local row r, tp_src[j] = previous local T row of pivot j or -1. */
+ * Schur row of local row r, tp_src[j] = previous local T row of pivot j or -1.
+ * Rows [*count, pad_to) get harmless entries (loc 0, spos -1, src_row 0,
+ * wsrc 0) for launches sized by an upper bound of the row count. */
 int rs_shard_maps(const int64_t* perm, int m, int k, long long lo, long long hi, const int64_t* lrow_old,
                   const int64_t* sub, int k_old, int nc, int64_t* lrow, int64_t* loc, int64_t* spos,
-                  int64_t* src_row, int64_t* wsrc, int64_t* tp_src, int64_t* ytop_src, int* count, void* stream);
+                  int64_t* src_row, int64_t* wsrc, int64_t* tp_src, int64_t* ytop_src, int* count, int pad_to,
+                  void* stream);
 
 /* dst[idx[i], :] = src[i, :] for idx[i] >= 0. */
 int rs_scatter_rows(const double* src, long long lds, const int64_t* idx, int nrows, int ncols, double* dst,

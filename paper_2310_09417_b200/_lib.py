@@ -53,7 +53,7 @@ SIGNATURES = {
                              ctypes.c_size_t, _p, _p]),
     "rs_iota": (_c_int, [_p, _c_int, _p]),
     "rs_shard_maps": (_c_int, [_p, _c_int, _c_int, _c_ll, _c_ll, _p, _p, _c_int, _c_int, _p, _p, _p, _p, _p,
-                               _p, _p, _p, _p]),
+                               _p, _p, _p, _c_int, _p]),
     "rs_scatter_rows": (_c_int, [_p, _c_ll, _p, _c_int, _c_int, _p, _c_ll, _p]),
     "rs_scatter_interp_local": (_c_int, [_p, _c_ll, _p, _c_int, _p, _c_int, _c_ll, _c_ll, _p, _c_ll, _p]),
 }

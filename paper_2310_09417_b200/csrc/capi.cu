@@ -258,9 +258,10 @@ int rs_iota(int64_t* p, int n, void* stream) { return rs::launch_iota(p, n, S(st
 
 int rs_shard_maps(const int64_t* perm, int m, int k, long long lo, long long hi, const int64_t* lrow_old,
                   const int64_t* sub, int k_old, int nc, int64_t* lrow, int64_t* loc, int64_t* spos,
-                  int64_t* src_row, int64_t* wsrc, int64_t* tp_src, int64_t* ytop_src, int* count, void* stream) {
+                  int64_t* src_row, int64_t* wsrc, int64_t* tp_src, int64_t* ytop_src, int* count, int pad_to,
+                  void* stream) {
   return rs::launch_shard_maps(perm, m, k, lo, hi, lrow_old, sub, k_old, nc, lrow, loc, spos, src_row, wsrc,
-                               tp_src, ytop_src, count, S(stream));
+                               tp_src, ytop_src, count, pad_to, S(stream));
 }
 
 int rs_scatter_rows(const double* src, long long lds, const int64_t* idx, int nrows, int ncols, double* dst,

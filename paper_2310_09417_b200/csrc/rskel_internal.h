@@ -60,7 +60,7 @@ int launch_iota(int64_t* p, int n, cudaStream_t st);
 int launch_shard_maps(const int64_t* perm, int m, int k, long long lo, long long hi, const int64_t* lrow_old,
                       const int64_t* sub, int k_old, int nc, int64_t* lrow, int64_t* loc, int64_t* spos,
                       int64_t* src_row, int64_t* wsrc, int64_t* tp_src, int64_t* ytop_src, int* count,
-                      cudaStream_t st);
+                      int pad_to, cudaStream_t st);
 int launch_scatter_rows(const double* src, long long lds, const int64_t* idx, int nrows, int ncols, double* dst,
                         long long ldd, cudaStream_t st);
 int launch_scatter_interp_local(const double* T, long long ldt, const int64_t* perm, int k, const int64_t* loc,

@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(MAP_T) shard_maps_kernel(
     const int64_t* __restrict__ lrow_old, const int64_t* __restrict__ sub, int k_old, int nc,
     int64_t* __restrict__ lrow, int64_t* __restrict__ loc, int64_t* __restrict__ spos,
     int64_t* __restrict__ src_row, int64_t* __restrict__ wsrc, int64_t* __restrict__ tp_src,
-    int64_t* __restrict__ ytop_src, int* __restrict__ count) {
+    int64_t* __restrict__ ytop_src, int* __restrict__ count, int pad_to) {
   const int t = threadIdx.x;
   for (int p = t; p < k; p += MAP_T) {
     const int64_t c = perm[p];
@@ -82,19 +82,29 @@ __global__ void __launch_bounds__(MAP_T) shard_maps_kernel(
     }
     ++r;
   }
+  // rows [total, pad_to): harmless entries for launches sized by an upper
+  // bound of the row count (valid gather indices, no scatter)
+  for (int r2 = total + t; r2 < pad_to; r2 += MAP_T) {
+    loc[r2] = 0;
+    spos[r2] = -1;
+    if (sub != nullptr) {
+      src_row[r2] = 0;
+      wsrc[r2] = 0;
+    }
+  }
   if (t == 0) *count = total;
 }
 
 int launch_shard_maps(const int64_t* perm, int m, int k, long long lo, long long hi, const int64_t* lrow_old,
                       const int64_t* sub, int k_old, int nc, int64_t* lrow, int64_t* loc, int64_t* spos,
                       int64_t* src_row, int64_t* wsrc, int64_t* tp_src, int64_t* ytop_src, int* count,
-                      cudaStream_t st) {
+                      int pad_to, cudaStream_t st) {
   if (m < 0 || k < 0 || k > m || lo > hi) return RS_ERR_ARG;
   if (sub != nullptr && (lrow_old == nullptr || src_row == nullptr || wsrc == nullptr || tp_src == nullptr ||
                          k_old < 0 || nc < 0 || k_old + nc != k))
     return RS_ERR_ARG;
   shard_maps_kernel<<<1, MAP_T, 0, st>>>(perm, m, k, lo, hi, lrow_old, sub, k_old, nc, lrow, loc, spos, src_row,
-                                         wsrc, tp_src, ytop_src, count);
+                                         wsrc, tp_src, ytop_src, count, pad_to);
   count_launch(1);
   return cudaGetLastError() == cudaSuccess ? RS_OK : RS_ERR_CUDA;
 }

@@ -110,11 +110,11 @@ class DeviceShardOps:
         _lib.call("rs_perm_update", perm.data_ptr(), perm_new.data_ptr(), m, k, sub.data_ptr(), self.st)
 
     def maps(self, perm, m, k, lo, hi, lrow_old, sub, k_old, nc, lrow, loc, spos, src_row, wsrc, tp_src,
-             ytop_src, count):
+             ytop_src, count, pad_to=0):
         p = (lambda x: x.data_ptr() if x is not None else None)
         _lib.call("rs_shard_maps", perm.data_ptr(), m, k, lo, hi, p(lrow_old), p(sub), k_old, nc, lrow.data_ptr(),
                   loc.data_ptr(), spos.data_ptr(), p(src_row), p(wsrc), p(tp_src), ytop_src.data_ptr(),
-                  count.data_ptr(), self.st)
+                  count.data_ptr(), pad_to, self.st)
 
     def what(self, S, lds, sub, nc, wsrc, r, linv, out, ldo):
         """out[i, :nc] = S[wsrc[i]] L1^{-1}, L1 = unit lower part of rows S[sub[:nc]]."""
@@ -197,6 +197,14 @@ def rand_lupp_adaptive_sharded(a_local, b, tau, spec, rng, max_rank=None, group=
 
 
 class _ShardedLoop:
+    """One host readback per block, as the single-GPU driver: the absorb of
+    block t is enqueued assuming a full-width elimination (nc = b) and sized
+    by the previous exact local row count (an upper bound; padded map entries
+    are inert); block t+1's sketch and Schur exchange follow at once, and one
+    readback returns (e2 of t+1, eliminated columns of t, new row count).  A
+    short block (an exactly zero pivot) is re-absorbed from its own factored
+    Schur block, kept in the other S buffer."""
+
     def __init__(self, ops, group, m, n, lo, hi, b, tau, rng, max_rank):
         self.ops, self.group = ops, group
         self.m, self.n, self.lo, self.hi = m, n, lo, hi
@@ -208,23 +216,25 @@ class _ShardedLoop:
         self.lrow = [o.i64(m), o.i64(m)]
         self.loc, self.spos, self.src_row, self.wsrc = o.i64(mg), o.i64(mg), o.i64(mg), o.i64(mg)
         self.tp_src, self.ytop_src = o.i64(b), o.i64(kcap)
-        self.count, self.ncols = o.i32(1), o.i32(1)
+        self.meta = o.i32(2)  # [ncols of the last panel, local row count after the last maps]
         self.sub = o.i64(m)
         self.iota_b = o.i64(b)
         o.iota(self.iota_b, b)
         self.Y = o.f64(mg * b)
         self.Ytop = o.f64(kcap * b)
         self.Sg = o.f64(mg * b)
-        self.S = o.f64(m * b)
+        self.S = [o.f64(m * b), o.f64(m * b)]
+        self.scur = 0
         self.TP = o.f64(b * kcap)
         self.linv = o.f64(MAX_BLOCK * MAX_BLOCK)
         self.e2 = o.f64(1)
-        pts = {kcap, min(kcap, max(0, m - mg)), min(kcap, m // 2), min(kcap, (m + 1) // 2)}
-        cap = max(1, max(min(mg, m - kk) * kk for kk in pts))
+        # T rows are written up to the row-count bound (<= min(mg, m - k_old)) at ld k_new
+        pts = {kcap, min(kcap, max(0, m - mg + b)), min(kcap, (m + b) // 2), min(kcap, (m + b + 1) // 2)}
+        cap = max(1, max(min(mg, m - kk + b) * kk for kk in pts))
         self.T = [o.f64(cap), o.f64(cap)]
         self.cur = 0
         self.k = 0
-        self.r = mg
+        self.r = mg  # upper bound of the local row count (exact after each readback)
 
     def _schur(self):
         o, b, k = self.ops, self.b, self.k
@@ -234,42 +244,46 @@ class _ShardedLoop:
             _allreduce(self.Ytop[: k * b], self.group)
         o.schur(self.r, k, b, Tg, self.Ytop, self.Y, self.loc, self.Sg)
         R = self.m - k
-        S = self.S[: R * b]
+        S = self.S[self.scur][: R * b]
         S.zero_()
         o.scatter_rows(self.Sg, b, self.spos, self.r, b, S, b)
         _allreduce(S, self.group)
         o.sumsq(S, R, b, self.e2)
 
     def _absorb(self, nc):
+        """Fold nc factored columns of the current S into (T, perm); launches
+        sized by the row-count bound self.r."""
         o, b, m = self.ops, self.b, self.m
-        k_old, cur = self.k, self.cur
+        k_old, cur, S = self.k, self.cur, self.S[self.scur]
         k_new = k_old + nc
         nxt = 1 - cur
+        rb = self.r
         o.perm_update(self.perm[cur], self.perm[nxt], m, k_old, self.sub)
         o.maps(self.perm[nxt], m, k_new, self.lo, self.hi, self.lrow[cur], self.sub, k_old, nc, self.lrow[nxt],
-               self.loc, self.spos, self.src_row, self.wsrc, self.tp_src, self.ytop_src, self.count)
-        (r_new,) = o.read(self.count)
+               self.loc, self.spos, self.src_row, self.wsrc, self.tp_src, self.ytop_src, self.meta[1:], rb)
         Tg, Tn = self.T[cur], self.T[nxt]
         if k_old > 0 and nc > 0:
             o.gather_rows(Tg, k_old, self.tp_src, nc, k_old, self.TP, k_old)
             _allreduce(self.TP[: nc * k_old], self.group)
         if nc > 0:
-            o.what(self.S, b, self.sub, nc, self.wsrc, r_new, self.linv, Tn[k_old:], k_new)
+            o.what(S, b, self.sub, nc, self.wsrc, rb, self.linv, Tn[k_old:], k_new)
             if k_old > 0:
-                o.t_update(r_new, k_old, nc, Tn, k_new, self.TP, self.iota_b, Tg, self.src_row)
-        self.cur, self.k, self.r = nxt, k_new, r_new
+                o.t_update(rb, k_old, nc, Tn, k_new, self.TP, self.iota_b, Tg, self.src_row)
+        self._prev = (cur, k_old)
+        self.cur, self.k = nxt, k_new
 
     def run(self):
         o, b, m, tau = self.ops, self.b, self.m, self.tau
         o.iota(self.perm[0], m)
         o.maps(self.perm[0], m, 0, self.lo, self.hi, None, None, 0, 0, self.lrow[0], self.loc, self.spos, None,
-               None, None, self.ytop_src, self.count)
+               None, None, self.ytop_src, self.meta[1:], 0)
         trace = ErrorTrace()
         status = STATUS_NOT_CONVERGED
-        t = 0
         from . import skeleton
 
         prof = skeleton._PHASE_TIMER or skeleton._NullTimer()
+        pending = False  # speculative full-width absorb awaiting its ncols
+        t = 0
         while True:
             om = o.omega(self.rng, t, b)
             tok = prof.start("sketch_gemm")
@@ -278,7 +292,17 @@ class _ShardedLoop:
             tok = prof.start("schur_exchange")
             self._schur()
             prof.stop(tok)
-            (e2,) = o.read(self.e2)
+            e2, nc_prev, r_now = o.read(self.e2, self.meta[0:1], self.meta[1:2])
+            if pending:
+                pending = False
+                if nc_prev < b:  # zero pivot mid-block: redo the absorb truncated
+                    self.cur, self.k = self._prev
+                    self.scur = 1 - self.scur
+                    self._absorb(nc_prev)
+                    (self.r,) = o.read(self.meta[1:2])
+                    status = STATUS_RANK_EXHAUSTED
+                    break
+            self.r = r_now
             if t == 0:
                 # adaptive_init (`skeleton.py:298-314`): full lupp of block 0
                 if not math.isfinite(e2):
@@ -295,18 +319,18 @@ class _ShardedLoop:
                     raise ValueError("matrix contains non-finite entries")
             R = m - self.k
             tok = prof.start("panel")
-            o.panel(self.S, R, b, self.sub, self.ncols)
+            o.panel(self.S[self.scur], R, b, self.sub, self.meta[0:1])
             prof.stop(tok)
-            (nc,) = o.read(self.ncols)
-            if t == 0 and nc < b:
-                raise RankDeficientError(nc)
+            if t == 0:
+                (nc,) = o.read(self.meta[0:1])
+                if nc < b:
+                    raise RankDeficientError(nc)
             tok = prof.start("absorb")
-            self._absorb(nc)
+            self._absorb(b)
             prof.stop(tok)
+            self.scur = 1 - self.scur  # the next Schur block goes to the other buffer
+            pending = True
             t += 1
-            if nc < b:
-                status = STATUS_RANK_EXHAUSTED
-                break
         k = self.k
         mg = self.hi - self.lo
         W = o.f64(mg * k)

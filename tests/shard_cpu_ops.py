@@ -83,7 +83,7 @@ class CpuShardOps:
         q[k:m] = p[k + s[: m - k]]
 
     def maps(self, perm, m, k, lo, hi, lrow_old, sub, k_old, nc, lrow, loc, spos, src_row, wsrc, tp_src,
-             ytop_src, count):
+             ytop_src, count, pad_to=0):
         p = _np(perm)[:m]
         own = (p >= lo) & (p < hi)
         ys = _np(ytop_src)
@@ -101,6 +101,12 @@ class CpuShardOps:
             _np(src_row)[:r] = lo_old[k_old + j]
             _np(wsrc)[:r] = j
             _np(tp_src)[:nc] = lo_old[k_old + s[:nc]]
+        if pad_to > r:
+            _np(loc)[r:pad_to] = 0
+            _np(spos)[r:pad_to] = -1
+            if sub is not None:
+                _np(src_row)[r:pad_to] = 0
+                _np(wsrc)[r:pad_to] = 0
         _np(count)[0] = r
 
     def what(self, S, lds, sub, nc, wsrc, r, linv, out, ldo):
