@@ -64,6 +64,8 @@ class DeviceShardOps:
         self.dev = _device.device()
         self.ws = _device.workspace()
         self.st = _device.stream_handle()
+        self.host_rng = _device.host_rng()
+        self.rng_status = torch.zeros(4096, dtype=torch.int32, device=self.dev)
 
     def f64(self, n):
         return torch.empty(max(int(n), 1), dtype=torch.float64, device=self.dev)
@@ -75,8 +77,21 @@ class DeviceShardOps:
         return torch.empty(max(int(n), 1), dtype=torch.int32, device=self.dev)
 
     def omega(self, rng, t, b):
-        """Omega_t = rng.child(t) Gaussian block (n x b), drawn on this device."""
-        return _device.gaussian(rng.child(t), self.a.shape[1], b)
+        """Omega_t = rng.child(t) Gaussian block (n x b), drawn on this device
+        without a host sync (statuses checked once at the end, `rng_ok`)."""
+        n = self.a.shape[1]
+        if self.host_rng:
+            return torch.as_tensor(_device.host_gaussian(rng.child(t), n, b)).to(self.dev)
+        slot = t % self.rng_status.numel()
+        return _device.gaussian(rng.child(t), n, b, status=self.rng_status[slot:slot + 1])
+
+    def rng_ok(self):
+        """True if every device draw was resolved (else rerun with host draws)."""
+        if self.host_rng or not bool(self.rng_status.any()):
+            return True
+        self.host_rng = True
+        self.rng_status.zero_()
+        return False
 
     def sketch(self, om, b, out):
         m, n = self.a.shape
@@ -193,7 +208,16 @@ def rand_lupp_adaptive_sharded(a_local, b, tau, spec, rng, max_rank=None, group=
     if max_rank is None:
         max_rank = max(b, min(m, n) - b)
     max_rank = min(max_rank, min(m, n))
-    return _ShardedLoop(ops, group, m, n, lo, hi, b, tau, rng, max_rank).run()
+    res = _ShardedLoop(ops, group, m, n, lo, hi, b, tau, rng, max_rank).run()
+    ok = torch.tensor([1 if (not hasattr(ops, "rng_ok") or ops.rng_ok()) else 0], dtype=torch.int32,
+                      device=ops.dev)
+    if _world(group)[0] > 1:
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+    if int(ok.item()) == 0:  # a draw the device resolver could not place (never observed): host draws
+        if hasattr(ops, "host_rng"):
+            ops.host_rng = True
+        res = _ShardedLoop(ops, group, m, n, lo, hi, b, tau, rng, max_rank).run()
+    return res
 
 
 class _ShardedLoop:
@@ -220,7 +244,7 @@ class _ShardedLoop:
         self.sub = o.i64(m)
         self.iota_b = o.i64(b)
         o.iota(self.iota_b, b)
-        self.Y = o.f64(mg * b)
+        self.Ys = [o.f64(mg * b), o.f64(mg * b)]  # sketch of block t and the look-ahead t+1
         self.Ytop = o.f64(kcap * b)
         self.Sg = o.f64(mg * b)
         self.S = [o.f64(m * b), o.f64(m * b)]
@@ -236,13 +260,13 @@ class _ShardedLoop:
         self.k = 0
         self.r = mg  # upper bound of the local row count (exact after each readback)
 
-    def _schur(self):
+    def _schur(self, Y):
         o, b, k = self.ops, self.b, self.k
         Tg = self.T[self.cur]
         if k > 0:
-            o.gather_rows(self.Y, b, self.ytop_src, k, b, self.Ytop, b)
+            o.gather_rows(Y, b, self.ytop_src, k, b, self.Ytop, b)
             _allreduce(self.Ytop[: k * b], self.group)
-        o.schur(self.r, k, b, Tg, self.Ytop, self.Y, self.loc, self.Sg)
+        o.schur(self.r, k, b, Tg, self.Ytop, Y, self.loc, self.Sg)
         R = self.m - k
         S = self.S[self.scur][: R * b]
         S.zero_()
@@ -283,15 +307,25 @@ class _ShardedLoop:
 
         prof = skeleton._PHASE_TIMER or skeleton._NullTimer()
         pending = False  # speculative full-width absorb awaiting its ncols
+        sketched = set()
+
+        def sketch(tt):
+            if tt in sketched:
+                return
+            sketched.add(tt)
+            om = o.omega(self.rng, tt, b)
+            tok = prof.start("sketch_gemm")
+            o.sketch(om, b, self.Ys[tt % 2])
+            prof.stop(tok)
+
         t = 0
         while True:
-            om = o.omega(self.rng, t, b)
-            tok = prof.start("sketch_gemm")
-            o.sketch(om, b, self.Y)
-            prof.stop(tok)
+            sketch(t)
             tok = prof.start("schur_exchange")
-            self._schur()
+            self._schur(self.Ys[t % 2])
             prof.stop(tok)
+            if t > 0 and self.k + 2 * b <= self.max_rank:
+                sketch(t + 1)  # look-ahead: the GPU keeps busy while the host reads back
             e2, nc_prev, r_now = o.read(self.e2, self.meta[0:1], self.meta[1:2])
             if pending:
                 pending = False
