@@ -48,22 +48,38 @@ def up_to_date():
 
 
 def build(force=False, verbose=False):
-    """Compile every .cu under csrc/ into librskel.so (skipped when fresh)."""
+    """Compile every .cu under csrc/ (in parallel, one object each) and link
+    librskel.so (skipped when fresh)."""
     if not force and up_to_date():
         return LIB_PATH
-    cmd = [
-        _nvcc(), *ARCH_FLAGS, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
-        "-Xcompiler", "-fPIC", "-shared", "-I", INCLUDE,
-        "-o", LIB_PATH + ".tmp", *sources(),
-    ]
+    import tempfile
+    from concurrent.futures import ThreadPoolExecutor
+
+    nvcc = _nvcc()
+    flags = [*ARCH_FLAGS, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
+             "-I", INCLUDE]
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    if res.returncode != 0:
-        sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building librskel.so")
-    if verbose:
-        sys.stderr.write(res.stderr)
+        flags.insert(0, "-Xptxas=-v")
+    with tempfile.TemporaryDirectory(prefix="rskel_build_") as tmp:
+        objs = [os.path.join(tmp, os.path.basename(src) + ".o") for src in sources()]
+
+        def compile_one(pair):
+            src, obj = pair
+            return subprocess.run([nvcc, *flags, "-c", src, "-o", obj], capture_output=True, text=True)
+
+        with ThreadPoolExecutor(max_workers=max(1, min(len(objs), os.cpu_count() or 1))) as pool:
+            results = list(pool.map(compile_one, zip(sources(), objs)))
+        for res in results:
+            if res.returncode != 0:
+                sys.stderr.write(res.stdout + res.stderr)
+                raise RuntimeError("nvcc failed building librskel.so")
+            if verbose:
+                sys.stderr.write(res.stderr)
+        link = subprocess.run([nvcc, *ARCH_FLAGS, "-shared", "-o", LIB_PATH + ".tmp", *objs],
+                              capture_output=True, text=True)
+        if link.returncode != 0:
+            sys.stderr.write(link.stdout + link.stderr)
+            raise RuntimeError("nvcc failed linking librskel.so")
     os.replace(LIB_PATH + ".tmp", LIB_PATH)
     return LIB_PATH
 

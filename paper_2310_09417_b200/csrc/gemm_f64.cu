@@ -52,20 +52,12 @@ struct GemmCfg {
 
 // Production configuration and the alternatives the tuner compares
 // (RSKEL_GEMM_CFG=i selects one at run time, for tools/bench_kernels.py).
-using Cfg0 = GemmCfg<128, 64, 16, 4, 2, 3, 2>;   // warp 32x32
-using Cfg1 = GemmCfg<128, 64, 32, 4, 2, 2, 2>;   // BK 32, 2 stages
-using Cfg2 = GemmCfg<128, 64, 16, 4, 2, 4, 2>;   // 4 stages
-using Cfg3 = GemmCfg<256, 64, 16, 8, 2, 3, 1>;   // 16 warps, 1 CTA/SM
-using Cfg4 = GemmCfg<128, 64, 16, 2, 2, 4, 2>;   // 4 warps of 64x32
-using Cfg5 = GemmCfg<64, 64, 16, 2, 2, 4, 4>;    // 4 warps of 32x32, 4 CTAs/SM
-using Cfg6 = GemmCfg<128, 64, 16, 2, 2, 3, 2>;   // 4 warps of 64x32, 3 stages
-using Cfg7 = GemmCfg<256, 64, 16, 4, 2, 3, 1>;   // 8 warps of 64x32, 1 CTA/SM
-using Cfg8 = GemmCfg<128, 64, 32, 2, 2, 2, 2>;   // 4 warps of 64x32, BK 32
-using Cfg9 = GemmCfg<64, 32, 16, 2, 2, 4, 4>;    // 4 warps of 32x16, 4 stages, 4 CTAs/SM
-using Cfg10 = GemmCfg<64, 64, 32, 2, 2, 3, 2>;   // 4 warps of 32x32, BK 32
-using Cfg11 = GemmCfg<128, 32, 16, 4, 1, 4, 3>;  // 4 warps of 32x32 along M, 4 stages
+using Cfg0 = GemmCfg<128, 64, 16, 4, 2, 3, 2>;   // row-major A (Schur, W_hat, small products): 8 warps of 32x32
+using Cfg8 = GemmCfg<128, 64, 32, 2, 2, 2, 2>;   // column-major A (sketch): 4 warps of 64x32, BK 32
 using Cfg12 = GemmCfg<128, 64, 32, 4, 2, 2, 2>;  // 8 warps of 32x32, BK 32
-using Cfg13 = GemmCfg<256, 64, 32, 4, 2, 2, 1>;  // 8 warps of 64x32, BK 32, 1 CTA/SM
+// Measured alternatives (tools/tune_gemm.sh, B200, sketch 20000^2 x 64 / Schur k=7000):
+// 128x64x16 4 stages 28.x / 24; 64x64x16 4 CTA/SM 26 / 17; 64x32x16 (cuBLAS-like tile) 26.8 / 13.7;
+// 256x64 one CTA/SM 29.0 / 21.7; 8 warps BK 32 (Cfg12) 29.1 / 23.3; Cfg8 31.4 / 19.8; Cfg0 28.2 / 25.5.
 // Stream-K partial slots: 2 per CTA, THREADS * ACC doubles each; every config
 // has MINB * THREADS * ACC <= 16384 doubles per SM.
 constexpr int SK_SLOT_DOUBLES_PER_SM = 16384;
@@ -410,19 +402,8 @@ int launch_dgemm(const DGemmParams& p, bool a_col, cudaStream_t st) {
   if (p.M == 0 || p.N == 0) return RS_OK;
   bool vec2 = al16(p.A) && al16(p.B) && (p.lda % 2 == 0) && (p.ldb % 2 == 0);
   switch (selected_cfg()) {
-    case 1: return launch_cfg<Cfg1>(p, a_col, vec2, st);
-    case 2: return launch_cfg<Cfg2>(p, a_col, vec2, st);
-    case 3: return launch_cfg<Cfg3>(p, a_col, vec2, st);
-    case 4: return launch_cfg<Cfg4>(p, a_col, vec2, st);
-    case 5: return launch_cfg<Cfg5>(p, a_col, vec2, st);
-    case 6: return launch_cfg<Cfg6>(p, a_col, vec2, st);
-    case 7: return launch_cfg<Cfg7>(p, a_col, vec2, st);
     case 8: return launch_cfg<Cfg8>(p, a_col, vec2, st);
-    case 9: return launch_cfg<Cfg9>(p, a_col, vec2, st);
-    case 10: return launch_cfg<Cfg10>(p, a_col, vec2, st);
-    case 11: return launch_cfg<Cfg11>(p, a_col, vec2, st);
     case 12: return launch_cfg<Cfg12>(p, a_col, vec2, st);
-    case 13: return launch_cfg<Cfg13>(p, a_col, vec2, st);
     default:
       // Measured on B200 (tools/tune_gemm.sh): the column-major sketch operand
       // prefers 64x32 warp tiles (31.4 TF/s vs 28.2), the gathered row-major
