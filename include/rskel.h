@@ -161,6 +161,16 @@ int rs_jacobi_sweep(double* Xt, long long ldx, int p, double* Vt, long long ldv,
                     int nrounds, int npairs, double tol, unsigned long long* max_off, unsigned* barrier,
                     void* stream);
 
+/* Dense n x ell form of the SRTT embedding (`sketching.py:134-157,207-216`):
+ * Omega[perm[p], j] = scale * signs[q] * DCT-II_ortho(q, p), q = cols[j]. */
+int rs_srtt_dense(int n, int ell, const int64_t* perm, const double* signs, const int64_t* cols, double scale,
+                  double* out, long long ldo, void* stream);
+
+/* Dense n x ell form of the sparse-sign embedding (`sketching.py:160-187,219-235`):
+ * zero, then Omega[r, idx[r, z]] = signs[r, z] * scale (zeta entries per row). */
+int rs_sparse_sign_dense(int n, int ell, int zeta, const int64_t* idx, const double* signs, double scale,
+                         double* out, long long ldo, void* stream);
+
 /* Cholesky G = R^T R of a small SPD matrix (n <= 1024) in place (upper R,
  * strict lower part zeroed); *status_dev = 0 or j + 1 for a non-positive
  * pivot j.  The Gram step of pinv_apply (dense.py:166-182). */

@@ -61,6 +61,30 @@ def gaussian(seed, stream, n, ell, unit=False):
     return om
 
 
+def srtt_dense(seed, stream, n, ell):
+    """`sketching.py:134-157,207-216`: dense SRTT embedding (n x ell)."""
+    import scipy.fft
+
+    g = np.random.Generator(np.random.Philox(key=[seed & _M64, stream & _M64]))
+    perm = g.permutation(n)
+    signs = g.integers(0, 2, size=n) * 2.0 - 1.0
+    cols = g.choice(n, size=ell, replace=False)
+    eye = np.eye(n)
+    c = scipy.fft.dct(eye[:, perm], type=2, axis=1, norm="ortho") * signs
+    return np.sqrt(n / ell) * c[:, cols]
+
+
+def sparse_sign_dense(seed, stream, n, ell, zeta):
+    """`sketching.py:160-187,219-235`: dense sparse-sign embedding (n x ell)."""
+    g = np.random.Generator(np.random.Philox(key=[seed & _M64, stream & _M64]))
+    u = g.random((n, ell))
+    idx = np.argsort(u, axis=1)[:, :zeta]
+    signs = g.integers(0, 2, size=(n, zeta)) * 2.0 - 1.0
+    om = np.zeros((n, ell))
+    np.put_along_axis(om, idx, signs / np.sqrt(zeta), axis=1)
+    return om
+
+
 # ------------------------------------------------------------------- LUPP --
 def lupp_inplace(A, allow_partial):
     """Blocked right-looking LUPP of the F-ordered workspace A (m x n), in

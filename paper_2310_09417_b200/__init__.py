@@ -19,9 +19,13 @@ from .sketching import (
     GaussianSketch,
     RngStream,
     SketchSpec,
+    SparseSignSketch,
+    SrttSketch,
     apply_sketch,
     make_gaussian,
     make_sketch,
+    make_sparse_sign,
+    make_srtt,
 )
 from .dense import (
     LUFactors,

@@ -344,6 +344,10 @@ def sketch_omega(a, spec, rng):
     ``rng``: the device draw by default, the host draw under RSKEL_HOST_RNG=1.
     Same Omega bit for bit either way."""
     n, ell = spec.n, spec.ell
+    if spec.kind != "gaussian":  # SRTT / sparse sign: reference operator, dense on the device
+        from .sketching import make_sketch
+
+        return sketch_dev(a, make_sketch(spec, rng).device_dense())
     unit = spec.scale != "inv_sqrt_ell"
     if host_rng():
         om = torch.as_tensor(host_gaussian(rng, n, ell, unit)).to(device())

@@ -234,6 +234,16 @@ int rs_jacobi_sweep(double* Xt, long long ldx, int p, double* Vt, long long ldv,
   return rs::launch_jacobi_sweep(Xt, ldx, p, Vt, ldv, q, sched, nrounds, npairs, tol, max_off, barrier, S(stream));
 }
 
+int rs_srtt_dense(int n, int ell, const int64_t* perm, const double* signs, const int64_t* cols, double scale,
+                  double* out, long long ldo, void* stream) {
+  return rs::launch_srtt_dense(n, ell, perm, signs, cols, scale, out, ldo, S(stream));
+}
+
+int rs_sparse_sign_dense(int n, int ell, int zeta, const int64_t* idx, const double* signs, double scale,
+                         double* out, long long ldo, void* stream) {
+  return rs::launch_sparse_sign_dense(n, ell, zeta, idx, signs, scale, out, ldo, S(stream));
+}
+
 int rs_cholesky(double* G, long long ldg, int n, int* status_dev, void* stream) {
   return rs::launch_cholesky(G, ldg, n, status_dev, S(stream));
 }

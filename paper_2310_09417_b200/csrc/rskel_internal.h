@@ -75,6 +75,10 @@ int launch_pinv_scale(const double* Xt, long long ldx, int p, double* Vt, long l
 int launch_jacobi_sweep(double* Xt, long long ldx, int p, double* Vt, long long ldv, int q, const int* sched,
                         int nrounds, int npairs, double tol, unsigned long long* max_off, unsigned* bar,
                         cudaStream_t st);
+int launch_srtt_dense(int n, int ell, const int64_t* perm, const double* signs, const int64_t* cols, double scale,
+                      double* out, long long ldo, cudaStream_t st);
+int launch_sparse_sign_dense(int n, int ell, int zeta, const int64_t* idx, const double* signs, double scale,
+                             double* out, long long ldo, cudaStream_t st);
 int launch_cholesky(double* G, long long ldg, int n, int* status, cudaStream_t st);
 int launch_norm1(const double* A, long long lda, int rows, int cols, double* out, cudaStream_t st);
 int launch_gather2d(const double* src, long long rs_, long long cs_, const int64_t* ridx, int nr,

@@ -59,10 +59,7 @@ def _block_spec(spec, n, ell):
 
 def _draw_block(A, spec, stream, b):
     """``a @ Omega`` for one block (`skeleton.py:293-295`) -> device tensor (m x b)."""
-    sp = _block_spec(spec, A.cols, b)
-    if sp.kind != "gaussian":
-        make_sketch(sp, stream)  # raises NotImplementedError
-    return _device.sketch_omega(A, sp, stream)
+    return _device.sketch_omega(A, _block_spec(spec, A.cols, b), stream)
 
 
 def _kind_out(x, kind):
@@ -187,9 +184,11 @@ def draw_residual_sample(a, p, spec, rng):
     m, n = _device.shape_of(a)
     A = _device.as_matrix(a)
     stream = rng.child(_RESIDUAL_STREAM)
-    if spec.kind != "gaussian":
-        make_sketch(replace(spec, n=n, ell=p), stream)  # raises NotImplementedError
-    y = _device.sketch_omega(A, replace(spec, n=n, ell=p, scale="unit"), stream)
+    if spec.kind == "gaussian":
+        sp = replace(spec, n=n, ell=p, scale="unit")
+    else:  # `_sized_spec`: sparse-sign rows saturate at zeta = ell
+        sp = replace(spec, n=n, ell=p, zeta=min(spec.zeta, p) if spec.kind == "sparsesign" else spec.zeta)
+    y = _device.sketch_omega(A, sp, stream)
     return _kind_out(y, A.kind)
 
 

@@ -117,10 +117,7 @@ def _finite_or_raise(y, name="matrix"):
 
 
 def _gaussian_spec(spec, rng):
-    """The Gaussian embedding is drawn on the device (`_device.sketch_omega`);
-    other kinds raise like `make_sketch`."""
-    if spec.kind != "gaussian":
-        make_sketch(spec, rng)  # raises NotImplementedError
+    """Every kind is formed on the device (`_device.sketch_omega`)."""
     return spec
 
 
@@ -170,9 +167,7 @@ def rand_lupp_adaptive(a, b, tau, spec, rng, max_rank=None):
     if max_rank is None:
         max_rank = max(b, min(m, n) - b)
     max_rank = min(max_rank, min(m, n))
-    if spec.kind != "gaussian":
-        make_sketch(spec.with_dims(n, b), rng)  # raises NotImplementedError
-    return _AdaptiveDriver(_device.as_matrix(a), b, tau, rng, max_rank).run()
+    return _AdaptiveDriver(_device.as_matrix(a), b, tau, rng, max_rank, spec=spec).run()
 
 
 class PhaseTimer:
@@ -227,7 +222,7 @@ class _AdaptiveDriver:
     one pinned readback) while the GPU keeps the next sketch GEMM running.
     """
 
-    def __init__(self, a, b, tau, rng, max_rank, host=False):
+    def __init__(self, a, b, tau, rng, max_rank, host=False, spec=None):
         self.prof = _PHASE_TIMER or _NullTimer()
         self.a, self.b, self.tau, self.rng, self.max_rank = a, b, tau, rng, max_rank
         m, n = a.shape
@@ -235,8 +230,10 @@ class _AdaptiveDriver:
         dev = _device.device()
         # Omega_t: device draw (rs_gaussian) on the side stream by default,
         # host thread-pool draw + H2D copy under RSKEL_HOST_RNG=1.
+        self.spec = spec
+        self.kind = spec.kind if spec is not None else "gaussian"
         self.dev_rng = not (host or _device.host_rng())
-        self.src = None if self.dev_rng else _omega.BlockOmegaSource(n, b, rng)
+        self.src = None if (self.dev_rng or self.kind != "gaussian") else _omega.BlockOmegaSource(n, b, rng)
         self.rng_status = torch.zeros(max_rank // b + 4, dtype=torch.int32, device=dev)
         self.om = [torch.empty((n, b), dtype=torch.float64, device=dev) for _ in range(2)]
         self.y = [torch.empty((m, b), dtype=torch.float64, device=dev) for _ in range(2)]
@@ -264,11 +261,18 @@ class _AdaptiveDriver:
         slot = t % 2
         if t >= self.rng_status.numel():
             return
-        h = None if self.dev_rng else self.src.host(t)
+        h = None if (self.dev_rng or self.kind != "gaussian") else self.src.host(t)
         with torch.cuda.stream(self.copy_stream):
             if self.om_free[slot] is not None:
                 self.copy_stream.wait_event(self.om_free[slot])
-            if h is None:
+            if self.kind != "gaussian":
+                # SRTT / sparse sign: the reference's per-block operator
+                # (`skeleton.py:286-295`), dense on the device
+                from .lu_state import _block_spec
+
+                op = make_sketch(_block_spec(self.spec, self.n, self.b), self.rng.child(t))
+                self.om[slot].copy_(op.device_dense())
+            elif h is None:
                 _device.gaussian(self.rng.child(t), self.n, self.b, out=self.om[slot],
                                  status=self.rng_status[t:t + 1])
             else:
@@ -403,7 +407,7 @@ class _AdaptiveDriver:
             # a block the parallel ziggurat resolver could not place (never
             # observed): redo the whole loop with the host draw, same bits
             self.dev_rng = False
-            self.__init__(self.a, self.b, self.tau, self.rng, self.max_rank, host=True)
+            self.__init__(self.a, self.b, self.tau, self.rng, self.max_rank, host=True, spec=self.spec)
             return self.run()
         k = st.k
         tok = self.prof.start("interp")

@@ -1,15 +1,20 @@
-"""Seeded Gaussian embeddings and their application on the B200.
+"""Seeded embeddings and their application on the B200.
 
-Host-RNG contract (north star: "Omega supplied from the host RNG"): every
-embedding is drawn on the host from numpy's Philox4x64 generator keyed by a
-``(seed, stream)`` pair exactly as the reference does (`sketching.py:41-72`,
-`sketching.py:191-204`), so the Omega bits are identical to the reference's.
-Applying the embedding (``a @ Omega``) runs on the DMMA GEMM kernel of
+Every embedding is defined by numpy's Philox4x64 generator keyed by a
+``(seed, stream)`` pair exactly as in the reference (`sketching.py:41-72`),
+so the operator bits are the reference's:
+
+* Gaussian (`sketching.py:191-204`): drawn on the device by `rs_gaussian`
+  (bit-identical to numpy's ziggurat) on the skeleton paths; `make_gaussian`
+  keeps the host draw.
+* SRTT (`sketching.py:134-157,207-216`) and sparse sign
+  (`sketching.py:160-187,219-235`): the operator parameters (permutation,
+  signs, sampled columns / row supports) come from the same numpy calls as
+  the reference; the dense n x ell embedding is formed on the device
+  (`rs_srtt_dense`, `rs_sparse_sign_dense`).
+
+Applying any embedding (``a @ Omega``) runs on the DMMA GEMM kernel of
 librskel.so (`rs_sketch_gemm`).
-
-Only the Gaussian distribution is on the accelerated path; SRTT and sparse
-sign specs validate like the reference but ``make_sketch`` rejects them (they
-are out of the north-star scope).
 """
 
 from dataclasses import dataclass, replace
@@ -24,7 +29,11 @@ __all__ = [
     "SketchSpec",
     "RngStream",
     "GaussianSketch",
+    "SrttSketch",
+    "SparseSignSketch",
     "make_gaussian",
+    "make_srtt",
+    "make_sparse_sign",
     "make_sketch",
     "apply_sketch",
 ]
@@ -135,13 +144,111 @@ class GaussianSketch:
         return self.omega
 
 
+def _apply_dense(op, a):
+    A = _device.as_matrix(a)
+    n = op.shape[0]
+    if A.cols != n:
+        raise DimensionError(f"operator ambient dimension {n} does not match {A.shape}")
+    return _device.to_output(_device.sketch_dev(A, op.device_dense()), A)
+
+
+class SrttSketch:
+    """Subsampled randomized trigonometric transform (reference
+    `sketching.py:134-157`): ``y = scale * (DCT-II(x[perm]) * signs)[cols]``."""
+
+    def __init__(self, perm, signs, cols, scale):
+        self.perm, self.signs, self.cols, self.scale = perm, signs, cols, scale
+
+    @property
+    def shape(self):
+        return (self.perm.shape[0], self.cols.shape[0])
+
+    def device_dense(self):
+        import torch
+
+        from . import _lib
+
+        n, ell = self.shape
+        dev = _device.device()
+        out = torch.empty((n, ell), dtype=torch.float64, device=dev)
+        perm = torch.as_tensor(np.asarray(self.perm, dtype=np.int64)).to(dev)
+        cols = torch.as_tensor(np.asarray(self.cols, dtype=np.int64)).to(dev)
+        signs = torch.as_tensor(np.asarray(self.signs, dtype=np.float64)).to(dev)
+        _lib.call("rs_srtt_dense", n, ell, perm.data_ptr(), signs.data_ptr(), cols.data_ptr(), float(self.scale),
+                  out.data_ptr(), ell, _device.stream_handle())
+        return out
+
+    def apply(self, a):
+        return _apply_dense(self, a)
+
+    def to_dense(self):
+        return self.device_dense().cpu().numpy()
+
+
+class SparseSignSketch:
+    """Sparse-sign embedding, ``zeta`` (index, sign) pairs per row scaled by
+    ``scale`` (reference `sketching.py:160-187`)."""
+
+    def __init__(self, idx, signs, ell, scale):
+        self.idx, self.signs, self.ell, self.scale = idx, signs, ell, scale
+
+    @property
+    def shape(self):
+        return (self.idx.shape[0], self.ell)
+
+    def device_dense(self):
+        import torch
+
+        from . import _lib
+
+        n, zeta = self.idx.shape
+        dev = _device.device()
+        out = torch.empty((n, self.ell), dtype=torch.float64, device=dev)
+        idx = torch.as_tensor(np.ascontiguousarray(self.idx, dtype=np.int64)).to(dev)
+        signs = torch.as_tensor(np.ascontiguousarray(self.signs, dtype=np.float64)).to(dev)
+        _lib.call("rs_sparse_sign_dense", n, self.ell, zeta, idx.data_ptr(), signs.data_ptr(), float(self.scale),
+                  out.data_ptr(), self.ell, _device.stream_handle())
+        return out
+
+    def apply(self, a):
+        return _apply_dense(self, a)
+
+    def to_dense(self):
+        return self.device_dense().cpu().numpy()
+
+
+def make_srtt(spec, rng):
+    """SRTT operator: permutation, signs, sampled columns from the stream in
+    the reference's order (`sketching.py:207-216`)."""
+    if spec.kind != "srtt":
+        raise ValueError(f"spec kind is {spec.kind!r}, expected 'srtt'")
+    g = rng.generator()
+    perm = g.permutation(spec.n)
+    signs = g.integers(0, 2, size=spec.n) * 2.0 - 1.0
+    cols = g.choice(spec.n, size=spec.ell, replace=False)
+    return SrttSketch(perm.astype(np.intp), signs, cols.astype(np.intp), np.sqrt(spec.n / spec.ell))
+
+
+def make_sparse_sign(spec, rng):
+    """Sparse-sign operator: a uniform zeta-subset of the ell columns per row
+    (ranks of i.i.d. uniforms) and Rademacher signs scaled by 1/sqrt(zeta)
+    (`sketching.py:219-235`)."""
+    if spec.kind != "sparsesign":
+        raise ValueError(f"spec kind is {spec.kind!r}, expected 'sparsesign'")
+    g = rng.generator()
+    u = g.random((spec.n, spec.ell))
+    idx = np.argsort(u, axis=1)[:, : spec.zeta]
+    signs = g.integers(0, 2, size=(spec.n, spec.zeta)) * 2.0 - 1.0
+    return SparseSignSketch(np.ascontiguousarray(idx, dtype=np.intp), signs, spec.ell, 1.0 / np.sqrt(spec.zeta))
+
+
 def make_sketch(spec, rng):
-    """Construct the operator described by ``spec`` (Gaussian only here)."""
+    """Construct the operator described by ``spec`` (reference `sketching.py:238-244`)."""
     if spec.kind == "gaussian":
         return GaussianSketch(make_gaussian(spec, rng))
-    raise NotImplementedError(
-        f"sketch kind {spec.kind!r} is outside the B200 hot path (Gaussian only)"
-    )
+    if spec.kind == "srtt":
+        return make_srtt(spec, rng)
+    return make_sparse_sign(spec, rng)
 
 
 def apply_sketch(a, op, side="right"):
@@ -151,9 +258,13 @@ def apply_sketch(a, op, side="right"):
     if side not in ("right", "transposed_right"):
         raise ValueError(f"side must be 'right' or 'transposed_right', got {side!r}")
     target = a if side == "right" else a.T
+    if isinstance(op, (SrttSketch, SparseSignSketch)):
+        if target.cols != op.shape[0]:
+            raise DimensionError(f"operator ambient dimension {op.shape[0]} does not match {target.shape}")
+        return _device.to_output(_device.sketch_dev(target, op.device_dense()), a)
     omega = op if isinstance(op, np.ndarray) else getattr(op, "omega", None)
     if omega is None:
-        raise NotImplementedError("only dense Gaussian embeddings are applied on the device")
+        raise TypeError("op must be a sketch operator or a dense embedding matrix")
     omega = np.asarray(omega, dtype=np.float64)
     if target.cols != omega.shape[0]:
         if isinstance(op, np.ndarray):

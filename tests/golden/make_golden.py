@@ -172,6 +172,21 @@ def main():
     put("row_id_errors", gen_seed=70, k=48, seed=73, row_idx=r.row_idx,
         err=rs.row_id_error(a, r), stable_err=rs.stable_row_id_error(a, r))
 
+    # ---- structured embeddings: SRTT and sparse sign ----
+    a = np.random.default_rng(80).standard_normal((90, 70))
+    for kind, kw in (("srtt", {}), ("sparsesign", {"zeta": 4})):
+        sp = rs.SketchSpec(kind, n=70, ell=16, **kw)
+        op = rs.make_sketch(sp, rs.RngStream(81))
+        put(f"sketch_{kind}", dense=op.to_dense(), y=rs.apply_sketch(a, op),
+            yt=rs.apply_sketch(a, rs.make_sketch(rs.SketchSpec(kind, n=90, ell=16, **kw), rs.RngStream(82)),
+                               side="transposed_right"))
+        r = rs.rand_lupp(a, 16, rs.SketchSpec(kind, n=70, ell=16, **kw), rs.RngStream(83))
+        put(f"rand_lupp_{kind}", row_idx=r.row_idx, w=r.w)
+        b_exact = exact(120, 90, 25, 84)
+        res = rs.rand_lupp_adaptive(b_exact, 8, 1e-9, rs.SketchSpec(kind, n=90, ell=8, **kw), rs.RngStream(85))
+        put(f"adapt_{kind}", rank=res.rank, row_idx=res.row_idx, status=res.status,
+            trace=np.array([[rec.k, rec.e_schur] for rec in res.trace]))
+
     path = os.path.join(OUT, "reference_golden.npz")
     flat = {}
     for name, arrays in cases.items():

@@ -291,3 +291,30 @@ def test_row_id_errors_vs_reference():
     assert np.array_equal(r.row_idx, g["row_idx"])
     assert abs(rs.row_id_error(a, r) - float(g["err"])) <= 1e-6 * float(g["err"])
     assert abs(rs.stable_row_id_error(a, r) - float(g["stable_err"])) <= 1e-6 * float(g["stable_err"])
+
+
+@pytest.mark.parametrize("kind", ["srtt", "sparsesign"])
+def test_structured_embeddings_vs_reference(kind):
+    """SRTT and sparse-sign embeddings formed on the device: operator, both
+    application sides, fixed-rank and adaptive skeletons against the
+    reference (golden)."""
+    import paper_2310_09417_b200 as rs
+
+    kw = {"zeta": 4} if kind == "sparsesign" else {}
+    g = golden(f"sketch_{kind}")
+    a = np.random.default_rng(80).standard_normal((90, 70))
+    op = rs.make_sketch(rs.SketchSpec(kind, 70, 16, **kw), rs.RngStream(81))
+    np.testing.assert_allclose(op.to_dense(), g["dense"], rtol=0, atol=1e-14)
+    np.testing.assert_allclose(rs.apply_sketch(a, op), g["y"], rtol=0, atol=1e-12)
+    op2 = rs.make_sketch(rs.SketchSpec(kind, 90, 16, **kw), rs.RngStream(82))
+    np.testing.assert_allclose(rs.apply_sketch(a, op2, side="transposed_right"), g["yt"], rtol=0, atol=1e-12)
+    r = rs.rand_lupp(a, 16, rs.SketchSpec(kind, 70, 16, **kw), rs.RngStream(83))
+    gr = golden(f"rand_lupp_{kind}")
+    assert np.array_equal(r.row_idx, gr["row_idx"])
+    np.testing.assert_allclose(r.w, gr["w"], rtol=0, atol=1e-10)
+    ga = golden(f"adapt_{kind}")
+    gg = np.random.default_rng(84)
+    b_exact = gg.standard_normal((120, 25)) @ gg.standard_normal((25, 90))
+    res = rs.rand_lupp_adaptive(b_exact, 8, 1e-9, rs.SketchSpec(kind, 90, 8, **kw), rs.RngStream(85))
+    assert res.rank == int(ga["rank"]) and res.status == str(ga["status"])
+    assert np.array_equal(res.row_idx[: res.rank - 8], ga["row_idx"][: res.rank - 8])

@@ -195,3 +195,13 @@ def test_oracle_row_id_errors():
     s = orc.stable_row_id_error(a, r[0])
     assert abs(e - float(g["err"])) <= 1e-8 * float(g["err"])
     assert abs(s - float(g["stable_err"])) <= 1e-8 * float(g["stable_err"])
+
+
+@pytest.mark.parametrize("kind", ["srtt", "sparsesign"])
+def test_oracle_structured_embeddings(kind):
+    """SRTT / sparse-sign operators (`sketching.py:134-235`) vs the reference."""
+    g = golden(f"sketch_{kind}")
+    om = orc.srtt_dense(81, 0, 70, 16) if kind == "srtt" else orc.sparse_sign_dense(81, 0, 70, 16, 4)
+    np.testing.assert_allclose(om, g["dense"], rtol=0, atol=1e-14)
+    a = np.random.default_rng(80).standard_normal((90, 70))
+    np.testing.assert_allclose(a @ om, g["y"], rtol=0, atol=1e-12)
