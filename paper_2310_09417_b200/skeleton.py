@@ -116,16 +116,11 @@ def _finite_or_raise(y, name="matrix"):
         raise ValueError(f"{name} contains non-finite entries")
 
 
-def _gaussian_spec(spec, rng):
-    """Every kind is formed on the device (`_device.sketch_omega`)."""
-    return spec
-
-
 def rand_lupp(a, k, spec, rng):
     """Row skeletons by LUPP of ``a @ Omega`` (fixed rank k)."""
     m, n = _device.shape_of(a)
     _check_rank(k, m, n)
-    sp = _gaussian_spec(spec.with_dims(n, k), rng)
+    sp = spec.with_dims(n, k)
     a = _device.as_matrix(a)
     y = _device.Matrix(_device.sketch_omega(a, sp, rng), m, k, k, False, a.kind)
     _finite_or_raise(y)
@@ -139,7 +134,7 @@ def column_id(a, k, spec, rng):
     """Column skeletons by LUPP of ``a.T @ Gamma``; ``x[:, col_idx] = I``."""
     m, n = _device.shape_of(a)
     _check_rank(k, m, n)
-    sp = _gaussian_spec(spec.with_dims(m, k), rng)
+    sp = spec.with_dims(m, k)
     a = _device.as_matrix(a)
     y = _device.Matrix(_device.sketch_omega(a.T, sp, rng), n, k, k, False, a.kind)
     _finite_or_raise(y)
