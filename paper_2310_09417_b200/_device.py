@@ -215,6 +215,52 @@ def h2d(arr):
     return out
 
 
+def h2d_rows(arr, on_chunk, out=None, chunk_bytes=128 << 20):
+    """Row-chunked device copy of a C-contiguous 2-D host array: after each
+    chunk's copy is enqueued, ``on_chunk(r0, r1, event)`` is called so work
+    on the rows that have landed can be enqueued behind ``event`` while the
+    rest is in flight.  Returns the device tensor; the current stream waits
+    for the whole copy at the end."""
+    dev = device()
+    rows, cols = arr.shape
+    host = torch.from_numpy(arr)
+    if out is None:
+        out = torch.empty(arr.shape, dtype=host.dtype, device=dev)
+    pinned = host.is_pinned()
+    row_bytes = max(1, arr.strides[0])
+    ring = _stage_ring(dev)
+    cs = ring["stream"]
+    cs.wait_stream(torch.cuda.current_stream(dev))
+    step = max(1, (chunk_bytes if pinned else _STAGE_BYTES) // row_bytes)
+    pool = _copy_pool()
+    nthr = max(1, min(16, pool._max_workers))
+    for i, r0 in enumerate(range(0, rows, step)):
+        r1 = min(rows, r0 + step)
+        if pinned:
+            with torch.cuda.stream(cs):
+                out[r0:r1].copy_(host[r0:r1], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(cs)
+        else:
+            slot = i % _STAGE_DEPTH
+            prev = ring["events"][slot]
+            if prev is not None:
+                prev.synchronize()
+            nb = (r1 - r0) * row_bytes
+            buf = ring["bufs"][slot].numpy()[:nb]
+            src = arr[r0:r1].reshape(-1).view(np.uint8)
+            part = -(-nb // nthr)
+            list(pool.map(lambda q: np.copyto(buf[q:q + part], src[q:q + part]), range(0, nb, part)))
+            with torch.cuda.stream(cs):
+                out[r0:r1].view(-1).view(torch.uint8).copy_(ring["bufs"][slot][:nb], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(cs)
+            ring["events"][slot] = ev
+        on_chunk(r0, r1, ev)
+    torch.cuda.current_stream(dev).wait_stream(cs)
+    return out
+
+
 def as_index(idx, kind):
     """Index vector -> int64 device tensor."""
     if isinstance(idx, torch.Tensor):

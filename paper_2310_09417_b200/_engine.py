@@ -112,7 +112,7 @@ class TFormState:
         self._cur = nxt
         self.k += nc
 
-    def absorb_schur(self, w, nc, y_next_ptr, e2_out):
+    def absorb_schur(self, w, nc, y_next_ptr, e2_out, ldy=64):
         """absorb(w, nc) fused with the Schur block of the next sketch block
         (m x 64 at y_next_ptr) into S, e2_out = ||S||^2 (rs_absorb_schur)."""
         nxt = 1 - self._cur
@@ -120,7 +120,7 @@ class TFormState:
         _lib.call(
             "rs_absorb_schur", self.m, self.k, nc, self.S.data_ptr(), w, self.sub.data_ptr(),
             self.T.data_ptr(), max(self.k, 1), self._T[nxt].data_ptr(), self.perm.data_ptr(),
-            self._perm[nxt].data_ptr(), y_next_ptr, 64, s_next.data_ptr(),
+            self._perm[nxt].data_ptr(), y_next_ptr, ldy, s_next.data_ptr(),
             e2_out.data_ptr() if e2_out is not None else None, self.ws.data_ptr(), self.stream,
         )
         self._prev = (self._cur, self.k, self._scur)

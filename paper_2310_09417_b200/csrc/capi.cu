@@ -160,8 +160,9 @@ int rs_absorb_schur(int m, int k, int nc, const double* S_, long long lds, const
   if (!fused) {
     int rc = rs_absorb_block(m, k, nc, S_, lds, sub_perm, T, ldt, T_new, perm, perm_new, workspace, stream);
     if (rc != RS_OK) return rc;
-    return rs_schur_block(m, k + nc, nc > 0 ? (int)ldy : 0, Y_next, ldy, perm_new, T_new, ldn, S_next,
-                          nc > 0 ? ldy : 1, e2_dev, workspace, stream);
+    // the next block is 64 columns wide at row stride ldy; S_next is m x 64
+    return rs_schur_block(m, k + nc, nc > 0 ? kMaxB : 0, Y_next, ldy, perm_new, T_new, ldn, S_next,
+                          kMaxB, e2_dev, workspace, stream);
   }
   double* linv = reinterpret_cast<double*>(W(workspace, layout().linv_off));
   double* zp = reinterpret_cast<double*>(W(workspace, layout().zp_off));

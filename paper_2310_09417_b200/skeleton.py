@@ -16,7 +16,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from . import _device, _engine, _omega
+from . import _device, _engine, _omega, dense
 from .errors import DimensionError, RankDeficientError
 from .sketching import make_sketch
 
@@ -162,7 +162,68 @@ def rand_lupp_adaptive(a, b, tau, spec, rng, max_rank=None):
     if max_rank is None:
         max_rank = max(b, min(m, n) - b)
     max_rank = min(max_rank, min(m, n))
+    pre = _presketch(a, b, rng, max_rank, spec)
+    if pre is not None:
+        A, yb, nb = pre
+        return _AdaptiveDriver(A, b, tau, rng, max_rank, spec=spec, presketch=(yb, nb)).run()
     return _AdaptiveDriver(_device.as_matrix(a), b, tau, rng, max_rank, spec=spec).run()
+
+
+_PRESKETCH_MIN_BYTES = 64 << 20
+_PRESKETCH_MAX_BLOCKS = 32
+
+
+def _presketch(a, b, rng, max_rank, spec):
+    """Host input: overlap the H2D of A with the sketches of the first blocks.
+
+    One wide product A-side x [Omega_0 | ... | Omega_{NB-1}] is accumulated
+    over row chunks of the host array as they land on the device, so the
+    copy engine and the DMMA pipe work at the same time; the loop then starts
+    with NB sketch blocks already computed.  Returns None when not
+    applicable (device input, small input, non-Gaussian or host draws)."""
+    import os
+
+    if isinstance(a, (torch.Tensor, _device.Matrix)) or os.environ.get("RSKEL_PRESKETCH", "1") == "0":
+        return None
+    if spec.kind != "gaussian" or _device.host_rng() or b > _engine.MAX_BLOCK:
+        return None
+    arr = np.asarray(a)
+    if arr.dtype != np.float64 or arr.ndim != 2 or arr.nbytes < _PRESKETCH_MIN_BYTES:
+        return None
+    if not (arr.flags.c_contiguous or arr.flags.f_contiguous):
+        return None
+    m, n = arr.shape
+    nb = min(_PRESKETCH_MAX_BLOCKS, max_rank // b + 1)
+    if nb < 2:
+        return None
+    dev = _device.device()
+    width = b * nb
+    om = torch.empty((n, width), dtype=torch.float64, device=dev)
+    for t in range(nb):
+        om[:, b * t: b * (t + 1)].copy_(_device.gaussian(rng.child(t), n, b))
+    yb = torch.empty((m, width), dtype=torch.float64, device=dev)
+    Y = dense._mat(yb)
+    OM = dense._mat(om)
+    colmajor = not arr.flags.c_contiguous
+    under = arr.T if colmajor else arr            # C-ordered rows: K (colmajor) or M (row-major)
+    compute = torch.cuda.current_stream(dev)
+    holder = {}
+
+    def on_chunk(r0, r1, ev):
+        compute.wait_event(ev)
+        U = holder["U"]
+        if colmajor:   # a = U.T: rows r0..r1 of U are columns (K) of a
+            A_part = _device.Matrix(U, m, r1 - r0, m, True, "numpy", off=r0 * m)
+            dense._gemm(Y, A_part, OM.sub(r0, 0, r1 - r0, width), alpha=1.0,
+                        beta=0.0 if r0 == 0 else 1.0, Cin=Y if r0 > 0 else None)
+        else:          # rows r0..r1 of a are candidates r0..r1
+            A_part = _device.Matrix(U, r1 - r0, n, n, False, "numpy", off=r0 * n)
+            dense._gemm(Y.sub(r0, 0, r1 - r0, width), A_part, OM)
+
+    holder["U"] = torch.empty(under.shape, dtype=torch.float64, device=dev)
+    U_dev = _device.h2d_rows(under, on_chunk, out=holder["U"])
+    A = _device.Matrix(U_dev, m, n, m if colmajor else n, colmajor, "numpy")
+    return A, yb, nb
 
 
 class PhaseTimer:
@@ -217,7 +278,7 @@ class _AdaptiveDriver:
     one pinned readback) while the GPU keeps the next sketch GEMM running.
     """
 
-    def __init__(self, a, b, tau, rng, max_rank, host=False, spec=None):
+    def __init__(self, a, b, tau, rng, max_rank, host=False, spec=None, presketch=None):
         self.prof = _PHASE_TIMER or _NullTimer()
         self.a, self.b, self.tau, self.rng, self.max_rank = a, b, tau, rng, max_rank
         m, n = a.shape
@@ -227,6 +288,8 @@ class _AdaptiveDriver:
         # host thread-pool draw + H2D copy under RSKEL_HOST_RNG=1.
         self.spec = spec
         self.kind = spec.kind if spec is not None else "gaussian"
+        # blocks t < nb_pre were sketched during the H2D (`_presketch`)
+        self.yb, self.nb_pre = presketch if presketch is not None else (None, 0)
         self.dev_rng = not (host or _device.host_rng())
         self.src = None if (self.dev_rng or self.kind != "gaussian") else _omega.BlockOmegaSource(n, b, rng)
         self.rng_status = torch.zeros(max_rank // b + 4, dtype=torch.int32, device=dev)
@@ -274,8 +337,16 @@ class _AdaptiveDriver:
                 self.om[slot].copy_(h, non_blocking=True)
             self.om_ready[slot].record(self.copy_stream)
 
+    def _y(self, t):
+        """(pointer, leading dimension) of block t's sketch."""
+        if t < self.nb_pre:
+            return self.yb.data_ptr() + 8 * self.b * t, self.b * self.nb_pre
+        return self.y[t % 2].data_ptr(), self.b
+
     def _sketch(self, t):
         from . import _lib
+        if t < self.nb_pre:
+            return
         slot = t % 2
         self._issue_copy(t)
         self.compute.wait_event(self.om_ready[slot])
@@ -292,13 +363,15 @@ class _AdaptiveDriver:
     # -- blocks ------------------------------------------------------------------
     def _absorb_block(self, y, first):
         """Eliminate the current block synchronously (first block, and b > 64);
-        returns eliminated columns (< b iff a zero pivot column, `_lupp_partial`)."""
+        returns eliminated columns (< b iff a zero pivot column, `_lupp_partial`).
+        ``y`` = (pointer, leading dimension) of the block's sketch."""
         st, b = self.st, self.b
+        yp, ld = y
         done = 0
         for j0 in range(0, b, _engine.MAX_BLOCK):
             w = min(_engine.MAX_BLOCK, b - j0)
             if j0 > 0 or first or b > _engine.MAX_BLOCK:
-                st.schur(y.data_ptr() + 8 * j0, b, w, None)
+                st.schur(yp + 8 * j0, ld, w, None)
             st.panel(w, self.nc)
             nc = int(self.nc[0].item())
             st.absorb(w, nc)
@@ -321,10 +394,13 @@ class _AdaptiveDriver:
         try:
             # adaptive_init (`skeleton.py:298-314`): lupp of the first block.
             self._sketch(0)
-            y0 = self.y[0]
-            st.schur(y0.data_ptr(), b, min(b, _engine.MAX_BLOCK), self.e2)
+            y0 = self._y(0)
+            st.schur(y0[0], y0[1], min(b, _engine.MAX_BLOCK), self.e2)
             if wide or not math.isfinite(float(self.e2.item())):
-                _finite_or_raise(_device.Matrix(y0, self.m, b, b, False, self.a.kind))
+                if self.nb_pre:
+                    _finite_or_raise(_device.Matrix(self.yb, self.m, b, b * self.nb_pre, False, self.a.kind))
+                else:
+                    _finite_or_raise(_device.Matrix(self.y[0], self.m, b, b, False, self.a.kind))
             done = self._absorb_block(y0, first=True)
             if done < b:
                 raise RankDeficientError(done)
@@ -338,16 +414,16 @@ class _AdaptiveDriver:
             fused = b == _engine.MAX_BLOCK
             have_schur = False
             while True:
-                y = self.y[t % 2]
+                y = self._y(t)
                 if not wide and not have_schur:
                     tok = self.prof.start("schur")
-                    st.schur(y.data_ptr(), b, b, self.e2)
+                    st.schur(y[0], y[1], b, self.e2)
                     self.prof.stop(tok)
                 if wide:
                     e2 = 0.0
                     for j0 in range(0, b, _engine.MAX_BLOCK):
                         w = min(_engine.MAX_BLOCK, b - j0)
-                        st.schur(y.data_ptr() + 8 * j0, b, w, self.e2)
+                        st.schur(y[0] + 8 * j0, y[1], w, self.e2)
                         e2 += float(self.e2.item())
                     ev = None
                 else:
@@ -380,7 +456,8 @@ class _AdaptiveDriver:
                     self.prof.stop(tok)
                     tok = self.prof.start("absorb")
                     if fused:
-                        st.absorb_schur(b, b, self.y[(t + 1) % 2].data_ptr(), self.e2)
+                        yn = self._y(t + 1)
+                        st.absorb_schur(b, b, yn[0], self.e2, ldy=yn[1])
                         have_schur = True
                     else:
                         st.absorb(b, b)
@@ -403,6 +480,7 @@ class _AdaptiveDriver:
             # observed): redo the whole loop with the host draw, same bits
             self.dev_rng = False
             self.__init__(self.a, self.b, self.tau, self.rng, self.max_rank, host=True, spec=self.spec)
+            # (the presketched blocks are dropped: every block is redrawn on the host)
             return self.run()
         k = st.k
         tok = self.prof.start("interp")
