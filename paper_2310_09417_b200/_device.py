@@ -385,6 +385,20 @@ def host_gaussian(stream, n, ell, unit=False):
     return h
 
 
+def omega_dense(spec, rng):
+    """The (n x ell) embedding of ``spec`` from ``rng`` as a device tensor (any
+    kind; Gaussian drawn on the device unless RSKEL_HOST_RNG=1)."""
+    n, ell = spec.n, spec.ell
+    if spec.kind != "gaussian":
+        from .sketching import make_sketch
+
+        return make_sketch(spec, rng).device_dense()
+    unit = spec.scale != "inv_sqrt_ell"
+    if host_rng():
+        return torch.as_tensor(host_gaussian(rng, n, ell, unit)).to(device())
+    return gaussian(rng, n, ell, unit=unit)
+
+
 def sketch_omega(a, spec, rng):
     """Y = a @ Omega for the Gaussian embedding ``spec`` (n x ell) drawn from
     ``rng``: the device draw by default, the host draw under RSKEL_HOST_RNG=1.

@@ -121,8 +121,13 @@ def rand_lupp(a, k, spec, rng):
     m, n = _device.shape_of(a)
     _check_rank(k, m, n)
     sp = spec.with_dims(n, k)
-    a = _device.as_matrix(a)
-    y = _device.Matrix(_device.sketch_omega(a, sp, rng), m, k, k, False, a.kind)
+    arr = _streamable(a)
+    if arr is not None:  # H2D overlapped with the sketch, chunk by chunk
+        a, yt = _streamed_sketch(arr, _device.omega_dense(sp, rng))
+    else:
+        a = _device.as_matrix(a)
+        yt = _device.sketch_omega(a, sp, rng)
+    y = _device.Matrix(yt, m, k, k, False, a.kind)
     _finite_or_raise(y)
     st, w = _factor_sketch(y, a.kind)
     idx = st.perm[:k].clone()
@@ -135,8 +140,13 @@ def column_id(a, k, spec, rng):
     m, n = _device.shape_of(a)
     _check_rank(k, m, n)
     sp = spec.with_dims(m, k)
-    a = _device.as_matrix(a)
-    y = _device.Matrix(_device.sketch_omega(a.T, sp, rng), n, k, k, False, a.kind)
+    arr = _streamable(a)
+    if arr is not None:  # H2D overlapped with the sketch, chunk by chunk
+        a, yt = _streamed_sketch(arr, _device.omega_dense(sp, rng), transpose=True)
+    else:
+        a = _device.as_matrix(a)
+        yt = _device.sketch_omega(a.T, sp, rng)
+    y = _device.Matrix(yt, n, k, k, False, a.kind)
     _finite_or_raise(y)
     st, w = _factor_sketch(y, a.kind)
     idx = st.perm[:k].clone()
@@ -173,6 +183,52 @@ _PRESKETCH_MIN_BYTES = 64 << 20
 _PRESKETCH_MAX_BLOCKS = 32
 
 
+def _streamable(a):
+    """The host array behind ``a`` if its H2D can be overlapped with the
+    sketch (fp64, C- or F-contiguous, >= 64 MB), else None."""
+    import os
+
+    if isinstance(a, (torch.Tensor, _device.Matrix)) or os.environ.get("RSKEL_PRESKETCH", "1") == "0":
+        return None
+    arr = np.asarray(a)
+    if arr.dtype != np.float64 or arr.ndim != 2 or arr.nbytes < _PRESKETCH_MIN_BYTES:
+        return None
+    if not (arr.flags.c_contiguous or arr.flags.f_contiguous):
+        return None
+    return arr
+
+
+def _streamed_sketch(arr, om, transpose=False):
+    """Copy ``arr`` to the device in row chunks and accumulate
+    ``target @ om`` (target = arr, or arr.T with ``transpose``) chunk by
+    chunk as the rows land.  Returns (device Matrix of arr, Y tensor)."""
+    dev = _device.device()
+    m, n = arr.shape
+    tm, tn = (n, m) if transpose else (m, n)   # target shape
+    width = om.shape[1]
+    Y = dense._mat(torch.empty((tm, width), dtype=torch.float64, device=dev))
+    OM = dense._mat(om)
+    a_colmajor = not arr.flags.c_contiguous
+    under = arr.T if a_colmajor else arr       # C-ordered host rows
+    t_colmajor = a_colmajor != transpose       # target's layout over `under`
+    compute = torch.cuda.current_stream(dev)
+    U = torch.empty(under.shape, dtype=torch.float64, device=dev)
+
+    def on_chunk(r0, r1, ev):
+        compute.wait_event(ev)
+        if t_colmajor:   # rows r0..r1 of `under` are columns (K) of the target
+            A_part = _device.Matrix(U, tm, r1 - r0, tm, True, "numpy", off=r0 * tm)
+            dense._gemm(Y, A_part, OM.sub(r0, 0, r1 - r0, width), alpha=1.0,
+                        beta=0.0 if r0 == 0 else 1.0, Cin=Y if r0 > 0 else None)
+        else:            # rows r0..r1 of `under` are rows of the target
+            A_part = _device.Matrix(U, r1 - r0, tn, tn, False, "numpy", off=r0 * tn)
+            dense._gemm(Y.sub(r0, 0, r1 - r0, width), A_part, OM)
+
+    _device.h2d_rows(under, on_chunk, out=U)
+    A = _device.Matrix(U, m, n, m if a_colmajor else n, a_colmajor, "numpy")
+    return A, Y.t
+
+
 def _presketch(a, b, rng, max_rank, spec):
     """Host input: overlap the H2D of A with the sketches of the first blocks.
 
@@ -181,48 +237,20 @@ def _presketch(a, b, rng, max_rank, spec):
     copy engine and the DMMA pipe work at the same time; the loop then starts
     with NB sketch blocks already computed.  Returns None when not
     applicable (device input, small input, non-Gaussian or host draws)."""
-    import os
-
-    if isinstance(a, (torch.Tensor, _device.Matrix)) or os.environ.get("RSKEL_PRESKETCH", "1") == "0":
-        return None
     if spec.kind != "gaussian" or _device.host_rng() or b > _engine.MAX_BLOCK:
         return None
-    arr = np.asarray(a)
-    if arr.dtype != np.float64 or arr.ndim != 2 or arr.nbytes < _PRESKETCH_MIN_BYTES:
-        return None
-    if not (arr.flags.c_contiguous or arr.flags.f_contiguous):
+    arr = _streamable(a)
+    if arr is None:
         return None
     m, n = arr.shape
     nb = min(_PRESKETCH_MAX_BLOCKS, max_rank // b + 1)
     if nb < 2:
         return None
     dev = _device.device()
-    width = b * nb
-    om = torch.empty((n, width), dtype=torch.float64, device=dev)
+    om = torch.empty((n, b * nb), dtype=torch.float64, device=dev)
     for t in range(nb):
         om[:, b * t: b * (t + 1)].copy_(_device.gaussian(rng.child(t), n, b))
-    yb = torch.empty((m, width), dtype=torch.float64, device=dev)
-    Y = dense._mat(yb)
-    OM = dense._mat(om)
-    colmajor = not arr.flags.c_contiguous
-    under = arr.T if colmajor else arr            # C-ordered rows: K (colmajor) or M (row-major)
-    compute = torch.cuda.current_stream(dev)
-    holder = {}
-
-    def on_chunk(r0, r1, ev):
-        compute.wait_event(ev)
-        U = holder["U"]
-        if colmajor:   # a = U.T: rows r0..r1 of U are columns (K) of a
-            A_part = _device.Matrix(U, m, r1 - r0, m, True, "numpy", off=r0 * m)
-            dense._gemm(Y, A_part, OM.sub(r0, 0, r1 - r0, width), alpha=1.0,
-                        beta=0.0 if r0 == 0 else 1.0, Cin=Y if r0 > 0 else None)
-        else:          # rows r0..r1 of a are candidates r0..r1
-            A_part = _device.Matrix(U, r1 - r0, n, n, False, "numpy", off=r0 * n)
-            dense._gemm(Y.sub(r0, 0, r1 - r0, width), A_part, OM)
-
-    holder["U"] = torch.empty(under.shape, dtype=torch.float64, device=dev)
-    U_dev = _device.h2d_rows(under, on_chunk, out=holder["U"])
-    A = _device.Matrix(U_dev, m, n, m if colmajor else n, colmajor, "numpy")
+    A, yb = _streamed_sketch(arr, om)
     return A, yb, nb
 
 

@@ -36,3 +36,23 @@ def test_presketch_matches_plain_path(order, monkeypatch):
     e1 = np.linalg.norm(a - r1.w @ a[r1.row_idx]) / na
     e0 = np.linalg.norm(a - r0.w @ a[r0.row_idx]) / na
     assert e1 <= 1.5 * e0 + 1e-13
+
+
+@pytest.mark.parametrize("order", ["C", "F"])
+def test_streamed_fixed_rank_matches_plain_path(order, monkeypatch):
+    import paper_2310_09417_b200 as rs
+
+    g = np.random.default_rng(3)
+    a = np.asarray(g.standard_normal((3000, 2900)), order=order)
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("RSKEL_PRESKETCH", mode)
+        out[mode] = (rs.column_id(a, 200, rs.SketchSpec("gaussian", 3000, 200), rs.RngStream(4)),
+                     rs.rand_lupp(a, 150, rs.SketchSpec("gaussian", 2900, 150), rs.RngStream(5)))
+    (c1, r1), (c0, r0) = out["1"], out["0"]
+    assert np.array_equal(c1.col_idx, c0.col_idx)
+    assert np.allclose(c1.x, c0.x, rtol=1e-9, atol=1e-9)
+    assert np.array_equal(r1.row_idx, r0.row_idx)
+    assert np.allclose(r1.w, r0.w, rtol=1e-9, atol=1e-9)
+    cidx, _ = orc.column_id(a, 200, 4)
+    assert np.array_equal(c1.col_idx, cidx)
