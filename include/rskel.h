@@ -161,6 +161,12 @@ int rs_jacobi_sweep(double* Xt, long long ldx, int p, double* Vt, long long ldv,
                     int nrounds, int npairs, double tol, unsigned long long* max_off, unsigned* barrier,
                     void* stream);
 
+/* W_hat rows of a factored panel: out[i, :nc] = S[ridx[i], :nc] L1^{-1}, L1 the
+ * unit lower triangle of the pivot rows S[sub[a], b] (b < a < nc <= 64); one
+ * row per thread (`_extend_state`, skeleton.py:326-351, on the T form). */
+int rs_what(const double* S, long long lds, const int64_t* sub, int nc, const int64_t* ridx, int R, double* out,
+            long long ldo, void* stream);
+
 /* Dense n x ell form of the SRTT embedding (`sketching.py:134-157,207-216`):
  * Omega[perm[p], j] = scale * signs[q] * DCT-II_ortho(q, p), q = cols[j]. */
 int rs_srtt_dense(int n, int ell, const int64_t* perm, const double* signs, const int64_t* cols, double scale,

@@ -170,6 +170,51 @@ int launch_trinv(const double* T, long long rs_, long long cs_, const int64_t* r
   return cudaGetLastError() == cudaSuccess ? RS_OK : RS_ERR_CUDA;
 }
 
+// ---- W_hat = L_r L_1^{-1} by row-parallel substitution ----------------------
+// out[i, :nc] solves y L1 = x with x = S[ridx[i], :nc] and L1 the unit lower
+// triangle of the pivot rows S[sub[a], b] (b < a < nc): one row per thread,
+// right-looking (y_a final once every later column has been folded in, then
+// x_j -= y_a L1[a][j] for all j < a -- 63 independent FMAs per step), L1 as
+// shared-memory broadcasts.  Replaces the trinv + GEMM pair of the absorb.
+constexpr int WH_T = 128;
+
+__global__ void __launch_bounds__(WH_T) what_kernel(const double* __restrict__ S, long long lds,
+                                                    const int64_t* __restrict__ sub, int nc,
+                                                    const int64_t* __restrict__ ridx, int R,
+                                                    double* __restrict__ out, long long ldo) {
+  __shared__ double L1[TI_MAX][TI_MAX + 1];
+  for (int e = threadIdx.x; e < TI_MAX * TI_MAX; e += blockDim.x) {
+    const int a = e / TI_MAX, b = e - a * TI_MAX;
+    L1[a][b] = (a < nc && b < a) ? S[sub[a] * lds + b] : 0.0;
+  }
+  __syncthreads();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= R) return;
+  const double* src = S + ridx[i] * lds;
+  double x[TI_MAX];
+#pragma unroll
+  for (int j = 0; j < TI_MAX; ++j) x[j] = j < nc ? src[j] : 0.0;
+#pragma unroll
+  for (int a = TI_MAX - 1; a > 0; --a) {
+    const double ya = x[a];  // final (unit diagonal)
+#pragma unroll
+    for (int j = 0; j < a; ++j) x[j] = fma(-ya, L1[a][j], x[j]);
+  }
+  double* dst = out + (long long)i * ldo;
+#pragma unroll
+  for (int j = 0; j < TI_MAX; ++j)
+    if (j < nc) dst[j] = x[j];
+}
+
+int launch_what(const double* S, long long lds, const int64_t* sub, int nc, const int64_t* ridx, int R, double* out,
+                long long ldo, cudaStream_t st) {
+  if (nc < 0 || nc > TI_MAX || R < 0 || ldo < nc) return RS_ERR_ARG;
+  if (nc == 0 || R == 0) return RS_OK;
+  what_kernel<<<(R + WH_T - 1) / WH_T, WH_T, 0, st>>>(S, lds, sub, nc, ridx, R, out, ldo);
+  count_launch(1);
+  return cudaGetLastError() == cudaSuccess ? RS_OK : RS_ERR_CUDA;
+}
+
 // ---- permutation update: perm'[:k] = perm[:k]; perm'[k+i] = perm[k + sub[i]] ----
 __global__ void perm_update_kernel(const int64_t* __restrict__ perm, int64_t* __restrict__ perm_new,
                                    int m, int k, const int64_t* __restrict__ sub) {

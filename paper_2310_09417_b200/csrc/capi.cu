@@ -118,16 +118,11 @@ int rs_absorb_block(int m, int k, int nc, const double* S_, long long lds, const
   if (m < 0 || k < 0 || nc < 0 || nc > kMaxB || k + nc > m) return RS_ERR_ARG;
   const int R = m - k;
   const long long ldn = k + nc;
-  double* linv = reinterpret_cast<double*>(W(workspace, layout().linv_off));
   int rc = RS_OK;
   if (nc > 0) {
-    // L_1^{-1}: unit lower triangle of the pivot rows (positions 0..nc-1).
-    rc = rs::launch_trinv(S_, lds, 1, sub_perm, nc, 1, 1, linv, kMaxB, S(stream));
-    if (rc != RS_OK) return rc;
-    // W_hat = L_r L_1^{-1} -> T_new[:, k:k+nc]
-    rs::DGemmParams pw{R - nc, nc, nc, S_, lds, sub_perm + nc, linv, kMaxB, nullptr, nullptr, 0,
-                       nullptr, T_new + k, ldn, 1.0, 0.0, gemm_ws(workspace)};
-    rc = rs::launch_dgemm(pw, false, S(stream));
+    // W_hat = L_r L_1^{-1} -> T_new[:, k:k+nc] (row-parallel substitution
+    // against the unit lower triangle of the pivot rows)
+    rc = rs::launch_what(S_, lds, sub_perm, nc, sub_perm + nc, R - nc, T_new + k, ldn, S(stream));
     if (rc != RS_OK) return rc;
     if (k > 0) {
       // T_new[:, :k] = T[Q_hat] - W_hat T[P_hat]  (persistent rank-nc update kernel)
@@ -164,14 +159,9 @@ int rs_absorb_schur(int m, int k, int nc, const double* S_, long long lds, const
     return rs_schur_block(m, k + nc, nc > 0 ? kMaxB : 0, Y_next, ldy, perm_new, T_new, ldn, S_next,
                           kMaxB, e2_dev, workspace, stream);
   }
-  double* linv = reinterpret_cast<double*>(W(workspace, layout().linv_off));
   double* zp = reinterpret_cast<double*>(W(workspace, layout().zp_off));
-  // L_1^{-1}, W_hat = L_r L_1^{-1} -> T_new[:, k:k+nc], perm' (as rs_absorb_block)
-  int rc = rs::launch_trinv(S_, lds, 1, sub_perm, nc, 1, 1, linv, kMaxB, S(stream));
-  if (rc != RS_OK) return rc;
-  rs::DGemmParams pw{Rn, nc, nc, S_, lds, sub_perm + nc, linv, kMaxB, nullptr, nullptr, 0,
-                     nullptr, T_new + k, ldn, 1.0, 0.0, gemm_ws(workspace)};
-  rc = rs::launch_dgemm(pw, false, S(stream));
+  // W_hat = L_r L_1^{-1} -> T_new[:, k:k+nc], perm' (as rs_absorb_block)
+  int rc = rs::launch_what(S_, lds, sub_perm, nc, sub_perm + nc, Rn, T_new + k, ldn, S(stream));
   if (rc != RS_OK) return rc;
   rc = rs::launch_perm_update(perm, perm_new, m, k, sub_perm, S(stream));
   if (rc != RS_OK) return rc;
@@ -233,6 +223,11 @@ int rs_jacobi_sweep(double* Xt, long long ldx, int p, double* Vt, long long ldv,
                     int nrounds, int npairs, double tol, unsigned long long* max_off, unsigned* barrier,
                     void* stream) {
   return rs::launch_jacobi_sweep(Xt, ldx, p, Vt, ldv, q, sched, nrounds, npairs, tol, max_off, barrier, S(stream));
+}
+
+int rs_what(const double* S_, long long lds, const int64_t* sub, int nc, const int64_t* ridx, int R, double* out,
+            long long ldo, void* stream) {
+  return rs::launch_what(S_, lds, sub, nc, ridx, R, out, ldo, S(stream));
 }
 
 int rs_srtt_dense(int n, int ell, const int64_t* perm, const double* signs, const int64_t* cols, double scale,

@@ -54,6 +54,8 @@ int launch_sumsq(const double* X, long long ldx, int R, int w, double* partial_w
                  cudaStream_t st);
 int launch_trinv(const double* T, long long rs_, long long cs_, const int64_t* ridx, int n, int lower,
                  int unit, double* out, long long ldo, cudaStream_t st);
+int launch_what(const double* S, long long lds, const int64_t* sub, int nc, const int64_t* ridx, int R, double* out,
+                long long ldo, cudaStream_t st);
 int launch_perm_update(const int64_t* perm, int64_t* perm_new, int m, int k, const int64_t* sub,
                        cudaStream_t st);
 int launch_iota(int64_t* p, int n, cudaStream_t st);

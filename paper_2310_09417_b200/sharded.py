@@ -132,12 +132,11 @@ class DeviceShardOps:
                   count.data_ptr(), pad_to, self.st)
 
     def what(self, S, lds, sub, nc, wsrc, r, linv, out, ldo):
-        """out[i, :nc] = S[wsrc[i]] L1^{-1}, L1 = unit lower part of rows S[sub[:nc]]."""
-        _lib.call("rs_trinv", S.data_ptr(), lds, 1, sub.data_ptr(), nc, 1, 1, linv.data_ptr(), MAX_BLOCK,
-                  self.st)
+        """out[i, :nc] = S[wsrc[i]] L1^{-1}, L1 = unit lower part of rows S[sub[:nc]]
+        (the same substitution kernel as the single-GPU absorb)."""
         if r > 0:
-            _lib.call("rs_dgemm", r, nc, nc, 1.0, S.data_ptr(), lds, 0, wsrc.data_ptr(), linv.data_ptr(),
-                      MAX_BLOCK, None, 0.0, None, 0, None, out.data_ptr(), ldo, self.ws.data_ptr(), self.st)
+            _lib.call("rs_what", S.data_ptr(), lds, sub.data_ptr(), nc, wsrc.data_ptr(), r, out.data_ptr(), ldo,
+                      self.st)
 
     def t_update(self, r, k, nc, Tn, ldn, TP, iota, Tg, src_row):
         """Tn[:, :k] = Tg[src_row] - Tn[:, k:k+nc] @ TP (nc x k)."""
