@@ -1,0 +1,80 @@
+"""The cfg2 recipe (BASELINE.json configs[1]: adaptive column ID, b=64, tau=1e-8 absolute,
+fast-decay beta=1e-16 with Haar bases) at n=6000, CUDA path vs the oracle on the same matrix.
+
+The full-size tolerance of DESIGN.md section 5: pivots identical up to the first candidate
+tie below the rounding level of the Schur block; over the blocks before it the e_schur trace
+agrees to 1e-12 * ||A||_F; once the paths part, rank within +-b, same status; residual
+||A - W A[I]|| / ||A|| within 1% of the oracle's at equal rank, and within 2 tau / ||A|| (the
+stop rule's contract) for both.  (At n=20000 the first tie is at pivot
+12529: profiles/r01_cfg2_full_parity.json, profiles/r01_cfg2_divergence.json.)
+"""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+import randskel_oracle as orc  # noqa: E402
+
+
+def _gen_fast_decay_device(n, beta, seed, device):
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+
+    def haar():
+        q, r = torch.linalg.qr(torch.randn(n, n, generator=g, dtype=torch.float64, device=device))
+        s = torch.sign(torch.diagonal(r))
+        s[s == 0] = 1.0
+        return q * s
+
+    u, v = haar(), haar()
+    d = beta ** (torch.arange(n, dtype=torch.float64, device=device) / (n - 1))
+    return (u * d) @ v.T
+
+
+def test_cfg2_recipe_n6000_vs_oracle():
+    import paper_2310_09417_b200 as rs
+    from threadpoolctl import threadpool_limits
+
+    n, b, tau = 6000, 64, 1e-8
+    dev = torch.device("cuda", 0)
+    a = _gen_fast_decay_device(n, 1e-16, 0, dev)
+    at = a.T
+    res = rs.rand_lupp_adaptive(at, b, tau, rs.SketchSpec("gaussian", n, b), rs.RngStream(0))
+    a_host = a.cpu().numpy()
+    with threadpool_limits(limits=os.cpu_count() or 1):
+        ref = orc.rand_lupp_adaptive(a_host.T, b, tau, 0, 0, want_w=True)
+
+    g_idx = res.row_idx.cpu().numpy()
+    r_idx = np.asarray(ref["row_idx"])
+    nmin = min(len(g_idx), len(r_idx))
+    d = np.nonzero(g_idx[:nmin] != r_idx[:nmin])[0]
+    p0 = nmin if d.size == 0 else int(d[0])
+    norm_a = float(torch.linalg.norm(a))
+
+    assert res.status == ref["status"] == "ok"
+    g_tr = [(r.k, r.e_schur) for r in res.trace]
+    r_tr = ref["trace"]
+    # trace entries whose factorisation used only common pivots
+    common = [i for i in range(min(len(g_tr), len(r_tr))) if g_tr[i][0] <= p0]
+    assert common
+    for i in common:
+        assert g_tr[i][0] == r_tr[i][0]
+        assert abs(g_tr[i][1] - r_tr[i][1]) <= 1e-12 * norm_a
+    if d.size == 0:
+        assert res.rank == ref["rank"]
+    else:
+        assert abs(res.rank - ref["rank"]) <= b
+    w_ref = torch.from_numpy(np.ascontiguousarray(ref["w"])).to(dev)
+    r_ref = float(torch.linalg.norm(at - w_ref @ at[torch.from_numpy(r_idx).to(dev)])) / norm_a
+    r_gpu = rs.row_id_error(at, res) / norm_a
+    print(f"n={n}: rank {res.rank}/{ref['rank']}, common prefix {p0}, resid {r_gpu:.4e}/{r_ref:.4e}, "
+          f"tau/||A|| {tau / norm_a:.4e}, last e/tau {g_tr[-1][1] / tau:.4f}/{r_tr[-1][1] / tau:.4f}")
+    if res.rank == ref["rank"]:
+        assert abs(r_gpu - r_ref) <= 0.01 * r_ref
+    # the stop rule's contract: e_schur (an unbiased estimate of the squared residual
+    # from b Gaussian samples) <= tau; the true residual stays within 2 tau
+    assert r_gpu * norm_a <= 2 * tau and r_ref * norm_a <= 2 * tau
