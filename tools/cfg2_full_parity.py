@@ -45,6 +45,7 @@ def main():
     ap.add_argument("--tau", type=float, default=1e-8)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--rowmajor", action="store_true", help="pass A.T as a row-major copy, not the column-major view")
     args = ap.parse_args()
 
     import torch
@@ -62,7 +63,8 @@ def main():
 
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    res = rs.rand_lupp_adaptive(a.T, b, tau, spec, rs.RngStream(args.seed))
+    at_in = a.T.contiguous() if args.rowmajor else a.T
+    res = rs.rand_lupp_adaptive(at_in, b, tau, spec, rs.RngStream(args.seed))
     torch.cuda.synchronize()
     t_gpu = time.perf_counter() - t0
     g_idx = host(res.row_idx).astype(np.int64)
@@ -93,6 +95,7 @@ def main():
         w_relerr = float(np.linalg.norm(g_w - ref["w"]) / np.linalg.norm(ref["w"]))
     tail = lambda tr: [[int(k), float(e), float(e / tau)] for k, e in tr[-4:]]
     out = {
+        "layout": "row-major A.T copy" if args.rowmajor else "column-major A.T view",
         "workload": f"cfg2 rand_lupp_adaptive(A.T, b={b}, tau={tau:g} abs) on the {n}x{n} fp64 "
                     f"fast-decay matrix of bench.py (beta=1e-16, Haar bases, seed {args.seed})",
         "norm_a": norm_a,
