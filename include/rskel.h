@@ -30,17 +30,24 @@
 extern "C" {
 #endif
 
-#define RS_ABI_VERSION 1
+#define RS_ABI_VERSION 2
 #define RS_OK 0
 #define RS_ERR_ARG -1
 #define RS_ERR_CUDA -2
 #define RS_ERR_CAPACITY -3
 
+/* GEMM accumulation modes (rs_dgemm_ex). */
+#define RS_GEMM_PLAIN 0 /* C = alpha * op(A) B + beta * Cin                          */
+#define RS_GEMM_FOLD 1  /* C = Cin + op(A) B, the K chunks folded onto Cin in order     */
+#define RS_GEMM_CHAIN 2 /* C = Cin + op(A) B, the DMMA chain continued from Cin (K <= kc) */
+
 int rs_abi_version(void);
 const char* rs_status_string(int status);
 
 /* Bytes of scratch the composite calls need (panel candidates, reduction
- * partials, the b x b inverse).  One workspace per stream. */
+ * partials, GEMM partial tiles and their arrival counters).  One workspace
+ * per stream; it must be zero-filled once before its first use (the GEMM
+ * counters return to zero after every call). */
 size_t rs_workspace_bytes(void);
 
 /* Number of kernels this library has launched in the process (instrumentation). */
@@ -51,12 +58,31 @@ unsigned long long rs_launch_count(void);
  * (A[k*lda + i]; aidx must be NULL).  B: K x N row-major, row k at bidx[k].
  * Cin row i at cidx[i].  Replaces the OpenBLAS dgemm calls of `gemm`
  * (dense.py:118-141), `GaussianSketch.apply` (sketching.py:122-128) and the
- * Schur/trailing updates (dense.py:232, skeleton.py:322).  `workspace` (may
- * be NULL) enables the deterministic stream-K split for skinny shapes. */
+ * Schur/trailing updates (dense.py:232, skeleton.py:322).
+ * Summation order: K is cut into chunks of rs_gemm_chunk(K) columns; each
+ * chunk is a DMMA chain from zero and the chunk sums are added in chunk
+ * order.  An output element therefore depends only on its row of op(A), on
+ * B and on K -- not on M, the layout of A, the grid or the device -- which
+ * makes row-sharded and single-GPU sketches / Schur blocks bitwise equal.
+ * `workspace` (rs_workspace_bytes, zero-filled once) is required. */
 int rs_dgemm(int M, int N, int K, double alpha, const double* A, long long lda, int a_colmajor,
              const int64_t* aidx, const double* B, long long ldb, const int64_t* bidx, double beta,
              const double* Cin, long long ldcin, const int64_t* cidx, double* C, long long ldc,
              void* workspace, void* stream);
+
+/* Chunk length (columns of K, a multiple of 32) of the summation order above. */
+int rs_gemm_chunk(long long K);
+
+/* rs_dgemm with an explicit chunk length kc (<= 0: rs_gemm_chunk(K)) and mode:
+ * RS_GEMM_FOLD adds the chunk sums to Cin in order, so a K range fed in
+ * kc-aligned pieces (C = Cin + piece, piece by piece, kc of the full K)
+ * gives the bits of the one-shot product; RS_GEMM_CHAIN continues the DMMA
+ * chain from Cin (K <= kc), the same for the single-chunk case.  Used by the
+ * host-input pre-sketch, which multiplies row chunks of A as they land. */
+int rs_dgemm_ex(int M, int N, int K, int kc, int mode, double alpha, const double* A, long long lda, int a_colmajor,
+                const int64_t* aidx, const double* B, long long ldb, const int64_t* bidx, double beta,
+                const double* Cin, long long ldcin, const int64_t* cidx, double* C, long long ldc,
+                void* workspace, void* stream);
 
 /* Y (m x ell) = A (m x n) * Omega (n x ell): the sketch `a @ omega`
  * (sketching.py:128, 272).  a_colmajor selects the `a.T` view of a C-ordered
@@ -101,8 +127,8 @@ int rs_rank_update(int M, int N, int K, const double* A, long long lda, const do
                    const int64_t* bidx, const double* Cin, long long ldcin, const int64_t* cidx,
                    double* C, long long ldc, void* stream);
 
-/* rs_absorb_block followed by the Schur block of the NEXT sketch block, in
- * one pass over T when nc == 64 (fused DMMA kernel, fused_update.cu):
+/* rs_absorb_block followed by the Schur block of the NEXT sketch block
+ * (the two enqueued back to back, so the host reads one scalar per block):
  *   T_new, perm_new as rs_absorb_block;
  *   S_next = Y_next[perm_new[k+nc:]] - T_new * Y_next[perm_new[:k+nc]],
  *   *e2_dev = ||S_next||_F^2                       (skeleton.py:326-351, 317-323)

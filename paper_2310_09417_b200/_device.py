@@ -31,7 +31,7 @@ def workspace():
     dev = device()
     ws = _workspaces.get(dev.index)
     if ws is None:
-        ws = torch.empty(_lib.load().rs_workspace_bytes(), dtype=torch.uint8, device=dev)
+        ws = torch.zeros(_lib.load().rs_workspace_bytes(), dtype=torch.uint8, device=dev)  # GEMM counters start at 0
         _workspaces[dev.index] = ws
     return ws
 
@@ -215,12 +215,15 @@ def h2d(arr):
     return out
 
 
-def h2d_rows(arr, on_chunk, out=None, chunk_bytes=128 << 20):
+def h2d_rows(arr, on_chunk, out=None, align=1):
     """Row-chunked device copy of a C-contiguous 2-D host array: after each
     chunk's copy is enqueued, ``on_chunk(r0, r1, event)`` is called so work
     on the rows that have landed can be enqueued behind ``event`` while the
     rest is in flight.  Returns the device tensor; the current stream waits
-    for the whole copy at the end."""
+    for the whole copy at the end.  Chunks are ~32 MB rounded to a multiple
+    of ``align`` rows -- the same boundaries for pinned and pageable input,
+    so the work on them (and its rounding) does not depend on the host
+    allocation.  Pageable rows are staged through the pinned 32 MB ring."""
     dev = device()
     rows, cols = arr.shape
     host = torch.from_numpy(arr)
@@ -231,10 +234,12 @@ def h2d_rows(arr, on_chunk, out=None, chunk_bytes=128 << 20):
     ring = _stage_ring(dev)
     cs = ring["stream"]
     cs.wait_stream(torch.cuda.current_stream(dev))
-    step = max(1, (chunk_bytes if pinned else _STAGE_BYTES) // row_bytes)
+    sub = max(1, _STAGE_BYTES // row_bytes)       # rows per pinned staging buffer
+    step = max(align, sub // align * align)       # rows per chunk handed to on_chunk
     pool = _copy_pool()
     nthr = max(1, min(16, pool._max_workers))
-    for i, r0 in enumerate(range(0, rows, step)):
+    i = 0
+    for r0 in range(0, rows, step):
         r1 = min(rows, r0 + step)
         if pinned:
             with torch.cuda.stream(cs):
@@ -242,20 +247,23 @@ def h2d_rows(arr, on_chunk, out=None, chunk_bytes=128 << 20):
                 ev = torch.cuda.Event()
                 ev.record(cs)
         else:
-            slot = i % _STAGE_DEPTH
-            prev = ring["events"][slot]
-            if prev is not None:
-                prev.synchronize()
-            nb = (r1 - r0) * row_bytes
-            buf = ring["bufs"][slot].numpy()[:nb]
-            src = arr[r0:r1].reshape(-1).view(np.uint8)
-            part = -(-nb // nthr)
-            list(pool.map(lambda q: np.copyto(buf[q:q + part], src[q:q + part]), range(0, nb, part)))
-            with torch.cuda.stream(cs):
-                out[r0:r1].view(-1).view(torch.uint8).copy_(ring["bufs"][slot][:nb], non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(cs)
-            ring["events"][slot] = ev
+            for s0 in range(r0, r1, sub):
+                s1 = min(r1, s0 + sub)
+                slot = i % _STAGE_DEPTH
+                i += 1
+                prev = ring["events"][slot]
+                if prev is not None:
+                    prev.synchronize()
+                nb = (s1 - s0) * row_bytes
+                buf = ring["bufs"][slot].numpy()[:nb]
+                src = arr[s0:s1].reshape(-1).view(np.uint8)
+                part = -(-nb // nthr)
+                list(pool.map(lambda q: np.copyto(buf[q:q + part], src[q:q + part]), range(0, nb, part)))
+                with torch.cuda.stream(cs):
+                    out[s0:s1].view(-1).view(torch.uint8).copy_(ring["bufs"][slot][:nb], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(cs)
+                ring["events"][slot] = ev
         on_chunk(r0, r1, ev)
     torch.cuda.current_stream(dev).wait_stream(cs)
     return out

@@ -27,6 +27,9 @@ SIGNATURES = {
     "rs_launch_count": (ctypes.c_ulonglong, []),
     "rs_dgemm": (_c_int, [_c_int, _c_int, _c_int, _c_double, _p, _c_ll, _c_int, _p, _p, _c_ll, _p,
                           _c_double, _p, _c_ll, _p, _p, _c_ll, _p, _p]),
+    "rs_gemm_chunk": (_c_int, [_c_ll]),
+    "rs_dgemm_ex": (_c_int, [_c_int, _c_int, _c_int, _c_int, _c_int, _c_double, _p, _c_ll, _c_int, _p, _p, _c_ll,
+                             _p, _c_double, _p, _c_ll, _p, _p, _c_ll, _p, _p]),
     "rs_sketch_gemm": (_c_int, [_c_int, _c_int, _c_int, _p, _c_ll, _c_int, _p, _c_ll, _p, _c_ll,
                                 _p, _p]),
     "rs_panel_lupp": (_c_int, [_p, _c_ll, _c_int, _c_int, _p, _p, _p, _p]),
@@ -61,7 +64,7 @@ SIGNATURES = {
     "rs_scatter_interp_local": (_c_int, [_p, _c_ll, _p, _c_int, _p, _c_int, _c_ll, _c_ll, _p, _c_ll, _p]),
 }
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 _lib = None
 

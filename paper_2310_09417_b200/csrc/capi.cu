@@ -17,32 +17,35 @@ namespace {
 constexpr int kMaxB = 64;
 
 struct WorkspaceLayout {
-  size_t panel_off, sumsq_off, linv_off, gemm_off, fused_off, zp_off, total;
+  size_t panel_off, sumsq_off, gemm_off, total;
 };
 
+// Fixed layout (device independent); the GEMM ticket counters at the end of
+// the GEMM region must be zero when the workspace is first used.
 WorkspaceLayout layout() {
-  int dev = 0, nsm = 148;
-  cudaGetDevice(&dev);
-  if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
-    cudaGetLastError();
-    nsm = 148;  // no device (build host): size for B200
-  }
   WorkspaceLayout L;
   auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
   L.panel_off = 0;
   L.sumsq_off = up(rs::panel_workspace_bytes());
-  L.linv_off = L.sumsq_off + up(rs::sumsq_workspace_bytes());
-  L.gemm_off = L.linv_off + up(sizeof(double) * kMaxB * kMaxB);
-  L.fused_off = L.gemm_off + up(rs::gemm_partials_bytes(nsm));
-  L.zp_off = L.fused_off + up(rs::absorb_schur_slots_bytes(nsm));
-  L.total = L.zp_off + up(sizeof(double) * kMaxB * kMaxB);
+  L.gemm_off = L.sumsq_off + up(rs::sumsq_workspace_bytes());
+  L.total = L.gemm_off + up(rs::gemm_workspace_bytes());
   return L;
 }
 
 inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 inline char* W(void* ws, size_t off) { return static_cast<char*>(ws) + off; }
-inline double* gemm_ws(void* ws) {
-  return ws ? reinterpret_cast<double*>(W(ws, layout().gemm_off)) : nullptr;
+
+rs::DGemmParams gemm_params(int M, int N, int K, double alpha, const double* A, long long lda, const int64_t* aidx,
+                            const double* B, long long ldb, const int64_t* bidx, double beta, const double* Cin,
+                            long long ldcin, const int64_t* cidx, double* C, long long ldc, int mode, void* ws) {
+  rs::DGemmParams p{M, N, K, A, lda, aidx, B, ldb, bidx, Cin, ldcin, cidx, C, ldc, alpha, beta, mode,
+                    nullptr, nullptr, 0};
+  if (ws) {
+    p.slots = reinterpret_cast<double*>(W(ws, layout().gemm_off));
+    p.tickets = reinterpret_cast<int*>(p.slots + (size_t)rs::GEMM_SLOTS * 128 * 64);
+    p.nslots = rs::GEMM_SLOTS;
+  }
+  return p;
 }
 
 }  // namespace
@@ -65,15 +68,25 @@ size_t rs_workspace_bytes(void) { return layout().total; }
 
 unsigned long long rs_launch_count(void) { return rs::g_launch_count.load(); }
 
+int rs_gemm_chunk(long long K) { return rs::gemm_chunk(K); }
+
+int rs_dgemm_ex(int M, int N, int K, int kc, int mode, double alpha, const double* A, long long lda, int a_colmajor,
+                const int64_t* aidx, const double* B, long long ldb, const int64_t* bidx, double beta,
+                const double* Cin, long long ldcin, const int64_t* cidx, double* C, long long ldc,
+                void* workspace, void* stream) {
+  if (a_colmajor && aidx) return RS_ERR_ARG;
+  if (mode == RS_GEMM_PLAIN && beta != 0.0 && Cin == nullptr) return RS_ERR_ARG;
+  rs::DGemmParams p = gemm_params(M, N, K, alpha, A, lda, aidx, B, ldb, bidx, beta, Cin, ldcin, cidx, C, ldc,
+                                  mode, workspace);
+  return rs::launch_dgemm(p, a_colmajor != 0, kc, S(stream));
+}
+
 int rs_dgemm(int M, int N, int K, double alpha, const double* A, long long lda, int a_colmajor,
              const int64_t* aidx, const double* B, long long ldb, const int64_t* bidx, double beta,
              const double* Cin, long long ldcin, const int64_t* cidx, double* C, long long ldc,
              void* workspace, void* stream) {
-  if (a_colmajor && aidx) return RS_ERR_ARG;
-  if (beta != 0.0 && Cin == nullptr) return RS_ERR_ARG;
-  rs::DGemmParams p{M, N, K, A, lda, aidx, B, ldb, bidx, Cin, ldcin, cidx, C, ldc, alpha, beta,
-                    gemm_ws(workspace)};
-  return rs::launch_dgemm(p, a_colmajor != 0, S(stream));
+  return rs_dgemm_ex(M, N, K, 0, RS_GEMM_PLAIN, alpha, A, lda, a_colmajor, aidx, B, ldb, bidx, beta, Cin, ldcin,
+                     cidx, C, ldc, workspace, stream);
 }
 
 int rs_sketch_gemm(int m, int n, int ell, const double* A, long long lda, int a_colmajor,
@@ -103,9 +116,9 @@ int rs_schur_block(int m, int k, int b, const double* Y, long long ldy, const in
   if (k == 0) {
     rc = rs::launch_gather_rows(Y, ldy, perm, R, b, S_, lds, S(stream));
   } else {
-    rs::DGemmParams p{R, b, k, T, ldt, nullptr, Y, ldy, perm, Y, ldy, perm + k, S_, lds, -1.0, 1.0,
-                      gemm_ws(workspace)};
-    rc = rs::launch_dgemm(p, false, S(stream));
+    rs::DGemmParams p = gemm_params(R, b, k, -1.0, T, ldt, nullptr, Y, ldy, perm, 1.0, Y, ldy, perm + k, S_, lds,
+                                    RS_GEMM_PLAIN, workspace);
+    rc = rs::launch_dgemm(p, false, 0, S(stream));
   }
   if (rc != RS_OK) return rc;
   if (e2_dev) rc = rs_sumsq(S_, lds, R, b, e2_dev, workspace, stream);
@@ -138,43 +151,11 @@ int rs_absorb_schur(int m, int k, int nc, const double* S_, long long lds, const
                     const double* T, long long ldt, double* T_new, const int64_t* perm, int64_t* perm_new,
                     const double* Y_next, long long ldy, double* S_next, double* e2_dev, void* workspace,
                     void* stream) {
-  if (m < 0 || k < 0 || nc < 0 || nc > kMaxB || k + nc > m) return RS_ERR_ARG;
-  const int R = m - k, Rn = R - nc;
-  const long long ldn = k + nc;
-  auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
-  // One pass over T (absorb_schur.cu) with RSKEL_FUSED=1: correct, but on
-  // B200 it is not yet faster than the two tuned kernels (rank update at 64%
-  // and Schur GEMM at 70% DMMA vs 68% for the fused pass), so the default is
-  // the two-pass path.
-  static const bool fused_enabled = [] {
-    const char* e = getenv("RSKEL_FUSED");
-    return e != nullptr && e[0] == '1';
-  }();
-  const bool fused = fused_enabled && nc >= 1 && k >= 1 && k % 2 == 0 && nc % 2 == 0 && ldy == 64 &&
-                     ldt == k && al16(T) && al16(T_new) && al16(Y_next) && al16(S_next) && S_next != S_;
-  if (!fused) {
-    int rc = rs_absorb_block(m, k, nc, S_, lds, sub_perm, T, ldt, T_new, perm, perm_new, workspace, stream);
-    if (rc != RS_OK) return rc;
-    // the next block is 64 columns wide at row stride ldy; S_next is m x 64
-    return rs_schur_block(m, k + nc, nc > 0 ? kMaxB : 0, Y_next, ldy, perm_new, T_new, ldn, S_next,
-                          kMaxB, e2_dev, workspace, stream);
-  }
-  double* zp = reinterpret_cast<double*>(W(workspace, layout().zp_off));
-  // W_hat = L_r L_1^{-1} -> T_new[:, k:k+nc], perm' (as rs_absorb_block)
-  int rc = rs::launch_what(S_, lds, sub_perm, nc, sub_perm + nc, Rn, T_new + k, ldn, S(stream));
+  int rc = rs_absorb_block(m, k, nc, S_, lds, sub_perm, T, ldt, T_new, perm, perm_new, workspace, stream);
   if (rc != RS_OK) return rc;
-  rc = rs::launch_perm_update(perm, perm_new, m, k, sub_perm, S(stream));
-  if (rc != RS_OK) return rc;
-  // Z[P] = Y[perm'[k:k+nc]] - T[P] Y[perm'[:k]]
-  rs::DGemmParams pz{nc, (int)ldy, k, T, ldt, sub_perm, Y_next, ldy, perm_new, Y_next, ldy,
-                     perm_new + k, zp, ldy, -1.0, 1.0, gemm_ws(workspace)};
-  rc = rs::launch_dgemm(pz, false, S(stream));
-  if (rc != RS_OK) return rc;
-  rc = rs::launch_absorb_schur(Rn, k, nc, T, sub_perm, T_new, Y_next, ldy, perm_new, zp, S_next, S_next,
-                               reinterpret_cast<double*>(W(workspace, layout().fused_off)), S(stream));
-  if (rc != RS_OK) return rc;
-  if (e2_dev) rc = rs_sumsq(S_next, ldy, Rn, (int)ldy, e2_dev, workspace, stream);
-  return rc;
+  // the next block is 64 columns wide at row stride ldy; S_next is m x 64
+  return rs_schur_block(m, k + nc, nc > 0 ? kMaxB : 0, Y_next, ldy, perm_new, T_new, k + nc, S_next, kMaxB,
+                        e2_dev, workspace, stream);
 }
 
 int rs_rank_update(int M, int N, int K, const double* A, long long lda, const double* B, long long ldb,

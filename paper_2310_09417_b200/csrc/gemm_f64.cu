@@ -1,6 +1,7 @@
 // fp64 GEMM on the B200 DMMA pipe with optional row gathers.
 //
-//   C[i, :] = alpha * (op(A) B)[i, :] + beta * Cin[cidx(i), :]
+//   C[i, :] = alpha * (op(A) B)[i, :] + beta * Cin[cidx(i), :]      (RS_GEMM_PLAIN)
+//   C[i, :] = Cin[cidx(i), :] + (op(A) B)[i, :]                      (RS_GEMM_FOLD / _CHAIN)
 //
 // A is M x K, either row-major with an optional row index (row i of A lives
 // at aidx[i]) or column-major (the transposed view of a C-ordered matrix, as
@@ -9,17 +10,8 @@
 // step reads the skeleton rows Y[perm[:k]] without materialising them
 // (`skeleton.py:317-323`).  C is row-major.
 //
-// Tiling: CTA 128 x 64 x 16, 8 warps as 4 (M) x 2 (N), warp tile 32 x 32 =
-// 2 x 4 DMMA m16n8k4 tiles, 3-stage cp.async pipeline, 2 CTAs per SM.
-//
-// Work distribution: the skeleton GEMMs are tall and skinny (N = 64, M up to
-// 65536, K up to 65536), so a plain tile grid leaves most of the 148 SMs idle
-// or runs 1.06 waves.  When the tile count is below a few waves the kernel
-// runs stream-K: exactly G = 2 x #SM persistent CTAs, CTA c owning the
-// contiguous range [c U / G, (c+1) U / G) of the U = tiles x k-tiles work
-// units.  Tiles split between CTAs write fragment-ordered partials; a fixup
-// kernel adds them in k order (CTA order) and applies the epilogue.  The
-// split depends only on (M, N, K, G), so results are bitwise reproducible.
+// Tiling: CTA 128 x 64, DMMA m16n8k4, cp.async multi-stage pipeline, 2 CTAs
+// per SM; the summation order is fixed by K alone (see below).
 #include <algorithm>
 #include <cstdlib>
 
@@ -50,35 +42,82 @@ struct GemmCfg {
   static constexpr size_t smem() { return sizeof(double) * STAGES * (a_stage<A_COL>() + b_stage()); }
 };
 
-// Production configuration and the alternatives the tuner compares
-// (RSKEL_GEMM_CFG=i selects one at run time, for tools/bench_kernels.py).
-using Cfg0 = GemmCfg<128, 64, 16, 4, 2, 3, 2>;   // row-major A (Schur, W_hat, small products): 8 warps of 32x32
-using Cfg8 = GemmCfg<128, 64, 32, 2, 2, 2, 2>;   // column-major A (sketch): 4 warps of 64x32, BK 32
-using Cfg12 = GemmCfg<128, 64, 32, 4, 2, 2, 2>;  // 8 warps of 32x32, BK 32
-// Measured alternatives (tools/tune_gemm.sh, B200, sketch 20000^2 x 64 / Schur k=7000):
-// 128x64x16 4 stages 28.x / 24; 64x64x16 4 CTA/SM 26 / 17; 64x32x16 (cuBLAS-like tile) 26.8 / 13.7;
-// 256x64 one CTA/SM 29.0 / 21.7; 8 warps BK 32 (Cfg12) 29.1 / 23.3; Cfg8 31.4 / 19.8; Cfg0 28.2 / 25.5.
-// Stream-K partial slots: 2 per CTA, THREADS * ACC doubles each; every config
-// has MINB * THREADS * ACC <= 16384 doubles per SM.
-constexpr int SK_SLOT_DOUBLES_PER_SM = 16384;
+// Production configurations (measured on B200, tools/tune_gemm.sh: the
+// column-major sketch operand prefers 64x32 warp tiles, the gathered
+// row-major Schur / interpolation operands the 32x32 tiles).
+using CfgRow = GemmCfg<128, 64, 16, 4, 2, 3, 2>;  // row-major A: 8 warps of 32x32, BK 16
+using CfgCol = GemmCfg<128, 64, 32, 2, 2, 2, 2>;  // column-major A: 4 warps of 64x32, BK 32
+constexpr int SLOT_DOUBLES = 128 * 64;            // one BM x BN partial tile
+static_assert(CfgRow::THREADS * CfgRow::ACC == SLOT_DOUBLES && CfgCol::THREADS * CfgCol::ACC == SLOT_DOUBLES,
+              "partial slots hold one tile");
 
-size_t gemm_partials_bytes(int nsm) {
-  return sizeof(double) * 2 * (size_t)nsm * SK_SLOT_DOUBLES_PER_SM;
+// ---------------------------------------------------------------------------
+// Summation order (the determinism contract).
+//
+// K is cut into chunks of kc = gemm_chunk(K) columns, fixed in global k and
+// independent of M, of the tile grid, of the CTA count and of the layout of
+// A.  Chunk c of every output element is a DMMA chain from zero over
+// k in [c kc, (c+1) kc) in steps of 4; the chunk sums are folded in chunk
+// order, v = ((p0 + p1) + p2) + ...  So an element's value depends only on
+// its row of A, B and K: a row gives the same bits whether it is one of
+// 20000 candidates on one GPU or one of 2500 on rank 3 of 8, whether A is
+// column- or row-major, and whether the K range arrives in one call or in
+// kc-aligned pieces (mode RS_GEMM_FOLD below).  Work units are (tile, chunk)
+// pairs spread over a persistent grid; each writes its partial tile to a
+// slot and the last unit of a tile to arrive (ticket counter) folds the slots
+// in chunk order and applies the epilogue.
+size_t gemm_workspace_bytes() {
+  return sizeof(double) * (size_t)GEMM_SLOTS * SLOT_DOUBLES + sizeof(int) * (size_t)GEMM_SLOTS;
 }
 
-struct SkPlan {
-  int tiles_n, tiles, KT, G;
-  long long U;
+int gemm_chunk(long long K) {
+  long long kc = (K + GEMM_MAX_CHUNKS - 1) / GEMM_MAX_CHUNKS;
+  kc = (kc + 31) / 32 * 32;
+  return (int)std::max<long long>(GEMM_MIN_CHUNK, kc);
+}
+
+struct ChunkPlan {
+  int tiles_n;     // tiles along N of the full grid
+  int tile0;       // first tile of this launch (tile groups when slots run out)
+  int KT;          // k-tiles of K
+  int kct;         // k-tiles per chunk
+  int nch;         // chunks
+  int units;       // (tiles of this launch) x nch
 };
 
-// First unit of CTA c.
-__host__ __device__ inline long long sk_u0(const SkPlan& s, int c) { return (long long)c * s.U / s.G; }
+// Fragment coordinates (within the tile) of accumulator element e of this thread.
+template <class C>
+__device__ __forceinline__ void frag_rc(int e, int wm, int wn, int g, int t, int& r, int& c) {
+  const int ee = e & 1, h = (e >> 1) & 1, ij = e >> 2, i = ij / C::NT, j = ij % C::NT;
+  r = wm + 16 * i + g + 8 * h;
+  c = wn + 8 * j + 2 * t + ee;
+}
+
+// acc[e] = the Cin element of fragment e (0 outside the matrix).
+template <class C>
+__device__ __forceinline__ void load_cin(const DGemmParams& p, int m0, int n0, int wm, int wn, int g, int t,
+                                         double (&acc)[C::ACC]) {
+#pragma unroll
+  for (int e = 0; e < C::ACC; ++e) {
+    int r, c;
+    frag_rc<C>(e, wm, wn, g, t, r, c);
+    r += m0;
+    c += n0;
+    double v = 0.0;
+    if (r < p.M && c < p.N) {
+      const long long rr = p.cidx ? p.cidx[r] : r;
+      v = p.Cin[rr * p.ldcin + c];
+    }
+    acc[e] = v;
+  }
+}
 
 // Epilogue for one accumulator set of tile (m0, n0).
 template <class C>
 __device__ __forceinline__ void epilogue_store(const DGemmParams& p, int m0, int n0, int wm, int wn,
                                                int g, int t, const double (&acc)[C::ACC]) {
   const double alpha = p.alpha, beta = p.beta;
+  const bool plain = p.mode == RS_GEMM_PLAIN;
 #pragma unroll
   for (int i = 0; i < C::MT; ++i) {
 #pragma unroll
@@ -87,7 +126,7 @@ __device__ __forceinline__ void epilogue_store(const DGemmParams& p, int m0, int
       if (row >= p.M) continue;
       double* crow = p.C + (long long)row * p.ldc;
       const double* cin = nullptr;
-      if (beta != 0.0) {
+      if (plain && beta != 0.0) {
         long long r = p.cidx ? p.cidx[row] : row;
         cin = p.Cin + r * p.ldcin;
       }
@@ -98,7 +137,7 @@ __device__ __forceinline__ void epilogue_store(const DGemmParams& p, int m0, int
           int col = n0 + wn + 8 * j + 2 * t + e;
           if (col < p.N) {
             double v = acc[(i * C::NT + j) * 4 + 2 * h + e];
-            crow[col] = cin ? fma(alpha, v, beta * cin[col]) : alpha * v;
+            crow[col] = !plain ? v : cin ? fma(alpha, v, beta * cin[col]) : alpha * v;
           }
         }
       }
@@ -106,6 +145,8 @@ __device__ __forceinline__ void epilogue_store(const DGemmParams& p, int m0, int
   }
 }
 
+// DMMA chain over k-tiles [kt0, kt1) of the tile at (m0, n0), continuing
+// from the values already in acc.
 template <class C, bool A_COL, bool VEC2>
 __device__ __forceinline__ void mainloop(const DGemmParams& p, double* As, double* Bs, int m0, int n0,
                                          int kt0, int kt1, double (&acc)[C::ACC]) {
@@ -183,9 +224,6 @@ __device__ __forceinline__ void mainloop(const DGemmParams& p, double* As, doubl
     }
   };
 
-#pragma unroll
-  for (int e = 0; e < C::ACC; ++e) acc[e] = 0.0;
-
   const int nkt = kt1 - kt0;
 #pragma unroll
   for (int s = 0; s < C::STAGES - 1; ++s) {
@@ -229,12 +267,16 @@ __device__ __forceinline__ void mainloop(const DGemmParams& p, double* As, doubl
     }
   }
   cp_async_wait<0>();
-  __syncthreads();  // stage buffers are reused by the next tile of this CTA
+  __syncthreads();  // stage buffers are reused by the next unit of this CTA
 }
 
+// Persistent grid over the (tile, chunk) units of one launch: unit u is tile
+// tile0 + u / nch, chunk u % nch; CTA c takes units c, c + G, c + 2G, ...,
+// so the chunks of a tile run side by side and their slots stay in L2.
 template <class C, bool A_COL, bool VEC2>
-__global__ void __launch_bounds__(C::THREADS, C::MINB) dgemm_kernel(DGemmParams p, SkPlan sk) {
+__global__ void __launch_bounds__(C::THREADS, C::MINB) dgemm_kernel(DGemmParams p, ChunkPlan pl) {
   extern __shared__ __align__(16) double smem[];
+  __shared__ int s_last;
   double* As = smem;
   double* Bs = smem + C::STAGES * C::template a_stage<A_COL>();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -242,139 +284,85 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) dgemm_kernel(DGemmParams 
   const int wm = (warp % C::WARPS_M) * C::WTM, wn = (warp / C::WARPS_M) * C::WTN;
   double acc[C::ACC];
 
-  if (sk.G == 0) {  // classic tile grid
-    const int n0 = blockIdx.x * C::BN, m0 = blockIdx.y * C::BM;
-    mainloop<C, A_COL, VEC2>(p, As, Bs, m0, n0, 0, sk.KT, acc);
-    epilogue_store<C>(p, m0, n0, wm, wn, g, t, acc);
-    return;
-  }
-  // stream-K
-  const int c = blockIdx.x;
-  long long u = sk_u0(sk, c), u1 = sk_u0(sk, c + 1);
-  while (u < u1) {
-    const int tile = (int)(u / sk.KT);
-    const int i0 = (int)(u - (long long)tile * sk.KT);
-    const int i1 = (int)min((long long)sk.KT, i0 + (u1 - u));
-    const int m0 = (tile / sk.tiles_n) * C::BM, n0 = (tile % sk.tiles_n) * C::BN;
-    mainloop<C, A_COL, VEC2>(p, As, Bs, m0, n0, i0, i1, acc);
-    if (i0 == 0 && i1 == sk.KT) {
-      epilogue_store<C>(p, m0, n0, wm, wn, g, t, acc);
+  for (int u = blockIdx.x; u < pl.units; u += gridDim.x) {
+    const int lt = u / pl.nch, ch = u - lt * pl.nch;
+    const int tile = pl.tile0 + lt;
+    const int m0 = (tile / pl.tiles_n) * C::BM, n0 = (tile % pl.tiles_n) * C::BN;
+    const int kt0 = ch * pl.kct, kt1 = min(pl.KT, kt0 + pl.kct);
+    if (p.mode == RS_GEMM_CHAIN) {
+      load_cin<C>(p, m0, n0, wm, wn, g, t, acc);
     } else {
-      // element-major slot layout: coalesced writes here and reads in the fixup
-      const int slot = (i0 > 0) ? 2 * c : 2 * c + 1;
-      double* dst = p.partials + (size_t)slot * C::THREADS * C::ACC + tid;
 #pragma unroll
-      for (int e = 0; e < C::ACC; ++e) dst[(size_t)e * C::THREADS] = acc[e];
+      for (int e = 0; e < C::ACC; ++e) acc[e] = 0.0;
     }
-    u += i1 - i0;
-  }
-}
-
-// Sum the partials of every split tile in k order and apply the epilogue.
-template <class C>
-__global__ void __launch_bounds__(C::THREADS) dgemm_fixup_kernel(DGemmParams p, SkPlan sk) {
-  const int tile = blockIdx.x;
-  const long long ub = (long long)tile * sk.KT, ue = ub + sk.KT;
-  // owner(u): largest c with u0(c) <= u
-  auto owner = [&](long long u) {
-    int c = (int)((u * sk.G) / sk.U);
-    while (c + 1 < sk.G && sk_u0(sk, c + 1) <= u) ++c;
-    while (c > 0 && sk_u0(sk, c) > u) --c;
-    return c;
-  };
-  const int clo = owner(ub), chi = owner(ue - 1);
-  if (clo == chi) return;  // complete tile, stored by its CTA
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  const int wm = (warp % C::WARPS_M) * C::WTM, wn = (warp / C::WARPS_M) * C::WTN;
-  double acc[C::ACC];
-  {
-    const double* src = p.partials + (size_t)(2 * clo + 1) * C::THREADS * C::ACC + tid;
+    mainloop<C, A_COL, VEC2>(p, As, Bs, m0, n0, kt0, kt1, acc);
+    if (pl.nch == 1) {
+      if (p.mode == RS_GEMM_FOLD) {
+        double v[C::ACC];
+        load_cin<C>(p, m0, n0, wm, wn, g, t, v);
 #pragma unroll
-    for (int e = 0; e < C::ACC; ++e) acc[e] = src[(size_t)e * C::THREADS];
-  }
-  for (int c = clo + 1; c <= chi; ++c) {
-    const double* src = p.partials + (size_t)(2 * c) * C::THREADS * C::ACC + tid;
+        for (int e = 0; e < C::ACC; ++e) v[e] += acc[e];
+        epilogue_store<C>(p, m0, n0, wm, wn, g, t, v);
+      } else {
+        epilogue_store<C>(p, m0, n0, wm, wn, g, t, acc);
+      }
+      continue;
+    }
+    // element-major slot layout: coalesced stores here and loads in the fold
+    double* slot = p.slots + (size_t)u * SLOT_DOUBLES + tid;
 #pragma unroll
-    for (int e = 0; e < C::ACC; ++e) acc[e] += src[(size_t)e * C::THREADS];
+    for (int e = 0; e < C::ACC; ++e) __stcg(slot + (size_t)e * C::THREADS, acc[e]);
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(p.tickets + lt, 1) == pl.nch - 1;
+    __syncthreads();
+    if (!s_last) continue;
+    __threadfence();
+    // last unit of the tile to arrive: fold the chunk partials in chunk order
+    const double* base = p.slots + (size_t)lt * pl.nch * SLOT_DOUBLES + tid;
+    if (p.mode == RS_GEMM_FOLD) {
+      load_cin<C>(p, m0, n0, wm, wn, g, t, acc);
+#pragma unroll
+      for (int e = 0; e < C::ACC; ++e) acc[e] += __ldcg(base + (size_t)e * C::THREADS);
+    } else {
+#pragma unroll
+      for (int e = 0; e < C::ACC; ++e) acc[e] = __ldcg(base + (size_t)e * C::THREADS);
+    }
+    for (int c = 1; c < pl.nch; ++c) {
+      const double* src = base + (size_t)c * SLOT_DOUBLES;
+#pragma unroll
+      for (int e = 0; e < C::ACC; ++e) acc[e] += __ldcg(src + (size_t)e * C::THREADS);
+    }
+    epilogue_store<C>(p, m0, n0, wm, wn, g, t, acc);
+    if (tid == 0) p.tickets[lt] = 0;  // ready for the next launch on this workspace
   }
-  const int m0 = (tile / sk.tiles_n) * C::BM, n0 = (tile % sk.tiles_n) * C::BN;
-  epilogue_store<C>(p, m0, n0, wm, wn, g, t, acc);
-}
-
-// Fixup for skinny splits (many CTAs per tile): CTA (tile, e) sums element e
-// of every thread's partial over the contributors (in CTA order) and stores it.
-template <class C>
-__global__ void __launch_bounds__(C::THREADS) dgemm_fixup_elem_kernel(DGemmParams p, SkPlan sk) {
-  const int tile = blockIdx.x, e = blockIdx.y;
-  const long long ub = (long long)tile * sk.KT, ue = ub + sk.KT;
-  auto owner = [&](long long u) {
-    int c = (int)((u * sk.G) / sk.U);
-    while (c + 1 < sk.G && sk_u0(sk, c + 1) <= u) ++c;
-    while (c > 0 && sk_u0(sk, c) > u) --c;
-    return c;
-  };
-  const int clo = owner(ub), chi = owner(ue - 1);
-  if (clo == chi) return;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  const int wm = (warp % C::WARPS_M) * C::WTM, wn = (warp / C::WARPS_M) * C::WTN;
-  double acc = p.partials[(size_t)(2 * clo + 1) * C::THREADS * C::ACC + (size_t)e * C::THREADS + tid];
-  for (int c = clo + 1; c <= chi; ++c)
-    acc += p.partials[(size_t)(2 * c) * C::THREADS * C::ACC + (size_t)e * C::THREADS + tid];
-  // e = ((i * NT + j) * 4 + 2h + ee): fragment row/column of this element
-  const int ee = e & 1, h = (e >> 1) & 1, ij = e >> 2, i = ij / C::NT, j = ij % C::NT;
-  const int m0 = (tile / sk.tiles_n) * C::BM, n0 = (tile % sk.tiles_n) * C::BN;
-  const int row = m0 + wm + 16 * i + g + 8 * h, col = n0 + wn + 8 * j + 2 * t + ee;
-  if (row >= p.M || col >= p.N) return;
-  double v = p.alpha * acc;
-  if (p.beta != 0.0) {
-    const long long r = p.cidx ? p.cidx[row] : row;
-    v = fma(p.alpha, acc, p.beta * p.Cin[r * p.ldcin + col]);
-  }
-  p.C[(long long)row * p.ldc + col] = v;
 }
 
 template <class C, bool A_COL, bool VEC2>
-static int launch_dgemm_t(const DGemmParams& p, cudaStream_t st) {
-  static_assert(C::MINB * C::THREADS * C::ACC <= SK_SLOT_DOUBLES_PER_SM, "partials workspace");
+static int launch_dgemm_t(const DGemmParams& p, int kc, cudaStream_t st) {
   constexpr size_t smem = C::template smem<A_COL>();
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(dgemm_kernel<C, A_COL, VEC2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = true;
-  }
+  // set on every launch: the attribute is per device and one process may drive several
+  cudaFuncSetAttribute(dgemm_kernel<C, A_COL, VEC2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  SkPlan sk;
-  sk.tiles_n = (p.N + C::BN - 1) / C::BN;
+  ChunkPlan pl;
+  pl.tiles_n = (p.N + C::BN - 1) / C::BN;
   const int tiles_m = (p.M + C::BM - 1) / C::BM;
-  sk.tiles = sk.tiles_n * tiles_m;
-  sk.KT = (p.K + C::BK - 1) / C::BK;
-  sk.G = 0;
-  sk.U = (long long)sk.tiles * sk.KT;
+  const long long tiles = (long long)pl.tiles_n * tiles_m;
+  pl.KT = (p.K + C::BK - 1) / C::BK;
+  pl.kct = kc / C::BK;
+  pl.nch = std::max(1, (pl.KT + pl.kct - 1) / pl.kct);
   const int slots = nsm * C::MINB;
-  // Stream-K when a plain grid would run fewer than ~4 waves and each CTA
-  // still gets a few k-tiles of work.
-  // Skinny products (fewer tiles than CTA slots, long K) split K over up to
-  // `slots` CTAs with at least 4 k-tiles each.
-  int G = 0;
-  if (p.partials != nullptr && sk.tiles < 4 * slots && sk.KT >= 8) {
-    if (sk.U >= 4LL * slots) G = slots;
-    else if (sk.tiles < slots && sk.KT >= 64) G = (int)std::max<long long>(sk.tiles, std::min<long long>(slots, sk.U / 4));
-  }
-  if (G > 0) {
-    sk.G = G;
-    dgemm_kernel<C, A_COL, VEC2><<<sk.G, C::THREADS, smem, st>>>(p, sk);
-    if (sk.G > 8 * sk.tiles)  // many contributors per tile: element-parallel sum
-      dgemm_fixup_elem_kernel<C><<<dim3(sk.tiles, C::ACC), C::THREADS, 0, st>>>(p, sk);
-    else
-      dgemm_fixup_kernel<C><<<sk.tiles, C::THREADS, 0, st>>>(p, sk);
-    count_launch(2);
-  } else {
-    dim3 grid(sk.tiles_n, tiles_m);
-    dgemm_kernel<C, A_COL, VEC2><<<grid, C::THREADS, smem, st>>>(p, sk);
+  // tile groups: as many tiles per launch as the partial slots hold, balanced
+  const long long per = pl.nch == 1 ? tiles : std::max<long long>(1, p.nslots / pl.nch);
+  const long long ngroups = (tiles + per - 1) / per;
+  for (long long gi = 0; gi < ngroups; ++gi) {
+    const long long t0 = tiles * gi / ngroups, t1 = tiles * (gi + 1) / ngroups;
+    pl.tile0 = (int)t0;
+    pl.units = (int)((t1 - t0) * pl.nch);
+    const int G = std::min(pl.units, slots);
+    dgemm_kernel<C, A_COL, VEC2><<<G, C::THREADS, smem, st>>>(p, pl);
     count_launch(1);
   }
   return cudaGetLastError() == cudaSuccess ? RS_OK : RS_ERR_CUDA;
@@ -382,34 +370,19 @@ static int launch_dgemm_t(const DGemmParams& p, cudaStream_t st) {
 
 static bool al16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; }
 
-template <class C>
-static int launch_cfg(const DGemmParams& p, bool a_col, bool vec2, cudaStream_t st) {
-  if (a_col) return vec2 ? launch_dgemm_t<C, true, true>(p, st) : launch_dgemm_t<C, true, false>(p, st);
-  return vec2 ? launch_dgemm_t<C, false, true>(p, st) : launch_dgemm_t<C, false, false>(p, st);
-}
-
-static int selected_cfg() {
-  static int cfg = -2;
-  if (cfg == -2) {
-    const char* e = getenv("RSKEL_GEMM_CFG");
-    cfg = e ? atoi(e) : -1;
-  }
-  return cfg;
-}
-
-int launch_dgemm(const DGemmParams& p, bool a_col, cudaStream_t st) {
+int launch_dgemm(const DGemmParams& p, bool a_col, int kc, cudaStream_t st) {
   if (p.M < 0 || p.N < 0 || p.K < 0) return RS_ERR_ARG;
+  if (p.mode != RS_GEMM_PLAIN && p.mode != RS_GEMM_FOLD && p.mode != RS_GEMM_CHAIN) return RS_ERR_ARG;
+  if (p.mode != RS_GEMM_PLAIN && p.Cin == nullptr) return RS_ERR_ARG;
+  if (kc <= 0) kc = gemm_chunk(p.K);
+  if (kc % 32 != 0) return RS_ERR_ARG;
+  if (p.mode == RS_GEMM_CHAIN && kc < p.K) return RS_ERR_ARG;  // a chain continues inside one chunk
   if (p.M == 0 || p.N == 0) return RS_OK;
-  bool vec2 = al16(p.A) && al16(p.B) && (p.lda % 2 == 0) && (p.ldb % 2 == 0);
-  switch (selected_cfg()) {
-    case 8: return launch_cfg<Cfg8>(p, a_col, vec2, st);
-    case 12: return launch_cfg<Cfg12>(p, a_col, vec2, st);
-    default:
-      // Measured on B200 (tools/tune_gemm.sh): the column-major sketch operand
-      // prefers 64x32 warp tiles (31.4 TF/s vs 28.2), the gathered row-major
-      // Schur/interpolation operands the 32x32 tiles of Cfg0.
-      return a_col ? launch_cfg<Cfg8>(p, a_col, vec2, st) : launch_cfg<Cfg0>(p, a_col, vec2, st);
-  }
+  if (p.slots == nullptr || p.tickets == nullptr || p.nslots < 1) return RS_ERR_ARG;
+  const bool vec2 = al16(p.A) && al16(p.B) && (p.lda % 2 == 0) && (p.ldb % 2 == 0);
+  if (a_col)
+    return vec2 ? launch_dgemm_t<CfgCol, true, true>(p, kc, st) : launch_dgemm_t<CfgCol, true, false>(p, kc, st);
+  return vec2 ? launch_dgemm_t<CfgRow, false, true>(p, kc, st) : launch_dgemm_t<CfgRow, false, false>(p, kc, st);
 }
 
 }  // namespace rs

@@ -25,30 +25,16 @@
 // Shared memory holds the rows with a 64-double stride and an XOR swizzle
 // (column c of local row i at i*64 + (c ^ (i & 31))), conflict-free for both
 // the row-per-thread (early) and row-per-warp (late) access patterns.
+//
+// Large panels (more rows than 148 x 227 KB of shared memory holds, about
+// 65,000 x 64): the same kernel with the rows left in place in global memory
+// (ROWS_GLOBAL; R x 64 fp64 is 51 MB at R = 100,000 and stays in the 126 MB
+// L2), the position map in shared memory.  Same arithmetic, same pivots.
 #include <atomic>
 #include <cstdlib>
 
 #include "common.cuh"
 #include "rskel_internal.h"
-
-// Optional per-phase timestamps (build with -DRS_PANEL_PROBE_ON; read with
-// rs_panel_probe): clock64 of thread 0 per phase and column, kept in shared
-// memory during the run and written out by CTAs 0 and 1 at the end (global
-// stores inside the step loop perturb the exchange they are timing).
-#ifdef RS_PANEL_PROBE_ON
-__device__ unsigned long long g_panel_probe[2][8][64];
-#define RS_PANEL_PROBE(k)                          \
-  do {                                             \
-    if (threadIdx.x == 0) s_probe[k][j] = clock64(); \
-  } while (0)
-extern "C" void rs_panel_probe(unsigned long long* out) {
-  cudaMemcpyFromSymbol(out, g_panel_probe, sizeof(g_panel_probe));
-}
-#else
-#define RS_PANEL_PROBE(k) \
-  do {                    \
-  } while (0)
-#endif
 
 namespace rs {
 
@@ -65,18 +51,13 @@ struct PanelScratch {
   // broadcast: no line is shared by two writers or polled by many readers
   // (a hot line serialises in its L2 slice and made each hop ~1.3 us).
   uint4 rec[2][PMAXG][8];           // [0] = {val.lo, f, val.hi, f}, [1] = {pos, f, row + 1, f}
-  uint4 bc[2][PMAXG][8];            // per-CTA winner copy: [0] val, [1] {pos, row + 1}, [2] {cta}
   uint4 rowdata[2][PMAXG][PMAXW];   // candidate row: {x.lo, f, x.hi, f} per column
 };
 
 RS_DEV void st_v4(uint4* p, unsigned a, unsigned b, unsigned c, unsigned d) {
-#ifdef RS_PANEL_WEAK_ST
-  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};\n" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
-#else
   // gpu-scope relaxed: .volatile (= relaxed.sys) stores were serialised (~150 ns each)
   asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1,%2,%3,%4};\n" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d)
                : "memory");
-#endif
 }
 RS_DEV uint4 ld_v4(const uint4* p) {
   uint4 v;
@@ -118,11 +99,11 @@ RS_DEV void block_best(double& v, int& p, int& r, double* red_v, int* red_p, int
   __syncthreads();
 }
 
-template <int QMAX>
+template <int QMAX, bool ROWS_GLOBAL>
 __global__ void __launch_bounds__(PTHREADS, 1)
     panel_kernel(double* __restrict__ S, long long lds, int R, int w, int rows_per,
                  int64_t* __restrict__ perm_out, int* __restrict__ ncols_out, PanelScratch* ws,
-                 unsigned flag_base, int central) {
+                 unsigned flag_base) {
   extern __shared__ __align__(16) double psm[];
   const int G = gridDim.x, cta = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -130,20 +111,25 @@ __global__ void __launch_bounds__(PTHREADS, 1)
   int nloc = R - r0;
   nloc = nloc < 0 ? 0 : (nloc > rows_per ? rows_per : nloc);
 
-  double* Ss = psm;                                                   // rows_per x 64 (swizzled)
-  int* pos = reinterpret_cast<int*>(psm + (size_t)rows_per * PMAXW);  // rows_per
+  // local row i, column c: swizzled shared memory, or the row in place in S
+  double* Ss = psm;
+  double* const Sg = S + (long long)r0 * lds;
+  auto at = [&](int i, int c) -> double& {
+    if constexpr (ROWS_GLOBAL) return Sg[(long long)i * lds + c];
+    else return Ss[swz(i, c)];
+  };
+  int* pos = reinterpret_cast<int*>(psm + (ROWS_GLOBAL ? 0 : (size_t)rows_per * PMAXW));  // rows_per
   __shared__ double Urow2[2][PMAXW];  // U row of step j in Urow2[j & 1] (late update reads j-1)
   __shared__ double red_v[PWARPS];
   __shared__ int red_p[PWARPS], red_r[PWARPS];
   __shared__ double s_val;
   __shared__ int s_pos, s_row;
-#ifdef RS_PANEL_PROBE_ON
-  __shared__ unsigned long long s_probe[8][PMAXW];
-#endif
 
-  for (int idx = tid; idx < nloc * w; idx += PTHREADS) {
-    int i = idx / w, c = idx - i * w;
-    Ss[swz(i, c)] = S[(long long)(r0 + i) * lds + c];
+  if constexpr (!ROWS_GLOBAL) {
+    for (int idx = tid; idx < nloc * w; idx += PTHREADS) {
+      int i = idx / w, c = idx - i * w;
+      Ss[swz(i, c)] = S[(long long)(r0 + i) * lds + c];
+    }
   }
   for (int i = tid; i < nloc; i += PTHREADS) pos[i] = r0 + i;
   __syncthreads();
@@ -152,7 +138,7 @@ __global__ void __launch_bounds__(PTHREADS, 1)
   double bv = -1.0;
   int bp = 0x7fffffff, br = -1;
   for (int i = tid; i < nloc; i += PTHREADS) {
-    double v = fabs(Ss[swz(i, 0)]);
+    double v = fabs(at(i, 0));
     if (key_better(v, pos[i], bv, bp) || br < 0) { bv = v; bp = pos[i]; br = i; }
   }
   block_best(bv, bp, br, red_v, red_p, red_r);
@@ -162,7 +148,6 @@ __global__ void __launch_bounds__(PTHREADS, 1)
   int late_skip = -1;
   for (int j = 0; j < w; ++j) {
     const int par = j & 1;
-    RS_PANEL_PROBE(0);
     if (warp == 0) {
       const unsigned f = flag_base + (unsigned)j + 1u;
       // ---- publish this CTA's candidate for column j (no fence needed).
@@ -176,17 +161,15 @@ __global__ void __launch_bounds__(PTHREADS, 1)
       }
       if (br >= 0) {
         for (int c = lane; c < w; c += 32) {
-          const unsigned long long x = (unsigned long long)__double_as_longlong(Ss[swz(br, c)]);
+          const unsigned long long x = (unsigned long long)__double_as_longlong(at(br, c));
           st_v4(&ws->rowdata[par][cta][c], (unsigned)x, f, (unsigned)(x >> 32), f);
         }
       }
-      RS_PANEL_PROBE(1);
       // ---- reduce the G candidates: every CTA polls all records itself
-      // (all-to-all, one hop) or, with `central`, CTA 0 reduces and writes a
-      // per-CTA broadcast copy (two hops, G x fewer polled lines) ----
+      // (all-to-all, one hop; identical reduction order on every CTA) ----
       double v = -1.0;
       int pp = 0x7fffffff, rr = -1, cc = -1;
-      if (cta == 0 || !central) {
+      {
         // Poll all of this lane's records in one pass (loads issued back to
         // back, then checked), repeat only for the ones not yet published.
         const int nq = (G - lane + 31) / 32;
@@ -221,29 +204,8 @@ __global__ void __launch_bounds__(PTHREADS, 1)
           int oc = __shfl_xor_sync(0xffffffffu, cc, off);
           if (orr >= 0 && (rr < 0 || key_better(ov, op, v, pp))) { v = ov; pp = op; rr = orr; cc = oc; }
         }
-        if (central) {
-          const unsigned long long x = (unsigned long long)__double_as_longlong(rr >= 0 ? v : 0.0);
-          for (int q = 1 + lane; q < G; q += 32) {
-            st_v4(&ws->bc[par][q][0], (unsigned)x, f, (unsigned)(x >> 32), f);
-            st_v4(&ws->bc[par][q][1], (unsigned)pp, f, (unsigned)(rr + 1), f);
-            st_v4(&ws->bc[par][q][2], (unsigned)cc, f, 0u, f);
-          }
-        }
-      } else {
-        uint4 h = make_uint4(0, 0, 0, 0);
-        if (lane < 3) {
-          do {
-            h = ld_v4(&ws->bc[par][cta][lane]);
-          } while (h.y != f || h.w != f);
-        }
-        const unsigned x0 = __shfl_sync(0xffffffffu, h.x, 0), x1 = __shfl_sync(0xffffffffu, h.z, 0);
-        v = join(x0, x1);
-        pp = (int)__shfl_sync(0xffffffffu, h.x, 1);
-        rr = (int)__shfl_sync(0xffffffffu, h.z, 1) - 1;
-        cc = (int)__shfl_sync(0xffffffffu, h.x, 2);
       }
       if (lane == 0) { s_val = rr >= 0 ? v : 0.0; s_pos = pp; s_row = rr; }
-      RS_PANEL_PROBE(2);
       // ---- pivot row (U row j) straight from the winner's published copy ----
       if (rr >= 0 && v > 0.0) {
         const int c0 = j + lane, c1 = j + lane + 32;
@@ -256,7 +218,6 @@ __global__ void __launch_bounds__(PTHREADS, 1)
           if (need1 && x1.y == f && x1.w == f) { Urow2[par][c1] = join(x1.x, x1.z); need1 = false; }
         }
       }
-      RS_PANEL_PROBE(3);
     } else if (late_j >= 0) {
       // ---- late update of the previous step (off the critical path) ----
       // Rank-1 update of columns jl+2.. of every live row; each lane owns at
@@ -277,22 +238,22 @@ __global__ void __launch_bounds__(PTHREADS, 1)
           for (int q = 0; q < 4; ++q) {
             rr4[q] = i + q * WS;
             ok[q] = pos[rr4[q]] > jl && rr4[q] != late_skip;
-            l[q] = Ss[swz(rr4[q], jl)];
-            a[q] = Ss[swz(rr4[q], c0)];
-            b[q] = h1 ? Ss[swz(rr4[q], c1)] : 0.0;
+            l[q] = at(rr4[q], jl);
+            a[q] = at(rr4[q], c0);
+            b[q] = h1 ? at(rr4[q], c1) : 0.0;
           }
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             if (!ok[q]) continue;
-            Ss[swz(rr4[q], c0)] = __dsub_rn(a[q], __dmul_rn(l[q], u0));
-            if (h1) Ss[swz(rr4[q], c1)] = __dsub_rn(b[q], __dmul_rn(l[q], u1));
+            at(rr4[q], c0) = __dsub_rn(a[q], __dmul_rn(l[q], u0));
+            if (h1) at(rr4[q], c1) = __dsub_rn(b[q], __dmul_rn(l[q], u1));
           }
         }
         for (; i < nloc; i += WS) {
           if (pos[i] <= jl || i == late_skip) continue;
-          const double l = Ss[swz(i, jl)];
-          Ss[swz(i, c0)] = __dsub_rn(Ss[swz(i, c0)], __dmul_rn(l, u0));
-          if (h1) Ss[swz(i, c1)] = __dsub_rn(Ss[swz(i, c1)], __dmul_rn(l, u1));
+          const double l = at(i, jl);
+          at(i, c0) = __dsub_rn(at(i, c0), __dmul_rn(l, u0));
+          if (h1) at(i, c1) = __dsub_rn(at(i, c1), __dmul_rn(l, u1));
         }
       }
     }
@@ -301,7 +262,6 @@ __global__ void __launch_bounds__(PTHREADS, 1)
     const int ppos = s_pos, prow = s_row;
 
     // ---- swap bookkeeping, scale column j, update column j+1, next candidate ----
-    RS_PANEL_PROBE(5);
     const double upiv = Urow2[par][j];
     const double unext = (j + 1 < w) ? Urow2[par][j + 1] : 0.0;
     bv = -1.0; bp = 0x7fffffff; br = -1;
@@ -310,45 +270,40 @@ __global__ void __launch_bounds__(PTHREADS, 1)
       if (pi < j) continue;
       if (r0 + i == prow) { pos[i] = j; continue; }
       if (pi == j) { pi = ppos; pos[i] = pi; }
-      const double l = __ddiv_rn(Ss[swz(i, j)], upiv);
-      Ss[swz(i, j)] = l;
+      const double l = __ddiv_rn(at(i, j), upiv);
+      at(i, j) = l;
       if (j + 1 < w) {
-        const int a = swz(i, j + 1);
-        const double v = __dsub_rn(Ss[a], __dmul_rn(l, unext));
-        Ss[a] = v;
+        double& a = at(i, j + 1);
+        const double v = __dsub_rn(a, __dmul_rn(l, unext));
+        a = v;
         const double av = fabs(v);
         if (br < 0 || key_better(av, pi, bv, bp)) { bv = av; bp = pi; br = i; }
       }
     }
-    RS_PANEL_PROBE(6);
     block_best(bv, bp, br, red_v, red_p, red_r);
-    RS_PANEL_PROBE(4);
     // The new local best row is published next step: bring it fully up to date.
     if (warp == 0 && br >= 0) {
-      const double l = Ss[swz(br, j)];
+      const double l = at(br, j);
       for (int c = j + 2 + lane; c < w; c += 32) {
-        const int a = swz(br, c);
-        Ss[a] = __dsub_rn(Ss[a], __dmul_rn(l, Urow2[par][c]));
+        double& a = at(br, c);
+        a = __dsub_rn(a, __dmul_rn(l, Urow2[par][c]));
       }
       __syncwarp();
     }
-    RS_PANEL_PROBE(7);
     late_j = j;
     late_skip = br;
   }
   __syncthreads();
 
   // ---- write back factors (physical row order) and the position map ----
-  for (int idx = tid; idx < nloc * w; idx += PTHREADS) {
-    int i = idx / w, c = idx - i * w;
-    S[(long long)(r0 + i) * lds + c] = Ss[swz(i, c)];
+  if constexpr (!ROWS_GLOBAL) {
+    for (int idx = tid; idx < nloc * w; idx += PTHREADS) {
+      int i = idx / w, c = idx - i * w;
+      S[(long long)(r0 + i) * lds + c] = Ss[swz(i, c)];
+    }
   }
   for (int i = tid; i < nloc; i += PTHREADS) perm_out[pos[i]] = r0 + i;
   if (cta == 0 && tid == 0) *ncols_out = ncols;
-#ifdef RS_PANEL_PROBE_ON
-  if (cta < 2)
-    for (int e = tid; e < 8 * PMAXW; e += PTHREADS) g_panel_probe[cta][e / PMAXW][e % PMAXW] = s_probe[e / PMAXW][e % PMAXW];
-#endif
 }
 
 int launch_panel(double* S, long long lds, int R, int w, int64_t* perm_out, int* ncols_dev,
@@ -365,33 +320,35 @@ int launch_panel(double* S, long long lds, int R, int w, int64_t* perm_out, int*
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   // Small panels: fewer CTAs (cheaper exchange).  Large: one CTA per SM.
   int G = (R + 127) / 128;
-  if (const char* e = getenv("RSKEL_PANEL_ROWS_PER_CTA")) {
-    int rp = atoi(e);
-    if (rp > 0) G = (R + rp - 1) / rp;
-  }
   if (G > nsm) G = nsm;
+  if (G > PMAXG) G = PMAXG;
   if (G < 1) G = 1;
-  int rows_per = (R + G - 1) / G;
+  const int rows_per = (R + G - 1) / G;
   const size_t static_smem = 2048;
-  size_t smem = (size_t)rows_per * PMAXW * sizeof(double) + (size_t)rows_per * sizeof(int);
-  smem = (smem + 15) & ~size_t(15);
+  auto round16 = [](size_t x) { return (x + 15) & ~size_t(15); };
+  size_t smem = round16((size_t)rows_per * PMAXW * sizeof(double) + (size_t)rows_per * sizeof(int));
+  // rows in shared memory when they fit, else in place in global memory (L2)
+  const bool rows_global = smem + static_smem > (size_t)max_smem;
+  if (rows_global) smem = round16((size_t)rows_per * sizeof(int));
   if (smem + static_smem > (size_t)max_smem) return RS_ERR_CAPACITY;
   // Polled record slots per lane: G <= 32 * QMAX (a small QMAX keeps the
   // exchange loop short).
-  const void* kern = G <= 32 ? (const void*)panel_kernel<1>
-                   : G <= 64 ? (const void*)panel_kernel<2>
-                   : G <= 128 ? (const void*)panel_kernel<4> : (const void*)panel_kernel<8>;
+  const int q = G <= 32 ? 0 : G <= 64 ? 1 : G <= 128 ? 2 : 3;
+  static const void* const kernels[2][4] = {
+      {(const void*)panel_kernel<1, false>, (const void*)panel_kernel<2, false>, (const void*)panel_kernel<4, false>,
+       (const void*)panel_kernel<8, false>},
+      {(const void*)panel_kernel<1, true>, (const void*)panel_kernel<2, true>, (const void*)panel_kernel<4, true>,
+       (const void*)panel_kernel<8, true>}};
+  const void* kern = kernels[rows_global ? 1 : 0][q];
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, PTHREADS, smem);
-  if (occ * nsm < G || G > PMAXG) return RS_ERR_CAPACITY;
+  if (occ * nsm < G) return RS_ERR_CAPACITY;
   PanelScratch* ws = static_cast<PanelScratch*>(workspace);
   // Flags of launch e are e*128 + j + 1: stale words of earlier launches never match.
   static std::atomic<unsigned> epoch{1};
   unsigned flag_base = (epoch.fetch_add(1) & 0x1ffffffu) << 7;
-  int central = 0;
-  if (const char* e = getenv("RSKEL_PANEL_CENTRAL")) central = atoi(e);
-  void* args[] = {&S, &lds, &R, &w, &rows_per, &perm_out, &ncols_dev, &ws, &flag_base, &central};
+  void* args[] = {&S, &lds, &R, &w, (void*)&rows_per, &perm_out, &ncols_dev, &ws, &flag_base};
   cudaError_t e = cudaLaunchCooperativeKernel(kern, dim3(G), dim3(PTHREADS), args, smem, st);
   count_launch(1);
   return e == cudaSuccess ? RS_OK : RS_ERR_CUDA;

@@ -5,73 +5,22 @@
 //
 // with C = T_new[:, :k] (M = m-k-nc rows, N = k columns), A = W_hat, B = the
 // pivot rows T[P_hat] and Cin = T[Q_hat].  Short K, huge M x N: the kernel is
-// a streaming pipeline, not a k-loop.
+// a streaming pipeline, not a k-loop.  Every element is one DMMA chain over
+// k = 0..K-1 in steps of 4 followed by Cin - acc, whichever kernel runs, so
+// the result of a row does not depend on M or on the tile it lands in.
 //
-// Warp-specialised persistent design (one CTA per SM):
-//  * 1 producer warp issues 1-D bulk async copies (cp.async.bulk, the TMA
-//    engine's non-tensor form) of whole gathered rows -- the K B rows and the
-//    64 Cin rows of a 64 x 32 output tile, and the 64 x K A strip -- into a
-//    4-stage shared-memory ring, completion tracked by mbarrier transaction
-//    counts (no per-thread address math or cp.async groups);
-//  * 8 consumer warps (warp tile 16 x 16, DMMA m16n8k4) wait on the stage's
-//    full barrier, run the 16 k-steps, write C = Cin - A B with 16-byte
-//    stores straight from registers, and release the stage.
-// Rows are placed at padded strides (68 / 36 doubles, = 4 mod 16) so the
-// 64-bit fragment loads are bank-conflict free.  A generic cp.async kernel
-// (rank_update_kernel) remains for shapes the bulk path cannot take
-// (odd K, N or leading dimensions, misaligned pointers).
+//  * rank_update_stream_kernel (default): one CTA per SM walks contiguous
+//    128 x 64 tiles; the W_hat strip stays in registers as DMMA fragments,
+//    the gathered B and Cin rows stream through a cp.async ring.
+//  * rank_update_kernel: the generic cp.async kernel for shapes the
+//    streaming kernel cannot take (odd K, N or leading dimensions,
+//    misaligned pointers).
 #include <cstdlib>
 
 #include "common.cuh"
 #include "rskel_internal.h"
 
 namespace rs {
-
-// ------------------------------------------------------------ mbarrier/bulk --
-RS_DEV unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
-RS_DEV void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-}
-RS_DEV void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-RS_DEV void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
-RS_DEV void mbar_wait(uint64_t* bar, unsigned parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-RS_DEV void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-// ------------------------------------------------------------- bulk kernel --
-#ifndef RS_RU_WBN
-#define RS_RU_WBN 64
-#endif
-#ifndef RS_RU_STAGES
-#define RS_RU_STAGES 2
-#endif
-constexpr int WBM = 64, WBN = RS_RU_WBN, WK = 64, WSTAGES = RS_RU_STAGES;
-constexpr int W_CONSUMERS = 8;                         // warps 0..7: 4 (M) x 2 (N), warp tile 16 x WBN/2
-constexpr int WNT = WBN / 16;                          // n8 tiles per warp
-constexpr int W_THREADS = (W_CONSUMERS + 1) * 32;      // + producer warp 8
-constexpr int WA_LD = WK + 4, WB_LD = WBN + 4, WC_LD = WBN + 4;  // = 4 (mod 16)
-constexpr int WA_ELEMS = WBM * WA_LD;
-constexpr int WB_ELEMS = WK * WB_LD, WC_ELEMS = WBM * WC_LD;
-constexpr int WSTAGE_ELEMS = WB_ELEMS + WC_ELEMS;
-constexpr size_t W_SMEM = sizeof(double) * (2 * WA_ELEMS + WSTAGES * WSTAGE_ELEMS) + 1024;
 
 struct RankUpdateParams {
   int M, N, K;
@@ -87,142 +36,6 @@ struct RankUpdateParams {
   long long ldc;
   int tiles_n, tiles;
 };
-
-__global__ void __launch_bounds__(W_THREADS, 1) rank_update_bulk_kernel(RankUpdateParams p) {
-  extern __shared__ __align__(128) double wsm[];
-  double* Abuf = wsm;                              // [2][WBM][WA_LD]
-  double* Sbuf = wsm + 2 * WA_ELEMS;               // [WSTAGES][B | C]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(Sbuf + WSTAGES * WSTAGE_ELEMS);
-  uint64_t* full = bars;                           // [WSTAGES]
-  uint64_t* empty = bars + WSTAGES;                // [WSTAGES]
-  uint64_t* a_full = bars + 2 * WSTAGES;           // [2]
-  uint64_t* a_empty = bars + 2 * WSTAGES + 2;      // [2]
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int G = gridDim.x, c = blockIdx.x;
-  const int t0 = (int)((long long)c * p.tiles / G), t1 = (int)((long long)(c + 1) * p.tiles / G);
-
-  // Zero the K padding of A and B once (the producer only writes columns /
-  // rows < K), then initialise the barriers.
-  for (int e = tid; e < 2 * WBM * (WA_LD - p.K); e += W_THREADS) {
-    const int r = e / (WA_LD - p.K), cc = p.K + e % (WA_LD - p.K);
-    Abuf[(r / WBM) * WA_ELEMS + (r % WBM) * WA_LD + cc] = 0.0;
-  }
-  for (int e = tid; e < WSTAGES * (WK - p.K) * WB_LD; e += W_THREADS) {
-    const int s = e / ((WK - p.K) * WB_LD), rem = e % ((WK - p.K) * WB_LD);
-    Sbuf[s * WSTAGE_ELEMS + (p.K + rem / WB_LD) * WB_LD + rem % WB_LD] = 0.0;
-  }
-  if (tid == 0) {
-    for (int s = 0; s < WSTAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], W_CONSUMERS);
-    }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&a_full[s], 1);
-      mbar_init(&a_empty[s], W_CONSUMERS);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncthreads();
-  if (t0 >= t1) return;
-
-  if (warp == W_CONSUMERS) {
-    // ================= producer =================
-    int stage = 0, phase = 0, a_slot = -1, strip = -1;
-    unsigned a_phase[2] = {0u, 0u};
-    const unsigned a_bytes = (unsigned)(p.K * 8);
-    for (int tile = t0; tile < t1; ++tile) {
-      const int tstrip = tile / p.tiles_n;
-      const int m0 = tstrip * WBM, n0 = (tile % p.tiles_n) * WBN;
-      const int rows = min(WBM, p.M - m0);
-      if (tstrip != strip) {
-        strip = tstrip;
-        a_slot = (a_slot + 1) & 1;
-        mbar_wait(&a_empty[a_slot], a_phase[a_slot] ^ 1u);
-        if (lane == 0) mbar_expect_tx(&a_full[a_slot], a_bytes * rows);
-        __syncwarp();
-        double* dst = Abuf + a_slot * WA_ELEMS;
-        for (int r = lane; r < rows; r += 32)
-          bulk_g2s(dst + r * WA_LD, p.A + (long long)(m0 + r) * p.lda, a_bytes, &a_full[a_slot]);
-        a_phase[a_slot] ^= 1u;
-      }
-      const int cols = min(WBN, p.N - n0);
-      const unsigned row_bytes = (unsigned)(cols * 8);
-      mbar_wait(&empty[stage], (unsigned)phase ^ 1u);
-      if (lane == 0) mbar_expect_tx(&full[stage], row_bytes * (p.K + rows));
-      __syncwarp();
-      double* bs = Sbuf + stage * WSTAGE_ELEMS;
-      double* cs = bs + WB_ELEMS;
-      for (int r = lane; r < p.K; r += 32)
-        bulk_g2s(bs + r * WB_LD, p.B + p.bidx[r] * p.ldb + n0, row_bytes, &full[stage]);
-      for (int r = lane; r < rows; r += 32)
-        bulk_g2s(cs + r * WC_LD, p.Cin + p.cidx[m0 + r] * p.ldcin + n0, row_bytes, &full[stage]);
-      if (++stage == WSTAGES) { stage = 0; phase ^= 1; }
-    }
-    return;
-  }
-
-  // ================= consumers =================
-  const int g = lane >> 2, t = lane & 3;
-  const int wm = (warp & 3) * 16, wn = (warp >> 2) * (WBN / 2);
-  int stage = 0, phase = 0, a_slot = -1, strip = -1;
-  unsigned a_phase[2] = {0u, 0u};
-  for (int tile = t0; tile < t1; ++tile) {
-    const int tstrip = tile / p.tiles_n;
-    const int m0 = tstrip * WBM, n0 = (tile % p.tiles_n) * WBN;
-    if (tstrip != strip) {
-      if (a_slot >= 0) {  // release the previous strip's A
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&a_empty[a_slot]);
-      }
-      strip = tstrip;
-      a_slot = (a_slot + 1) & 1;
-      mbar_wait(&a_full[a_slot], a_phase[a_slot]);
-      a_phase[a_slot] ^= 1u;
-    }
-    mbar_wait(&full[stage], (unsigned)phase);
-    const double* as = Abuf + a_slot * WA_ELEMS;
-    const double* bs = Sbuf + stage * WSTAGE_ELEMS;
-    const double* cs = bs + WB_ELEMS;
-    double acc[WNT][4];
-#pragma unroll
-    for (int j = 0; j < WNT; ++j)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) acc[j][e] = 0.0;
-#pragma unroll
-    for (int kk = 0; kk < WK; kk += 4) {
-      const double a0 = as[(wm + g) * WA_LD + kk + t];
-      const double a1 = as[(wm + g + 8) * WA_LD + kk + t];
-#pragma unroll
-      for (int j = 0; j < WNT; ++j) dmma_16x8x4(acc[j], a0, a1, bs[(kk + t) * WB_LD + wn + 8 * j + g]);
-    }
-    // epilogue: C = Cin - acc (one rounding, as cin - (a @ b)), 16-byte stores
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int r = wm + g + 8 * h;
-      const int gm = m0 + r;
-      if (gm < p.M) {
-        double* crow = p.C + (long long)gm * p.ldc;
-#pragma unroll
-        for (int j = 0; j < WNT; ++j) {
-          const int col = wn + 8 * j + 2 * t;
-          const int gn = n0 + col;
-          const double2 cin = *reinterpret_cast<const double2*>(cs + r * WC_LD + col);
-          const double v0 = cin.x - acc[j][2 * h];
-          const double v1 = cin.y - acc[j][2 * h + 1];
-          if (gn + 1 < p.N) {
-            *reinterpret_cast<double2*>(crow + gn) = make_double2(v0, v1);
-          } else if (gn < p.N) {
-            crow[gn] = v0;
-          }
-        }
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[stage]);
-    if (++stage == WSTAGES) { stage = 0; phase ^= 1; }
-  }
-}
 
 // -------------------------------------------------- generic cp.async kernel --
 constexpr int UBM = 64, UBN = 64, UK = 64;
@@ -540,12 +353,9 @@ static void launch_stream(RankUpdateParams p, int nsm, cudaStream_t st) {
   p.tiles_n = (p.N + C::BN - 1) / C::BN;
   p.tiles = p.tiles_n * ((p.M + BM - 1) / BM);
   const int G = p.tiles < nsm ? p.tiles : nsm;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(rank_update_stream_kernel<BM, WARPS_N, STAGES>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-    configured = true;
-  }
+  // set on every launch: the attribute is per device
+  cudaFuncSetAttribute(rank_update_stream_kernel<BM, WARPS_N, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)C::SMEM);
   rank_update_stream_kernel<BM, WARPS_N, STAGES><<<G, 256, C::SMEM, st>>>(p);
 }
 
@@ -558,54 +368,20 @@ int launch_rank_update(int M, int N, int K, const double* A, long long lda, cons
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
-  const bool bulk_ok = K > 0 && K % 2 == 0 && N % 2 == 0 && al16(A) && al16(B) && al16(Cin) && al16(C) &&
-                       lda % 2 == 0 && ldb % 2 == 0 && ldcin % 2 == 0 && ldc % 2 == 0;
+  const bool vec2 = al16(A) && al16(B) && al16(Cin) && al16(C) && lda % 2 == 0 && ldb % 2 == 0 &&
+                    ldcin % 2 == 0 && ldc % 2 == 0;
   RankUpdateParams p{M, N, K, A, lda, B, ldb, bidx, Cin, ldcin, cidx, C, ldc, 0, 0};
-  // Default: the 2-CTA/SM cp.async kernel (17-18 TF/s on B200); the bulk-copy
-  // pipeline (15 TF/s, per-row copy rate bound) is opt-in via RSKEL_RU_BULK=1.
-  static const bool prefer_bulk = [] {
-    const char* e = getenv("RSKEL_RU_BULK");
-    return e != nullptr && e[0] == '1';
-  }();
-  static const int ru_kernel = [] {
-    // 0: 2-CTA cp.async, 1: bulk, 3: streaming 128 x 64 tiles (default), 4: streaming 64 x 64
-    const char* e = getenv("RSKEL_RU_KERNEL");
-    return e != nullptr ? atoi(e) : 3;
-  }();
-  const bool stream_ok = bulk_ok && K <= 64;
-  if (stream_ok && (ru_kernel == 3 || ru_kernel == 4) && !prefer_bulk) {
-    if (ru_kernel == 4)
-      launch_stream<64, 2, 3>(p, nsm, st);
-    else
-      launch_stream<128, 1, 2>(p, nsm, st);
-  } else if (bulk_ok && (prefer_bulk || ru_kernel == 1)) {
-    p.tiles_n = (N + WBN - 1) / WBN;
-    p.tiles = p.tiles_n * ((M + WBM - 1) / WBM);
-    const int G = p.tiles < nsm ? p.tiles : nsm;
-    static bool configured = false;
-    if (!configured) {
-      cudaFuncSetAttribute(rank_update_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)W_SMEM);
-      configured = true;
-    }
-    rank_update_bulk_kernel<<<G, W_THREADS, W_SMEM, st>>>(p);
+  if (vec2 && K > 0 && K % 2 == 0 && N % 2 == 0) {
+    launch_stream<128, 1, 2>(p, nsm, st);
   } else {
     p.tiles_n = (N + UBN - 1) / UBN;
     p.tiles = p.tiles_n * ((M + UBM - 1) / UBM);
     const int G = p.tiles < 2 * nsm ? p.tiles : 2 * nsm;
-    const bool vec2 = al16(A) && al16(B) && al16(Cin) && al16(C) && lda % 2 == 0 && ldb % 2 == 0 &&
-                      ldcin % 2 == 0 && ldc % 2 == 0;
-    static bool configured[2] = {false, false};
     if (vec2) {
-      if (!configured[1]) {
-        cudaFuncSetAttribute(rank_update_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)U_SMEM);
-        configured[1] = true;
-      }
+      cudaFuncSetAttribute(rank_update_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)U_SMEM);
       rank_update_kernel<true><<<G, UTHREADS, U_SMEM, st>>>(p);
     } else {
-      if (!configured[0]) {
-        cudaFuncSetAttribute(rank_update_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)U_SMEM);
-        configured[0] = true;
-      }
+      cudaFuncSetAttribute(rank_update_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)U_SMEM);
       rank_update_kernel<false><<<G, UTHREADS, U_SMEM, st>>>(p);
     }
   }

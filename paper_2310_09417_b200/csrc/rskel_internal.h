@@ -23,20 +23,25 @@ struct DGemmParams {
   double* C;
   long long ldc;
   double alpha, beta;
-  double* partials;  // stream-K scratch (gemm_partials_bytes), nullptr = plain grid
+  int mode;          // RS_GEMM_PLAIN / RS_GEMM_FOLD / RS_GEMM_CHAIN (rskel.h)
+  double* slots;     // partial-tile slots (GEMM_SLOTS x 128 x 64 doubles)
+  int* tickets;      // per-tile arrival counters (GEMM_SLOTS ints, zero between launches)
+  int nslots;
 };
 
-int launch_dgemm(const DGemmParams& p, bool a_col, cudaStream_t st);
+// Deterministic chunking of K (gemm_f64.cu): at most GEMM_MAX_CHUNKS chunks of
+// kc >= GEMM_MIN_CHUNK columns, kc a multiple of 32, a function of K alone.
+constexpr int GEMM_SLOTS = 4096;
+constexpr int GEMM_MAX_CHUNKS = 32;
+constexpr int GEMM_MIN_CHUNK = 512;
+size_t gemm_workspace_bytes();
+int gemm_chunk(long long K);
+// kc <= 0: gemm_chunk(K)
+int launch_dgemm(const DGemmParams& p, bool a_col, int kc, cudaStream_t st);
 // C[i, :] = Cin[cidx[i], :] - A[i, :K] B[bidx[0..K), :], K <= 64 (rank_update.cu)
 int launch_rank_update(int M, int N, int K, const double* A, long long lda, const double* B,
                        long long ldb, const int64_t* bidx, const double* Cin, long long ldcin,
                        const int64_t* cidx, double* C, long long ldc, cudaStream_t st);
-size_t gemm_partials_bytes(int nsm);
-// Absorb(t) + Schur(t+1) with one read of T (absorb_schur.cu).
-size_t absorb_schur_slots_bytes(int nsm);
-int launch_absorb_schur(int Rn, int k, int nc, const double* T, const int64_t* sub, double* Tn,
-                        const double* Y, long long ldy, const int64_t* perm_new, const double* ZP, double* X,
-                        double* S, double* slots, cudaStream_t st);
 
 // Panel LUPP (cooperative grid).  Factors the R x w row-major block S in
 // place with partial pivoting (first maximum in the current position wins,

@@ -16,7 +16,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from . import _device, _engine, _omega, dense
+from . import _device, _engine, _lib, _omega, dense
 from .errors import DimensionError, RankDeficientError
 from .sketching import make_sketch
 
@@ -213,18 +213,26 @@ def _streamed_sketch(arr, om, transpose=False):
     t_colmajor = a_colmajor != transpose       # target's layout over `under`
     compute = torch.cuda.current_stream(dev)
     U = torch.empty(under.shape, dtype=torch.float64, device=dev)
+    K = under.shape[0]
+    # K-chunked accumulation (column-major target) in pieces aligned to the
+    # GEMM's fixed chunks: the bits equal the one-shot product (rs_dgemm_ex)
+    kc = _lib.load().rs_gemm_chunk(K) if t_colmajor else 1
+    mode = 1 if kc < K else 2   # RS_GEMM_FOLD across chunks / RS_GEMM_CHAIN inside one
 
     def on_chunk(r0, r1, ev):
         compute.wait_event(ev)
         if t_colmajor:   # rows r0..r1 of `under` are columns (K) of the target
             A_part = _device.Matrix(U, tm, r1 - r0, tm, True, "numpy", off=r0 * tm)
-            dense._gemm(Y, A_part, OM.sub(r0, 0, r1 - r0, width), alpha=1.0,
-                        beta=0.0 if r0 == 0 else 1.0, Cin=Y if r0 > 0 else None)
+            B_part = OM.sub(r0, 0, r1 - r0, width)
+            _lib.call("rs_dgemm_ex", tm, width, r1 - r0, kc if kc < K else K, 0 if r0 == 0 else mode, 1.0,
+                      A_part.ptr, A_part.ld, 1, None, B_part.ptr, B_part.ld, None, 0.0,
+                      Y.ptr if r0 > 0 else None, Y.ld, None, Y.ptr, Y.ld, _device.workspace().data_ptr(),
+                      _device.stream_handle())
         else:            # rows r0..r1 of `under` are rows of the target
             A_part = _device.Matrix(U, r1 - r0, tn, tn, False, "numpy", off=r0 * tn)
             dense._gemm(Y.sub(r0, 0, r1 - r0, width), A_part, OM)
 
-    _device.h2d_rows(under, on_chunk, out=U)
+    _device.h2d_rows(under, on_chunk, out=U, align=kc)
     A = _device.Matrix(U, m, n, m if a_colmajor else n, a_colmajor, "numpy")
     return A, Y.t
 
@@ -320,7 +328,7 @@ class _AdaptiveDriver:
         self.yb, self.nb_pre = presketch if presketch is not None else (None, 0)
         self.dev_rng = not (host or _device.host_rng())
         self.src = None if (self.dev_rng or self.kind != "gaussian") else _omega.BlockOmegaSource(n, b, rng)
-        self.rng_status = torch.zeros(max_rank // b + 4, dtype=torch.int32, device=dev)
+        self.rng_status = torch.zeros(max(max_rank, b) // b + 4, dtype=torch.int32, device=dev)
         self.om = [torch.empty((n, b), dtype=torch.float64, device=dev) for _ in range(2)]
         self.y = [torch.empty((m, b), dtype=torch.float64, device=dev) for _ in range(2)]
         self.om_ready = [torch.cuda.Event() for _ in range(2)]
@@ -334,7 +342,9 @@ class _AdaptiveDriver:
         self.nc = torch.empty(max(1, (b + 63) // 64), dtype=torch.int32, device=dev)
         self.h_e2 = torch.empty(1, dtype=torch.float64, pin_memory=True)
         self.h_nc = torch.empty(1, dtype=torch.int32, pin_memory=True)
-        self.st = _engine.TFormState(m, max_rank, min(b, _engine.MAX_BLOCK))
+        # the first block is always absorbed whole (adaptive_init), so the
+        # rank can reach b even when max_rank < b (`skeleton.py:435-441`)
+        self.st = _engine.TFormState(m, max(max_rank, b), min(b, _engine.MAX_BLOCK))
         self.stream = _device.stream_handle()
         self.ws = _device.workspace()
         self._issued = set()

@@ -49,7 +49,7 @@ def test_ctypes_table_matches_header():
 
 
 def test_abi_version_and_status_strings(lib):
-    assert lib.rs_abi_version() == 1
+    assert lib.rs_abi_version() == 2
     assert lib.rs_status_string(0) == b"ok"
     assert b"capacity" in lib.rs_status_string(-3)
     assert lib.rs_workspace_bytes() > (1 << 20)

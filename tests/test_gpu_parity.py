@@ -319,22 +319,3 @@ def test_adaptive_rank_exhausted_full_width_block(b):
     assert np.array_equal(res.row_idx, ref["row_idx"])
     err = np.linalg.norm(a - res.w @ a[res.row_idx]) / np.linalg.norm(a)
     assert err <= 1e-12
-
-
-def test_absorb_schur_one_pass_matches_two_pass():
-    """RSKEL_FUSED=1 (one pass over T: Schur of the next block against the
-    old factorisation + rank-nc correction) agrees with the two-pass kernels:
-    T' bitwise, S' and e2 to rounding (tools/check_absorb_schur.py)."""
-    import subprocess
-
-    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, RSKEL_FUSED="1", PYTHONPATH=repo)
-    out = subprocess.run([sys.executable, os.path.join(repo, "tools", "check_absorb_schur.py")], env=env,
-                         capture_output=True, text=True, timeout=600)
-    assert out.returncode == 0, out.stderr
-    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("n=")]
-    assert len(lines) == 3
-    for ln in lines:
-        assert "perm equal True" in ln and "T' max diff 0.000e+00" in ln, ln
-        rel = float(ln.split("S' max rel diff ")[1].split(",")[0])
-        assert rel < 1e-13, ln
