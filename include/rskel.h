@@ -254,6 +254,35 @@ int rs_scatter_rows(const double* src, long long lds, const int64_t* idx, int nr
 int rs_scatter_interp_local(const double* T, long long ldt, const int64_t* perm, int k, const int64_t* loc, int r,
                             long long lo, long long hi, double* W, long long ldw, void* stream);
 
+/* ---- input generators (input generation, not the
+ * skeleton path).  Each is restated in numpy by the oracle with the same
+ * rounding, so the device matrix equals the host one bit for bit. ------- */
+
+/* out[i] = numpy Generator(Philox(key=[seed, stream_id])).random(n)[i]. */
+int rs_uniform(unsigned long long seed, unsigned long long stream_id, long long n, double* out, void* stream);
+
+/* x (n x n, row-major, n a power of two) = rowscale * (c H), H the
+ * Walsh-Hadamard matrix: the first factor of the randomized-Hadamard
+ * fast-decay generator (cfg5).  rowscale may be NULL. */
+int rs_hadamard_init(double* x, long long ld, int n, double c, const double* rowscale, void* stream);
+
+/* x <- rowscale * (c * H x): Walsh-Hadamard transform of every column of the
+ * n x n row-major x (n a power of two, <= 2^17), butterflies in numpy's
+ * level order, then the scale c and the optional row scale. */
+int rs_fwht_rows(double* x, long long ld, int n, double c, const double* rowscale, void* stream);
+
+/* Kahan's matrix `gen_kahan` (zoo.py:78-88): a[i, j] = rowpow[i] * k[i, j],
+ * k = 1 on the diagonal, negphi above it, 0 below; rowpow[i] = zeta^i. */
+int rs_kahan(double* a, long long ld, int n, const double* rowpow, double negphi, void* stream);
+
+/* `gen_chan` (zoo.py:91-104): 1 on the diagonal, -1 below, last column 1. */
+int rs_chan(double* a, long long ld, int n, void* stream);
+
+/* out = x + beta * y elementwise (n values), to out64 or rounded to out32
+ * (exactly one non-NULL): the low-rank-plus-noise recipe of cfg3. */
+int rs_axpy_cast(const double* x, const double* y, double beta, long long n, double* out64, float* out32,
+                 void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -374,6 +374,62 @@ def gen_chan(n):
     return a
 
 
+def fwht_rows(x, c, rowscale=None):
+    """x <- rowscale * (c * H x), H acting on the row index, butterfly levels
+    h = 1, 2, ..., n/2 (the device generator rs_fwht_rows, gen.cu)."""
+    n = x.shape[0]
+    h = 1
+    while h < n:
+        v = x.reshape(n // (2 * h), 2, h, x.shape[1])
+        a = v[:, 0].copy()
+        b = v[:, 1].copy()
+        v[:, 0] = a + b
+        v[:, 1] = a - b
+        h *= 2
+    x *= c
+    if rowscale is not None:
+        x *= rowscale[:, None]
+    return x
+
+
+def gen_fast_decay_hadamard(n, beta, seed, stream=0):
+    """cfg5's input (paper_2310_09417_b200.zoo.gen_fast_decay_hadamard):
+    A = (H S0 H S1) diag(d) (S3 H S2 H), H = Walsh-Hadamard / sqrt(n),
+    signs from Generator(Philox(key=[seed, stream])).integers(0, 2, (4, n)).
+    Same operations and rounding order as the device kernels."""
+    gen = np.random.Generator(np.random.Philox(key=[seed & _M64, stream & _M64]))
+    signs = gen.integers(0, 2, size=(4, n)).astype(np.float64) * 2.0 - 1.0
+    d = np.ones(1) if n == 1 else beta ** (np.arange(n) / (n - 1))
+    c = 1.0 / np.sqrt(n)
+    x = fwht_rows(np.eye(n), c, signs[2])
+    x = fwht_rows(x, c, signs[3] * d * signs[1])
+    x = fwht_rows(x, c, signs[0])
+    x = fwht_rows(x, c)
+    return x, d
+
+
+def cfg3_test_matrix(m, n, r=200, rel_noise=1e-6, seed=0):
+    """cfg3's non-negative low-rank-plus-noise recipe at a checkable size,
+    made bit-reproducible on any host: W, H have 8-bit dyadic entries in
+    [0, 1) (so W @ H is exact whatever the BLAS), N is uniform [0, 1), the
+    norms are exactly rounded (math.fsum) and the rest is elementwise IEEE.
+    Returns the fp32 matrix (the reference upcasts it to fp64)."""
+    import math
+
+    g = np.random.default_rng(seed)
+    w = g.integers(0, 256, size=(m, r)).astype(np.float64) / 256.0
+    h = g.integers(0, 256, size=(r, n)).astype(np.float64) / 256.0
+    low = w @ h
+    noise = g.random((m, n))
+    eta = rel_noise * math.sqrt(math.fsum((low * low).ravel())) / math.sqrt(math.fsum((noise * noise).ravel()))
+    return (low + eta * noise).astype(np.float32)
+
+
+def philox_uniform(seed, stream, shape):
+    """numpy Generator(Philox(key=[seed, stream])).random(shape)."""
+    return np.random.Generator(np.random.Philox(key=[seed & _M64, stream & _M64])).random(shape)
+
+
 def exact_rank(m, n, r, seed):
     """`test_skeleton.py:12-14`."""
     g = np.random.default_rng(seed)

@@ -62,6 +62,12 @@ SIGNATURES = {
                                _p, _p, _p, _c_int, _p]),
     "rs_scatter_rows": (_c_int, [_p, _c_ll, _p, _c_int, _c_int, _p, _c_ll, _p]),
     "rs_scatter_interp_local": (_c_int, [_p, _c_ll, _p, _c_int, _p, _c_int, _c_ll, _c_ll, _p, _c_ll, _p]),
+    "rs_uniform": (_c_int, [ctypes.c_ulonglong, ctypes.c_ulonglong, _c_ll, _p, _p]),
+    "rs_hadamard_init": (_c_int, [_p, _c_ll, _c_int, _c_double, _p, _p]),
+    "rs_fwht_rows": (_c_int, [_p, _c_ll, _c_int, _c_double, _p, _p]),
+    "rs_kahan": (_c_int, [_p, _c_ll, _c_int, _p, _c_double, _p]),
+    "rs_chan": (_c_int, [_p, _c_ll, _c_int, _p]),
+    "rs_axpy_cast": (_c_int, [_p, _p, _c_double, _c_ll, _p, _p, _p]),
 }
 
 ABI_VERSION = 2

@@ -261,4 +261,27 @@ int rs_scatter_interp_local(const double* T, long long ldt, const int64_t* perm,
   return rs::launch_scatter_interp_local(T, ldt, perm, k, loc, r, lo, hi, W, ldw, S(stream));
 }
 
+int rs_uniform(unsigned long long seed, unsigned long long stream_id, long long n, double* out, void* stream) {
+  return rs::launch_uniform(seed, stream_id, n, out, S(stream));
+}
+
+int rs_hadamard_init(double* x, long long ld, int n, double c, const double* rowscale, void* stream) {
+  return rs::launch_hadamard_init(x, ld, n, c, rowscale, S(stream));
+}
+
+int rs_fwht_rows(double* x, long long ld, int n, double c, const double* rowscale, void* stream) {
+  return rs::launch_fwht_rows(x, ld, n, c, rowscale, S(stream));
+}
+
+int rs_kahan(double* a, long long ld, int n, const double* rowpow, double negphi, void* stream) {
+  return rs::launch_kahan(a, ld, n, rowpow, negphi, S(stream));
+}
+
+int rs_chan(double* a, long long ld, int n, void* stream) { return rs::launch_chan(a, ld, n, S(stream)); }
+
+int rs_axpy_cast(const double* x, const double* y, double beta, long long n, double* out64, float* out32,
+                 void* stream) {
+  return rs::launch_axpy_cast(x, y, beta, n, out64, out32, S(stream));
+}
+
 }  // extern "C"

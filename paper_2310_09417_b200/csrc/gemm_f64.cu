@@ -375,6 +375,7 @@ int launch_dgemm(const DGemmParams& p, bool a_col, int kc, cudaStream_t st) {
   if (p.mode != RS_GEMM_PLAIN && p.mode != RS_GEMM_FOLD && p.mode != RS_GEMM_CHAIN) return RS_ERR_ARG;
   if (p.mode != RS_GEMM_PLAIN && p.Cin == nullptr) return RS_ERR_ARG;
   if (kc <= 0) kc = gemm_chunk(p.K);
+  if (kc >= p.K) kc = std::max(32, (p.K + 31) / 32 * 32);  // one chunk: any kc >= K means the same
   if (kc % 32 != 0) return RS_ERR_ARG;
   if (p.mode == RS_GEMM_CHAIN && kc < p.K) return RS_ERR_ARG;  // a chain continues inside one chunk
   if (p.M == 0 || p.N == 0) return RS_OK;

@@ -94,6 +94,14 @@ int launch_gather2d(const double* src, long long rs_, long long cs_, const int64
 size_t gaussian_workspace_bytes(long long N);
 int launch_gaussian(uint64_t seed, uint64_t stream, long long N, double scale, double* out, void* ws,
                     size_t ws_bytes, int* status_dev, cudaStream_t st);
+// Input generators (gen.cu)
+int launch_uniform(uint64_t k0, uint64_t k1, long long n, double* out, cudaStream_t st);
+int launch_hadamard_init(double* x, long long ld, int n, double c, const double* rowscale, cudaStream_t st);
+int launch_fwht_rows(double* x, long long ld, int n, double c, const double* rowscale, cudaStream_t st);
+int launch_kahan(double* a, long long ld, int n, const double* rowpow, double negphi, cudaStream_t st);
+int launch_chan(double* a, long long ld, int n, cudaStream_t st);
+int launch_axpy_cast(const double* x, const double* y, double beta, long long n, double* out64, float* out32,
+                     cudaStream_t st);
 int launch_transpose(const double* src, long long lds, int rows, int cols, double* dst, long long ldd,
                      cudaStream_t st);
 

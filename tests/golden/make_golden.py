@@ -127,6 +127,11 @@ def main():
     adaptive("adapt_cfg2_n2000", np.ascontiguousarray(a.T), 64, 1e-8, 0, keep_w=False,
              gen_seed=0, a_sum=a.sum())
 
+    # max_rank below the block size: the first block is still absorbed whole
+    a, _ = rs.gen_fast_decay(120, 100, 1e-12, rs.RngStream(90))
+    adaptive("adapt_maxrank0", a, 16, 1e-30, 91, max_rank=0, a=a)
+    adaptive("adapt_maxrank15", a, 16, 1e-30, 92, max_rank=15, a=a)
+
     # ---- two-sided / CUR ---------------------------------------------------
     a = exact(80, 60, 20, 49)
     r = rs.two_sided_id(a, 20, spec(60), rs.RngStream(50))
@@ -188,6 +193,11 @@ def main():
             trace=np.array([[rec.k, rec.e_schur] for rec in res.trace]))
 
     path = os.path.join(OUT, "reference_golden.npz")
+    _save(cases, path)
+    configs()
+
+
+def _save(cases, path):
     flat = {}
     for name, arrays in cases.items():
         for key, val in arrays.items():
@@ -196,5 +206,71 @@ def main():
     print(f"wrote {len(cases)} cases, {os.path.getsize(path) / 1e6:.2f} MB -> {path}")
 
 
+def configs():
+    """BASELINE.json configs at checkable sizes, from the reference itself
+    (tests/test_gpu_configs.py): cfg1 at its full size, cfg4's Kahan matrix at
+    4096 with k = 512 (+ the CPQR comparator), cfg3's recipe at 4096 x 2048,
+    cfg5's device generator at 8192 (the oracle's numpy restatement of the
+    randomized-Hadamard construction, bit-identical to the device one)."""
+    sys.path.insert(0, REF)
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(OUT)), "oracle"))
+    import randskel as rs
+    import randskel_oracle as orc
+    from randskel.skeleton import _column_skeletons_from_rows
+
+    cases = {}
+
+    def put(name, **arrays):
+        cases[name] = arrays
+
+    # cfg1: column ID of the 4096^2 fast-decay matrix, k = 256 (BASELINE configs[0])
+    a, _ = rs.gen_fast_decay(4096, 4096, 1e-16, rs.RngStream(0).child(1 << 41))
+    c = rs.column_id(a, 256, rs.SketchSpec("gaussian", 4096, 256), rs.RngStream(0))
+    put("cfg1_full", col_idx=c.col_idx, x_sum=c.x.sum(), x_sq=(c.x ** 2).sum(), x_head=c.x[:, :16].copy(),
+        a_sum=a.sum(), resid=np.linalg.norm(a - a[:, c.col_idx] @ c.x) / np.linalg.norm(a))
+    del a, c
+
+    # cfg4: Kahan (zeta 0.99) at 4096, k = 512: LUPP vs CPQR skeletons (pivot robustness)
+    a = rs.gen_kahan(4096, 0.99)
+    sp = rs.SketchSpec("gaussian", 4096, 512)
+    c = rs.column_id(a, 512, sp, rs.RngStream(0))
+    r = rs.rand_lupp(a, 512, sp, rs.RngStream(0))
+    q = rs.rand_cpqr(a, 512, sp, rs.RngStream(0))
+    put("cfg4_kahan4096", col_idx=c.col_idx, x_sum=c.x.sum(), x_sq=(c.x ** 2).sum(), row_idx=r.row_idx,
+        w_sum=r.w.sum(), w_sq=(r.w ** 2).sum(), stable_err=rs.stable_row_id_error(a, r),
+        cpqr_row_idx=q.row_idx, cpqr_stable_err=rs.stable_row_id_error(a, q),
+        col_resid=np.linalg.norm(a - a[:, c.col_idx] @ c.x) / np.linalg.norm(a))
+    del a, c, r, q
+
+    # cfg3 recipe at 4096 x 2048 (fp32 input, the reference upcasts): adaptive CUR
+    a32 = orc.cfg3_test_matrix(4096, 2048)
+    a = a32.astype(np.float64)
+    tau = 1e-5 * np.linalg.norm(a)
+    res = rs.rand_lupp_adaptive(a, 64, tau, rs.SketchSpec("gaussian", 2048, 64), rs.RngStream(0))
+    k = res.rank
+    col_idx, _ = _column_skeletons_from_rows(a, res.row_idx, k)
+    cmat = a[:, col_idx]
+    rows = a[res.row_idx]
+    u_mid = rs.pinv_apply(cmat, rs.pinv_apply(rows.T, a.T).T)   # skeleton.py:639-646 with k = rank
+    put("cfg3_cur4096", a32_sum=a.sum(), a32_head=a32[:4, :64].copy(), tau=tau, rank=k, row_idx=res.row_idx, col_idx=col_idx, u_mid=u_mid,
+        status=res.status, trace=np.array([[rec.k, rec.e_schur] for rec in res.trace]),
+        resid=np.linalg.norm(a - cmat @ u_mid @ rows) / np.linalg.norm(a))
+    del a, a32, cmat, rows
+
+    # cfg5 recipe at 8192: randomized-Hadamard fast decay, adaptive column ID b = 64, tau = 1e-8
+    n = 8192
+    gen = rs.RngStream(0).child(1 << 41)
+    a, _ = orc.gen_fast_decay_hadamard(n, 1e-16, gen.seed, gen.stream)
+    res = rs.rand_lupp_adaptive(np.ascontiguousarray(a.T), 64, 1e-8, rs.SketchSpec("gaussian", n, 64),
+                                rs.RngStream(0))
+    put("cfg5_hadamard8192", a_sum=a.sum(), a_sq=(a ** 2).sum(), a_head=a[:4, :64].copy(), rank=res.rank,
+        row_idx=res.row_idx, status=res.status, trace=np.array([[rec.k, rec.e_schur] for rec in res.trace]))
+    path = os.path.join(OUT, "config_golden.npz")
+    _save(cases, path)
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["--configs"]:
+        configs()
+    else:
+        main()

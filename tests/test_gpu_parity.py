@@ -222,7 +222,7 @@ def test_rank_deficient_raises(rs):
 # ---------------------------------------------------------- adaptive ID ----
 ADAPTIVE_CASES = ["adapt_fd200", "adapt_fd150_s0", "adapt_fd150_s1", "adapt_fd150_s2",
                   "adapt_notconv", "adapt_exhausted", "adapt_wide", "adapt_b25",
-                  "adapt_fullwidth", "adapt_single"]
+                  "adapt_fullwidth", "adapt_single", "adapt_maxrank0", "adapt_maxrank15"]
 
 
 @pytest.mark.parametrize("case", ADAPTIVE_CASES)

@@ -98,7 +98,8 @@ def test_fast_decay_generator_matches_reference():
 
 
 ADAPTIVE = ["adapt_fd200", "adapt_fd150_s0", "adapt_fd150_s1", "adapt_fd150_s2", "adapt_notconv",
-            "adapt_exhausted", "adapt_wide", "adapt_b25", "adapt_fullwidth", "adapt_single"]
+            "adapt_exhausted", "adapt_wide", "adapt_b25", "adapt_fullwidth", "adapt_single", "adapt_maxrank0",
+            "adapt_maxrank15"]
 
 
 @pytest.mark.parametrize("case", ADAPTIVE)
