@@ -54,7 +54,9 @@ def common_prefix(a, b):
 def test_cfg1_full_size(rs):
     g = cgold("cfg1_full")
     a, _ = rs.gen_fast_decay(4096, 4096, 1e-16, rs.RngStream(0).child(1 << 41))
-    assert a.sum() == float(g["a_sum"])  # same host generator, same bits
+    # same generator; the host LAPACK QR of the Haar bases may differ in the last bits
+    # between CPUs (the fixture was frozen on another host), hence no bitwise check
+    assert abs(a.sum() - float(g["a_sum"])) <= 1e-12 * np.abs(a).sum()
     c = rs.column_id(a, 256, rs.SketchSpec("gaussian", 4096, 256), rs.RngStream(0))
     assert np.array_equal(c.col_idx, g["col_idx"])
     assert np.array_equal(c.x[:, c.col_idx], np.eye(256))
