@@ -254,6 +254,35 @@ int rs_scatter_rows(const double* src, long long lds, const int64_t* idx, int nr
 int rs_scatter_interp_local(const double* T, long long ldt, const int64_t* perm, int k, const int64_t* loc, int r,
                             long long lo, long long hi, double* W, long long ldw, void* stream);
 
+/* ---- Ozaki-scheme sketch GEMM on the int8 tensor cores (tcgen05 kind::i8,
+ * TMEM accumulators; ozaki.cu).  Y = A Omega with A and Omega cut into
+ * signed 7-bit digit planes per (row, K-chunk) / (column, K-chunk); the plane
+ * products are exact int32 sums, combined in fp64 in a fixed order and the
+ * chunk sums folded in chunk order: the same determinism contract as
+ * rs_dgemm.  Replaces the OpenBLAS dgemm of `GaussianSketch.apply`
+ * (sketching.py:122-128) on the adaptive loop's sketch (skeleton.py:293-295). */
+
+/* K-chunk length (multiple of 128, <= 16384) of the Ozaki sketch for K. */
+int rs_oz_chunk(long long K);
+
+/* Bytes of the digit planes of a rows x K operand with S planes, in tiles of
+ * tile_rows (128 for A, 64 for Omega^T). */
+size_t rs_oz_digits_bytes(int rows, long long K, int S, int tile_rows);
+
+/* Digit planes and exponents of X (rows x K; fp32 if fp32 else fp64; X[i, k]
+ * at X[i*ld + k] or, colmajor, X[k*ld + i]) for k in [k0, k1), k0 and k1
+ * multiples of kc or k1 = K.  expo: rows x ceil(K / kc) int32.  For Omega
+ * (K x N row-major) pass colmajor = 1, rows = N, ld = its row stride. */
+int rs_oz_slice(const void* X, int fp32, long long ld, int colmajor, int rows, int K, int k0, int k1, int kc, int S,
+                int tile_rows, int8_t* digits, int* expo, void* stream);
+
+/* C (M x N row-major) = alpha * A Omega + beta * Cin (mode RS_GEMM_PLAIN) or
+ * Cin + A Omega with the chunk sums folded onto Cin (RS_GEMM_FOLD), from the
+ * sliced operands (SA, SB <= 8 planes).  workspace: rs_workspace_bytes. */
+int rs_oz_gemm(int M, int N, int K, int kc, int mode, double alpha, const int8_t* a_digits, const int* a_expo,
+               int SA, const int8_t* b_digits, const int* b_expo, int SB, double beta, const double* Cin,
+               long long ldcin, double* C, long long ldc, void* workspace, void* stream);
+
 /* ---- input generators (input generation, not the
  * skeleton path).  Each is restated in numpy by the oracle with the same
  * rounding, so the device matrix equals the host one bit for bit. ------- */

@@ -62,6 +62,12 @@ SIGNATURES = {
                                _p, _p, _p, _c_int, _p]),
     "rs_scatter_rows": (_c_int, [_p, _c_ll, _p, _c_int, _c_int, _p, _c_ll, _p]),
     "rs_scatter_interp_local": (_c_int, [_p, _c_ll, _p, _c_int, _p, _c_int, _c_ll, _c_ll, _p, _c_ll, _p]),
+    "rs_oz_chunk": (_c_int, [_c_ll]),
+    "rs_oz_digits_bytes": (ctypes.c_size_t, [_c_int, _c_ll, _c_int, _c_int]),
+    "rs_oz_slice": (_c_int, [_p, _c_int, _c_ll, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _p,
+                             _p, _p]),
+    "rs_oz_gemm": (_c_int, [_c_int, _c_int, _c_int, _c_int, _c_int, _c_double, _p, _p, _c_int, _p, _p, _c_int,
+                            _c_double, _p, _c_ll, _p, _c_ll, _p, _p]),
     "rs_uniform": (_c_int, [ctypes.c_ulonglong, ctypes.c_ulonglong, _c_ll, _p, _p]),
     "rs_hadamard_init": (_c_int, [_p, _c_ll, _c_int, _c_double, _p, _p]),
     "rs_fwht_rows": (_c_int, [_p, _c_ll, _c_int, _c_double, _p, _p]),

@@ -261,6 +261,26 @@ int rs_scatter_interp_local(const double* T, long long ldt, const int64_t* perm,
   return rs::launch_scatter_interp_local(T, ldt, perm, k, loc, r, lo, hi, W, ldw, S(stream));
 }
 
+int rs_oz_chunk(long long K) { return rs::oz_chunk(K); }
+
+size_t rs_oz_digits_bytes(int rows, long long K, int S, int tile_rows) {
+  return rs::oz_digits_bytes(rows, K, S, tile_rows);
+}
+
+int rs_oz_slice(const void* X, int fp32, long long ld, int colmajor, int rows, int K, int k0, int k1, int kc,
+                int planes, int tile_rows, int8_t* digits, int* expo, void* stream) {
+  return rs::launch_oz_slice(X, fp32, ld, colmajor, rows, K, k0, k1, kc, planes, tile_rows, digits, expo, S(stream));
+}
+
+int rs_oz_gemm(int M, int N, int K, int kc, int mode, double alpha, const int8_t* a_digits, const int* a_expo,
+               int SA, const int8_t* b_digits, const int* b_expo, int SB, double beta, const double* Cin,
+               long long ldcin, double* C, long long ldc, void* workspace, void* stream) {
+  rs::DGemmParams g = gemm_params(0, 0, 0, 0.0, nullptr, 0, nullptr, nullptr, 0, nullptr, 0.0, nullptr, 0, nullptr,
+                                  nullptr, 0, RS_GEMM_PLAIN, workspace);
+  return rs::launch_oz_gemm(M, N, K, kc, mode, alpha, a_digits, a_expo, SA, b_digits, b_expo, SB, beta, Cin, ldcin,
+                            C, ldc, g.slots, g.tickets, g.nslots, S(stream));
+}
+
 int rs_uniform(unsigned long long seed, unsigned long long stream_id, long long n, double* out, void* stream) {
   return rs::launch_uniform(seed, stream_id, n, out, S(stream));
 }

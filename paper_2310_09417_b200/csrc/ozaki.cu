@@ -1,0 +1,520 @@
+// fp64 / fp32 sketch GEMM on the 5th-generation tensor cores: the Ozaki
+// scheme on tcgen05.mma kind::i8 with TMEM int32 accumulators.
+//
+//   Y = A Omega,  A: M x K (fp64 or fp32, either layout),  Omega: K x N fp64.
+//
+// Every row i of A and every column j of Omega is cut, per K-chunk c, into
+// signed 7-bit digits relative to a power of two above its largest entry in
+// the chunk:
+//     A[i, k] = 2^{e_ic} sum_{s<SA} a_s[i, k] 2^{-7(s+1)} + (|rem| < 2^{e_ic - 7 SA})
+// (exact: scaling by 2^-e and the digit extraction y <- 128 y - trunc(128 y)
+// are exact in fp64).  The products of digit planes are exact integers,
+// accumulated exactly in int32 by the tensor cores, one TMEM accumulator per
+// digit sum g = s + t (pairs with g >= G = max(SA, SB) are dropped: their
+// weight is below 2^{-7(G+2)} of the row x column scale):
+//     Y_chunk[i, j] = 2^{e_ic + f_jc} sum_{g<G} 2^{-7(g+2)} C_g[i, j],
+//     C_g = sum_{s+t=g} a_s b_t^T   (int32, |C_g| <= kc 127^2 min(SA, SB) < 2^31).
+// The G terms are converted and added in fp64 in a fixed order (smallest
+// first), then the chunk sums are folded in chunk order exactly as the DMMA
+// GEMM does (gemm_f64.cu).  Every quantity depends on row i, on Omega and on
+// K alone, so the determinism contract of rs_dgemm holds here too: a row's
+// bits do not depend on M, on the tile it lands in or on the device count.
+//
+// A is sliced ONCE per skeleton call (rs_oz_slice; it is multiplied by a
+// fresh Omega every block) into digit planes laid out in HBM as the exact
+// shared-memory image the MMA reads: 128-row x 128-byte tiles, K-major,
+// 128-byte swizzled (16-byte chunk c of row r at r*128 + ((c ^ r%8) * 16)),
+// tile order [row tile][k-block][digit plane].  So each pipeline stage is one
+// contiguous 16 KB bulk copy (cp.async.bulk, the TMA engine's linear mode)
+// and no tensor map is needed.  At SA = 8 the planes take 8 bytes per entry,
+// the same HBM traffic as the fp64 matrix, while the int8 tensor pipe does
+// the 36 plane products (4.5 POP/s dense) -- the sketch becomes HBM-bound
+// instead of bound by the 37 TF/s DMMA pipe.
+//
+// Kernel (one CTA per SM, persistent over (tile, chunk) units):
+//   warp 0  producer: bulk copies of the Omega planes of a k-block (one copy
+//           of SB x 8 KB) and of the A planes (one 16 KB stage each);
+//   warp 1  TMEM owner + MMA issuer (one elected lane): for every A plane s
+//           and Omega plane t with s + t < G, 4 x tcgen05.mma m128n64k32
+//           into accumulator g = s + t; tcgen05.commit releases the stages;
+//   warps 2-5 epilogue: tcgen05.ld of the G int32 accumulators (one TMEM
+//           lane = one output row per thread), fp64 combination, chunk slot
+//           or direct store, last-arriving unit folds the chunk slots.
+#include <algorithm>
+#include <cstdint>
+
+#include "common.cuh"
+#include "rskel_internal.h"
+
+namespace rs {
+
+namespace {
+
+constexpr int OZ_BM = 128, OZ_BN = 64, OZ_BK = 128;  // rows of A tile, rows of Omega^T tile, k bytes
+constexpr int OZ_ATILE = OZ_BM * OZ_BK;               // 16 KB
+constexpr int OZ_BTILE = OZ_BN * OZ_BK;               // 8 KB
+constexpr int OZ_MAXS = 8;
+constexpr int OZ_NA = 4;                              // A plane stages
+constexpr int OZ_NB = 2;                              // Omega k-block stages (SB planes each)
+constexpr int OZ_THREADS = 192;
+constexpr size_t OZ_SMEM = 1024 + (size_t)OZ_NA * OZ_ATILE + (size_t)OZ_NB * OZ_MAXS * OZ_BTILE + 256;
+
+// ------------------------------------------------------------------ PTX ----
+RS_DEV uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+RS_DEV void mb_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(b)), "r"(n));
+}
+RS_DEV void mb_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+RS_DEV void mb_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(b)) : "memory");
+}
+RS_DEV void mb_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "W_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W_%=;\n\t}\n" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+RS_DEV void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(bar))
+      : "memory");
+}
+RS_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+RS_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+RS_DEV void tc_commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(b))
+               : "memory");
+}
+RS_DEV void tc_mma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+RS_DEV void tc_ld16(uint32_t taddr, int (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+RS_DEV void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
+
+// K-major, 128-byte swizzled operand tile: rows of 128 bytes, 8-row groups
+// 1024 bytes apart (SBO), version 1 (sm_100), layout SWIZZLE_128B.
+RS_DEV uint64_t smem_desc(const void* p) {
+  const uint64_t addr = su32(p);
+  return ((addr >> 4) & 0x3FFFull) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
+}
+
+// kind::i8, signed x signed -> s32, both K-major, M = 128, N = 64
+constexpr uint32_t OZ_IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((OZ_BN >> 3) << 17) | ((OZ_BM >> 4) << 24);
+
+// ---------------------------------------------------------------- slicing ----
+template <typename T>
+RS_DEV double ld_elem(const T* X, long long ld, bool colmajor, long long i, long long k) {
+  return (double)(colmajor ? X[k * ld + i] : X[i * ld + k]);
+}
+
+// expo[i * nch + c] = e with max_{k in chunk c} |X[i, k]| < 2^e (frexp), for the
+// chunks c0 <= c < c1.  Column-major: one thread per row (coalesced along i);
+// row-major: one warp per row.
+template <typename T, bool COLMAJOR>
+__global__ void oz_expo_kernel(const T* __restrict__ X, long long ld, int rows, int K, int kc, int c0, int nch,
+                               int* __restrict__ expo) {
+  const int c = c0 + blockIdx.y;
+  const int k0 = c * kc, k1 = min(K, k0 + kc);
+  double m = 0.0;
+  long long i;
+  if constexpr (COLMAJOR) {
+    i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= rows) return;
+    for (int k = k0; k < k1; ++k) m = fmax(m, fabs((double)X[(long long)k * ld + i]));
+  } else {
+    const int lane = threadIdx.x & 31;
+    i = (long long)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    if (i >= rows) return;
+    for (int k = k0 + lane; k < k1; k += 32) m = fmax(m, fabs((double)X[i * ld + k]));
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+    if (lane != 0) return;
+  }
+  int e = 0;
+  if (m > 0.0) frexp(m, &e);
+  expo[i * nch + c] = e;
+}
+
+// Digit planes of rows [0, rows_pad) x k in [k0, k1_pad) (k0 a multiple of
+// 128, k1_pad = k1 rounded up to 128): thread (row, 16-k group); rows >= rows
+// and k >= K give zero digits (the tile padding).
+template <typename T, bool COLMAJOR>
+__global__ void oz_slice_kernel(const T* __restrict__ X, long long ld, int rows, int rows_pad, int K, int k0,
+                                int k1_pad, int kc, int nch, int S, int tile_rows, int KB,
+                                const int* __restrict__ expo, int8_t* __restrict__ dig) {
+  int i, q;
+  if constexpr (COLMAJOR) {  // lanes along rows: each k reads 32 consecutive rows
+    i = blockIdx.x * 32 + threadIdx.x;
+    q = blockIdx.y * blockDim.y + threadIdx.y;
+  } else {  // lanes along k groups: each row segment is read contiguously
+    i = blockIdx.x * blockDim.y + threadIdx.y;
+    q = blockIdx.y * 32 + threadIdx.x;
+  }
+  const int k = k0 + q * 16;
+  if (i >= rows_pad || k >= k1_pad) return;
+  double y[16];
+  const int e = (i < rows && k < K) ? expo[(long long)i * nch + k / kc] : 0;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int kk = k + j;
+    const double x = (i < rows && kk < K) ? ld_elem(X, ld, COLMAJOR, i, kk) : 0.0;
+    y[j] = ldexp(x, -e);  // |y| < 1, exact
+  }
+  const int tile = i / tile_rows, r = i % tile_rows, kb = k / OZ_BK, c16 = (k % OZ_BK) / 16;
+  const size_t tile_bytes = (size_t)tile_rows * OZ_BK;
+  int8_t* base = dig + ((size_t)tile * KB + kb) * S * tile_bytes + (size_t)(r >> 3) * 1024 + (r & 7) * 128 +
+                 ((c16 ^ (r & 7)) * 16);
+  for (int s = 0; s < S; ++s) {
+    uint32_t w[4];
+#pragma unroll
+    for (int j4 = 0; j4 < 4; ++j4) {
+      uint32_t packed = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int j = j4 * 4 + b;
+        const double z = y[j] * 128.0;  // exact
+        const double d = trunc(z);      // |d| <= 127
+        y[j] = z - d;                   // exact
+        packed |= (uint32_t)(uint8_t)(int8_t)(int)d << (8 * b);
+      }
+      w[j4] = packed;
+    }
+    *reinterpret_cast<uint4*>(base + (size_t)s * tile_bytes) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+// ------------------------------------------------------------------- GEMM ----
+struct OzParams {
+  int M, N, K;
+  const int8_t* adig;
+  const int* aexp;
+  int SA;
+  const int8_t* bdig;
+  const int* bexp;
+  int SB;
+  int G;             // accumulators (digit sums 0..G-1)
+  int KB, kbc, nch;  // k-blocks of K, k-blocks per chunk, chunks
+  int tiles_n, tile0, units;
+  int mode;
+  double alpha, beta;
+  const double* Cin;
+  long long ldcin;
+  double* C;
+  long long ldc;
+  double* slots;
+  int* tickets;
+};
+
+__global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(OzParams p) {
+  extern __shared__ __align__(1024) uint8_t oz_smem[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_smem) + 1023) & ~uintptr_t(1023));
+  uint8_t* sa = sm;                                      // OZ_NA x 16 KB
+  uint8_t* sb = sm + OZ_NA * OZ_ATILE;                   // OZ_NB x SB x 8 KB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sb + OZ_NB * OZ_MAXS * OZ_BTILE);
+  uint64_t* full_a = bars;
+  uint64_t* empty_a = bars + OZ_NA;
+  uint64_t* full_b = bars + 2 * OZ_NA;
+  uint64_t* empty_b = full_b + OZ_NB;
+  uint64_t* tm_full = empty_b + OZ_NB;
+  uint64_t* tm_empty = tm_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tm_empty + 1);
+  int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < OZ_NA; ++i) { mb_init(full_a + i, 1); mb_init(empty_a + i, 1); }
+    for (int i = 0; i < OZ_NB; ++i) { mb_init(full_b + i, 1); mb_init(empty_b + i, 1); }
+    mb_init(tm_full, 1);
+    mb_init(tm_empty, 128);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(su32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer --
+    if (lane == 0) {
+      int ai = 0, bi = 0;
+      uint32_t aph = 0, bph = 0;
+      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+        const int lt = u / p.nch, ch = u - lt * p.nch, tile = p.tile0 + lt;
+        const int tm = tile / p.tiles_n, tn = tile - tm * p.tiles_n;
+        const int kb0 = ch * p.kbc, kb1 = min(p.KB, kb0 + p.kbc);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mb_wait(empty_b + bi, bph ^ 1);
+          mb_expect_tx(full_b + bi, (uint32_t)(p.SB * OZ_BTILE));
+          bulk_load(sb + (size_t)bi * OZ_MAXS * OZ_BTILE,
+                    p.bdig + ((size_t)tn * p.KB + kb) * p.SB * OZ_BTILE, p.SB * OZ_BTILE, full_b + bi);
+          if (++bi == OZ_NB) { bi = 0; bph ^= 1; }
+          const int8_t* asrc = p.adig + ((size_t)tm * p.KB + kb) * p.SA * OZ_ATILE;
+          for (int s = 0; s < p.SA; ++s) {
+            mb_wait(empty_a + ai, aph ^ 1);
+            mb_expect_tx(full_a + ai, OZ_ATILE);
+            bulk_load(sa + (size_t)ai * OZ_ATILE, asrc + (size_t)s * OZ_ATILE, OZ_ATILE, full_a + ai);
+            if (++ai == OZ_NA) { ai = 0; aph ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------- MMA issuer --
+    int ai = 0, bi = 0;
+    uint32_t aph = 0, bph = 0, tph = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+      const int lt = u / p.nch, ch = u - lt * p.nch;
+      const int kb0 = ch * p.kbc, kb1 = min(p.KB, kb0 + p.kbc);
+      mb_wait(tm_empty, tph ^ 1);  // the epilogue has drained the previous unit
+      tph ^= 1;
+      tc_fence_after();
+      uint32_t inited = 0;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mb_wait(full_b + bi, bph);
+        const uint8_t* bst = sb + (size_t)bi * OZ_MAXS * OZ_BTILE;
+        for (int s = 0; s < p.SA; ++s) {
+          mb_wait(full_a + ai, aph);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint64_t da = smem_desc(sa + (size_t)ai * OZ_ATILE);
+            const int tmax = min(p.SB, p.G - s);
+            for (int t = 0; t < tmax; ++t) {
+              const int g = s + t;
+              const uint64_t db = smem_desc(bst + (size_t)t * OZ_BTILE);
+              const uint32_t d = tmem + (uint32_t)(g * OZ_BN);
+#pragma unroll
+              for (int kk = 0; kk < OZ_BK / 32; ++kk) {
+                const uint32_t acc = (kk > 0 || ((inited >> g) & 1u)) ? 1u : 0u;
+                tc_mma_i8(d, da + 2 * kk, db + 2 * kk, OZ_IDESC, acc);
+              }
+              inited |= 1u << g;
+            }
+            tc_commit(empty_a + ai);  // the A stage is free once these MMAs have read it
+          }
+          __syncwarp();
+          if (++ai == OZ_NA) { ai = 0; aph ^= 1; }
+        }
+        if (lane == 0) tc_commit(empty_b + bi);
+        __syncwarp();
+        if (++bi == OZ_NB) { bi = 0; bph ^= 1; }
+      }
+      if (lane == 0) tc_commit(tm_full);
+      __syncwarp();
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue --
+    const int q = warp & 3;              // TMEM lane quadrant this warp may read
+    const int r = q * 32 + lane;         // output row within the tile
+    const int et = threadIdx.x - 64;     // 0..127
+    uint32_t tph = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+      const int lt = u / p.nch, ch = u - lt * p.nch, tile = p.tile0 + lt;
+      const int tm = tile / p.tiles_n, tn = tile - tm * p.tiles_n;
+      const int row = tm * OZ_BM + r;
+      const int ea = row < p.M ? p.aexp[(long long)row * p.nch + ch] : 0;
+      mb_wait(tm_full, tph);
+      tph ^= 1;
+      tc_fence_after();
+      double* slot = p.slots + (size_t)u * (OZ_BM * OZ_BN);
+      for (int cb = 0; cb < OZ_BN / 16; ++cb) {
+        double v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = 0.0;
+        for (int g = p.G - 1; g >= 0; --g) {  // smallest weight first
+          int c[16];
+          tc_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(g * OZ_BN + cb * 16), c);
+          const int sh = -7 * (g + 2);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] += ldexp((double)c[j], sh);
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int col = tn * OZ_BN + cb * 16 + j;
+          const int eb = col < p.N ? p.bexp[(long long)col * p.nch + ch] : 0;
+          v[j] = ldexp(v[j], ea + eb);
+        }
+        if (p.nch == 1) {
+          if (row < p.M) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int col = tn * OZ_BN + cb * 16 + j;
+              if (col >= p.N) continue;
+              double out = v[j];
+              if (p.mode == RS_GEMM_FOLD) out = p.Cin[(long long)row * p.ldcin + col] + v[j];
+              else if (p.beta != 0.0) out = fma(p.alpha, v[j], p.beta * p.Cin[(long long)row * p.ldcin + col]);
+              else out = p.alpha * v[j];
+              p.C[(long long)row * p.ldc + col] = out;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) __stcg(slot + (size_t)(cb * 16 + j) * OZ_BM + r, v[j]);
+        }
+      }
+      tc_fence_before();
+      mb_arrive(tm_empty);  // TMEM may be overwritten by the next unit
+      if (p.nch == 1) continue;
+      __threadfence();
+      named_sync(1, 128);
+      if (et == 0) *s_last = atomicAdd(p.tickets + lt, 1) == p.nch - 1;
+      named_sync(1, 128);
+      if (!*s_last) continue;
+      __threadfence();
+      // last chunk of the tile to arrive: fold the chunk partials in chunk order
+      const double* base = p.slots + (size_t)lt * p.nch * (OZ_BM * OZ_BN) + r;
+      for (int cb = 0; cb < OZ_BN / 16; ++cb) {
+        double acc[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[j] = __ldcg(base + (size_t)(cb * 16 + j) * OZ_BM);
+        if (p.mode == RS_GEMM_FOLD && row < p.M) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int col = tn * OZ_BN + cb * 16 + j;
+            if (col < p.N) acc[j] = p.Cin[(long long)row * p.ldcin + col] + acc[j];
+          }
+        }
+        for (int c = 1; c < p.nch; ++c) {
+          const double* src = base + (size_t)c * (OZ_BM * OZ_BN);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc[j] += __ldcg(src + (size_t)(cb * 16 + j) * OZ_BM);
+        }
+        if (row < p.M) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int col = tn * OZ_BN + cb * 16 + j;
+            if (col >= p.N) continue;
+            double out = acc[j];
+            if (p.mode == RS_GEMM_PLAIN)
+              out = p.beta != 0.0 ? fma(p.alpha, acc[j], p.beta * p.Cin[(long long)row * p.ldcin + col])
+                                  : p.alpha * acc[j];
+            p.C[(long long)row * p.ldc + col] = out;
+          }
+        }
+      }
+      named_sync(1, 128);
+      if (et == 0) p.tickets[lt] = 0;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+}
+
+int ok_or_cuda() { return cudaGetLastError() == cudaSuccess ? RS_OK : RS_ERR_CUDA; }
+
+}  // namespace
+
+int oz_chunk(long long K) {
+  long long kc = (K + 7) / 8;
+  kc = (kc + OZ_BK - 1) / OZ_BK * OZ_BK;
+  return (int)std::min<long long>(16384, std::max<long long>(1024, kc));
+}
+
+size_t oz_digits_bytes(int rows, long long K, int S, int tile_rows) {
+  const long long tiles = (rows + tile_rows - 1) / tile_rows;
+  const long long KB = (K + OZ_BK - 1) / OZ_BK;
+  return (size_t)tiles * KB * S * tile_rows * OZ_BK;
+}
+
+int launch_oz_slice(const void* X, int fp32, long long ld, int colmajor, int rows, int K, int k0, int k1, int kc,
+                    int S, int tile_rows, int8_t* dig, int* expo, cudaStream_t st) {
+  if (rows < 0 || K < 0 || k0 < 0 || k1 > K || k0 > k1 || kc <= 0 || kc % OZ_BK || k0 % kc || S < 1 ||
+      S > OZ_MAXS || (tile_rows != OZ_BM && tile_rows != OZ_BN))
+    return RS_ERR_ARG;
+  if (rows == 0 || k0 == k1) return RS_OK;
+  const int nch = (K + kc - 1) / kc;
+  const int c0 = k0 / kc, c1 = (k1 + kc - 1) / kc;
+  const int KB = (K + OZ_BK - 1) / OZ_BK;
+  const int rows_pad = (rows + tile_rows - 1) / tile_rows * tile_rows;
+  const int k1_pad = k1 == K ? (K + OZ_BK - 1) / OZ_BK * OZ_BK : k1;
+  const int groups = (k1_pad - k0) / 16;
+  if (colmajor) {
+    dim3 ge((rows + 255) / 256, c1 - c0);
+    dim3 gs((rows_pad + 31) / 32, (groups + 7) / 8);
+    if (fp32) {
+      oz_expo_kernel<float, true><<<ge, 256, 0, st>>>((const float*)X, ld, rows, K, kc, c0, nch, expo);
+      oz_slice_kernel<float, true><<<gs, dim3(32, 8), 0, st>>>((const float*)X, ld, rows, rows_pad, K, k0, k1_pad,
+                                                               kc, nch, S, tile_rows, KB, expo, dig);
+    } else {
+      oz_expo_kernel<double, true><<<ge, 256, 0, st>>>((const double*)X, ld, rows, K, kc, c0, nch, expo);
+      oz_slice_kernel<double, true><<<gs, dim3(32, 8), 0, st>>>((const double*)X, ld, rows, rows_pad, K, k0,
+                                                                k1_pad, kc, nch, S, tile_rows, KB, expo, dig);
+    }
+  } else {
+    dim3 ge((rows + 7) / 8, c1 - c0);
+    dim3 gs((rows_pad + 7) / 8, (groups + 31) / 32);
+    if (fp32) {
+      oz_expo_kernel<float, false><<<ge, 256, 0, st>>>((const float*)X, ld, rows, K, kc, c0, nch, expo);
+      oz_slice_kernel<float, false><<<gs, dim3(32, 8), 0, st>>>((const float*)X, ld, rows, rows_pad, K, k0, k1_pad,
+                                                                kc, nch, S, tile_rows, KB, expo, dig);
+    } else {
+      oz_expo_kernel<double, false><<<ge, 256, 0, st>>>((const double*)X, ld, rows, K, kc, c0, nch, expo);
+      oz_slice_kernel<double, false><<<gs, dim3(32, 8), 0, st>>>((const double*)X, ld, rows, rows_pad, K, k0,
+                                                                 k1_pad, kc, nch, S, tile_rows, KB, expo, dig);
+    }
+  }
+  count_launch(2);
+  return ok_or_cuda();
+}
+
+int launch_oz_gemm(int M, int N, int K, int kc, int mode, double alpha, const int8_t* adig, const int* aexp, int SA,
+                   const int8_t* bdig, const int* bexp, int SB, double beta, const double* Cin, long long ldcin,
+                   double* C, long long ldc, double* slots, int* tickets, int nslots, cudaStream_t st) {
+  if (M < 0 || N < 0 || K < 0 || SA < 1 || SB < 1 || SA > OZ_MAXS || SB > OZ_MAXS || kc % OZ_BK || kc <= 0 ||
+      kc > 16384)
+    return RS_ERR_ARG;
+  if (mode != RS_GEMM_PLAIN && mode != RS_GEMM_FOLD) return RS_ERR_ARG;
+  if ((mode == RS_GEMM_FOLD || beta != 0.0) && Cin == nullptr) return RS_ERR_ARG;
+  if (M == 0 || N == 0) return RS_OK;
+  if (slots == nullptr || tickets == nullptr) return RS_ERR_ARG;
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  OzParams p{};
+  p.M = M; p.N = N; p.K = K;
+  p.adig = adig; p.aexp = aexp; p.SA = SA;
+  p.bdig = bdig; p.bexp = bexp; p.SB = SB;
+  p.G = std::max(SA, SB);
+  p.KB = (K + OZ_BK - 1) / OZ_BK;
+  p.kbc = kc / OZ_BK;
+  p.nch = std::max(1, (K + kc - 1) / kc);
+  p.tiles_n = (N + OZ_BN - 1) / OZ_BN;
+  p.mode = mode; p.alpha = alpha; p.beta = beta;
+  p.Cin = Cin; p.ldcin = ldcin; p.C = C; p.ldc = ldc;
+  p.slots = slots; p.tickets = tickets;
+  const long long tiles = (long long)p.tiles_n * ((M + OZ_BM - 1) / OZ_BM);
+  cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OZ_SMEM);
+  const long long per = p.nch == 1 ? tiles : std::max<long long>(1, nslots / p.nch);
+  const long long ngroups = (tiles + per - 1) / per;
+  for (long long gi = 0; gi < ngroups; ++gi) {
+    const long long t0 = tiles * gi / ngroups, t1 = tiles * (gi + 1) / ngroups;
+    p.tile0 = (int)t0;
+    p.units = (int)((t1 - t0) * p.nch);
+    oz_gemm_kernel<<<std::min(p.units, nsm), OZ_THREADS, OZ_SMEM, st>>>(p);
+    count_launch(1);
+  }
+  return ok_or_cuda();
+}
+
+}  // namespace rs

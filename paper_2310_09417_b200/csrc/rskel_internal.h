@@ -94,6 +94,14 @@ int launch_gather2d(const double* src, long long rs_, long long cs_, const int64
 size_t gaussian_workspace_bytes(long long N);
 int launch_gaussian(uint64_t seed, uint64_t stream, long long N, double scale, double* out, void* ws,
                     size_t ws_bytes, int* status_dev, cudaStream_t st);
+// Ozaki-scheme sketch GEMM on tcgen05 kind::i8 (ozaki.cu)
+int oz_chunk(long long K);
+size_t oz_digits_bytes(int rows, long long K, int S, int tile_rows);
+int launch_oz_slice(const void* X, int fp32, long long ld, int colmajor, int rows, int K, int k0, int k1, int kc,
+                    int S, int tile_rows, int8_t* dig, int* expo, cudaStream_t st);
+int launch_oz_gemm(int M, int N, int K, int kc, int mode, double alpha, const int8_t* adig, const int* aexp, int SA,
+                   const int8_t* bdig, const int* bexp, int SB, double beta, const double* Cin, long long ldcin,
+                   double* C, long long ldc, double* slots, int* tickets, int nslots, cudaStream_t st);
 // Input generators (gen.cu)
 int launch_uniform(uint64_t k0, uint64_t k1, long long n, double* out, cudaStream_t st);
 int launch_hadamard_init(double* x, long long ld, int n, double c, const double* rowscale, cudaStream_t st);
