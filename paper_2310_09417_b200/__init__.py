@@ -60,6 +60,7 @@ from .lu_state import (
 )
 from .cur import CurFactors, cur_decompose, cur_decompose_adaptive, pinv_apply, two_sided_id
 from .evaluate import row_id_error, stable_row_id_error
+from ._ozaki import set_sketch_engine, sketch_engine
 from .zoo import gen_chan, gen_fast_decay, gen_fast_decay_hadamard, gen_kahan, gen_nonneg_lowrank
 
 __version__ = "0.1.0"

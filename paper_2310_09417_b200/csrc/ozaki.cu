@@ -46,6 +46,10 @@
 #include "common.cuh"
 #include "rskel_internal.h"
 
+#ifndef OZ_DBG  // experiment switch for tools/oz_prof.py builds only (0 in the library)
+#define OZ_DBG 0
+#endif
+
 namespace rs {
 
 namespace {
@@ -54,10 +58,10 @@ constexpr int OZ_BM = 128, OZ_BN = 64, OZ_BK = 128;  // rows of A tile, rows of 
 constexpr int OZ_ATILE = OZ_BM * OZ_BK;               // 16 KB
 constexpr int OZ_BTILE = OZ_BN * OZ_BK;               // 8 KB
 constexpr int OZ_MAXS = 8;
-constexpr int OZ_NA = 4;                              // A plane stages
+constexpr int OZ_NA = 6;                              // A plane stages
 constexpr int OZ_NB = 2;                              // Omega k-block stages (SB planes each)
 constexpr int OZ_THREADS = 192;
-constexpr size_t OZ_SMEM = 1024 + (size_t)OZ_NA * OZ_ATILE + (size_t)OZ_NB * OZ_MAXS * OZ_BTILE + 256;
+constexpr size_t OZ_SMEM = 1024 + (size_t)OZ_NA * OZ_ATILE + (size_t)OZ_NB * OZ_MAXS * OZ_BTILE + 512;
 
 // ------------------------------------------------------------------ PTX ----
 RS_DEV uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -98,6 +102,14 @@ RS_DEV void tc_mma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
+RS_DEV void tc_ld16_async(uint32_t taddr, int* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+RS_DEV void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 RS_DEV void tc_ld16(uint32_t taddr, int (&v)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
@@ -105,6 +117,10 @@ RS_DEV void tc_ld16(uint32_t taddr, int (&v)[16]) {
         "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+// 2^e exactly (normal range; the digit exponents of finite fp64 data stay far inside it)
+RS_DEV double pow2(int e) {
+  return e >= -1022 && e <= 1023 ? __longlong_as_double((long long)(e + 1023) << 52) : ldexp(1.0, e);
 }
 RS_DEV void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
 
@@ -115,8 +131,10 @@ RS_DEV uint64_t smem_desc(const void* p) {
   return ((addr >> 4) & 0x3FFFull) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
 }
 
-// kind::i8, signed x signed -> s32, both K-major, M = 128, N = 64
-constexpr uint32_t OZ_IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((OZ_BN >> 3) << 17) | ((OZ_BM >> 4) << 24);
+// kind::i8, signed x signed -> s32, both K-major, M = 128, N = n (multiple of 16, <= 256)
+RS_DEV uint32_t oz_idesc(int n) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(OZ_BM >> 4) << 24);
+}
 
 // ---------------------------------------------------------------- slicing ----
 template <typename T>
@@ -129,24 +147,35 @@ RS_DEV double ld_elem(const T* X, long long ld, bool colmajor, long long i, long
 // row-major: one warp per row.
 template <typename T, bool COLMAJOR>
 __global__ void oz_expo_kernel(const T* __restrict__ X, long long ld, int rows, int K, int kc, int c0, int nch,
-                               int* __restrict__ expo) {
+                               int* __restrict__ expo, int* __restrict__ nonfinite) {
   const int c = c0 + blockIdx.y;
   const int k0 = c * kc, k1 = min(K, k0 + kc);
   double m = 0.0;
   long long i;
+  bool bad = false;
   if constexpr (COLMAJOR) {
     i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= rows) return;
-    for (int k = k0; k < k1; ++k) m = fmax(m, fabs((double)X[(long long)k * ld + i]));
+    for (int k = k0; k < k1; ++k) {
+      const double x = fabs((double)X[(long long)k * ld + i]);
+      m = fmax(m, x);
+      bad = bad || !isfinite(x);
+    }
   } else {
     const int lane = threadIdx.x & 31;
     i = (long long)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
     if (i >= rows) return;
-    for (int k = k0 + lane; k < k1; k += 32) m = fmax(m, fabs((double)X[i * ld + k]));
+    for (int k = k0 + lane; k < k1; k += 32) {
+      const double x = fabs((double)X[i * ld + k]);
+      m = fmax(m, x);
+      bad = bad || !isfinite(x);
+    }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+    bad = __any_sync(0xffffffffu, bad);
     if (lane != 0) return;
   }
+  if (bad && nonfinite) atomicOr(nonfinite, 1);  // NaN/inf: fmax drops NaN, so flag it
   int e = 0;
   if (m > 0.0) frexp(m, &e);
   expo[i * nch + c] = e;
@@ -236,6 +265,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(OzParams p) {
   uint64_t* tm_empty = tm_full + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tm_empty + 1);
   int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
+  int* s_eb = s_last + 1;  // OZ_BN column exponents of the current unit
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -289,7 +319,6 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(OzParams p) {
       mb_wait(tm_empty, tph ^ 1);  // the epilogue has drained the previous unit
       tph ^= 1;
       tc_fence_after();
-      uint32_t inited = 0;
       for (int kb = kb0; kb < kb1; ++kb) {
         mb_wait(full_b + bi, bph);
         const uint8_t* bst = sb + (size_t)bi * OZ_MAXS * OZ_BTILE;
@@ -297,18 +326,24 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(OzParams p) {
           mb_wait(full_a + ai, aph);
           tc_fence_after();
           if (lane == 0) {
+            // A plane s times Omega planes t = 0..G-1-s in MMAs of up to 4 planes
+            // (N <= 256): the planes are consecutive 64-row tiles in shared memory
+            // and their accumulators g = s + t consecutive 64-column TMEM blocks, so
+            // one MMA covers up to four (s, t) pairs and reads the A plane once.
             const uint64_t da = smem_desc(sa + (size_t)ai * OZ_ATILE);
-            const int tmax = min(p.SB, p.G - s);
-            for (int t = 0; t < tmax; ++t) {
-              const int g = s + t;
-              const uint64_t db = smem_desc(bst + (size_t)t * OZ_BTILE);
-              const uint32_t d = tmem + (uint32_t)(g * OZ_BN);
+            const int nt = p.G - s;
+            for (int t0 = 0; t0 < nt; t0 += 4) {
+              const int ntile = min(4, nt - t0);
+              const uint64_t db = smem_desc(bst + (size_t)t0 * OZ_BTILE);
+              const uint32_t d = tmem + (uint32_t)((s + t0) * OZ_BN);
+              const uint32_t idesc = oz_idesc(OZ_BN * ntile);
 #pragma unroll
               for (int kk = 0; kk < OZ_BK / 32; ++kk) {
-                const uint32_t acc = (kk > 0 || ((inited >> g) & 1u)) ? 1u : 0u;
-                tc_mma_i8(d, da + 2 * kk, db + 2 * kk, OZ_IDESC, acc);
+                // s = 0 of the unit's first k-block covers every accumulator: it
+                // starts them from zero, everything after accumulates
+                const uint32_t acc = (kb > kb0 || s > 0 || kk > 0) ? 1u : 0u;
+                if (OZ_DBG != 1) tc_mma_i8(d, da + 2 * kk, db + 2 * kk, idesc, acc);
               }
-              inited |= 1u << g;
             }
             tc_commit(empty_a + ai);  // the A stage is free once these MMAs have read it
           }
@@ -337,22 +372,51 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(OzParams p) {
       tph ^= 1;
       tc_fence_after();
       double* slot = p.slots + (size_t)u * (OZ_BM * OZ_BN);
+      // this unit's column exponents, staged once in shared memory
+      named_sync(1, 128);
+      if (et < OZ_BN) {
+        const int col = tn * OZ_BN + et;
+        s_eb[et] = col < p.N ? p.bexp[(long long)col * p.nch + ch] : 0;
+      }
+      named_sync(1, 128);
       for (int cb = 0; cb < OZ_BN / 16; ++cb) {
+        // The G <= 8 exact int32 digit-sum accumulators of 16 columns, combined
+        // exactly in two int64 words (H: g = 0..3, L: g = 4..7; 7-bit shifts,
+        // |H|, |L| < 2^55), then two conversions and one fma:
+        //   v = 2^(ea+eb) (H 2^-35 + L 2^-63).
+        long long H[16], L[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) { H[j] = 0; L[j] = 0; }
+        if (OZ_DBG != 2) {
+          const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(cb * 16);
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            const int g0 = 4 * half;
+            if (g0 >= p.G) break;
+            int c[4][16];  // four accumulators in flight, one wait
+#pragma unroll
+            for (int gg = 0; gg < 4; ++gg)
+              if (g0 + gg < p.G) tc_ld16_async(tb + (uint32_t)((g0 + gg) * OZ_BN), c[gg]);
+            tc_wait_ld();
+#pragma unroll
+            for (int gg = 0; gg < 4; ++gg) {
+              if (g0 + gg >= p.G) break;
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                if (half == 0) H[j] = H[j] * 128 + c[gg][j];
+                else L[j] = L[j] * 128 + c[gg][j];
+              }
+            }
+          }
+        }
+        // missing high accumulators (G < 8) still take their 7-bit shifts
+        const int gl = p.G > 4 ? p.G - 4 : 0, gh = p.G < 4 ? p.G : 4;
         double v[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = 0.0;
-        for (int g = p.G - 1; g >= 0; --g) {  // smallest weight first
-          int c[16];
-          tc_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(g * OZ_BN + cb * 16), c);
-          const int sh = -7 * (g + 2);
-#pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] += ldexp((double)c[j], sh);
-        }
-#pragma unroll
         for (int j = 0; j < 16; ++j) {
-          const int col = tn * OZ_BN + cb * 16 + j;
-          const int eb = col < p.N ? p.bexp[(long long)col * p.nch + ch] : 0;
-          v[j] = ldexp(v[j], ea + eb);
+          const double h = (double)H[j] * pow2(-7 * (gh + 1));
+          const double l = (double)L[j] * pow2(-7 * (gl + 5));
+          v[j] = (h + l) * pow2(ea + s_eb[cb * 16 + j]);
         }
         if (p.nch == 1) {
           if (row < p.M) {
@@ -438,7 +502,7 @@ size_t oz_digits_bytes(int rows, long long K, int S, int tile_rows) {
 }
 
 int launch_oz_slice(const void* X, int fp32, long long ld, int colmajor, int rows, int K, int k0, int k1, int kc,
-                    int S, int tile_rows, int8_t* dig, int* expo, cudaStream_t st) {
+                    int S, int tile_rows, int8_t* dig, int* expo, int* nonfinite, cudaStream_t st) {
   if (rows < 0 || K < 0 || k0 < 0 || k1 > K || k0 > k1 || kc <= 0 || kc % OZ_BK || k0 % kc || S < 1 ||
       S > OZ_MAXS || (tile_rows != OZ_BM && tile_rows != OZ_BN))
     return RS_ERR_ARG;
@@ -453,11 +517,11 @@ int launch_oz_slice(const void* X, int fp32, long long ld, int colmajor, int row
     dim3 ge((rows + 255) / 256, c1 - c0);
     dim3 gs((rows_pad + 31) / 32, (groups + 7) / 8);
     if (fp32) {
-      oz_expo_kernel<float, true><<<ge, 256, 0, st>>>((const float*)X, ld, rows, K, kc, c0, nch, expo);
+      oz_expo_kernel<float, true><<<ge, 256, 0, st>>>((const float*)X, ld, rows, K, kc, c0, nch, expo, nonfinite);
       oz_slice_kernel<float, true><<<gs, dim3(32, 8), 0, st>>>((const float*)X, ld, rows, rows_pad, K, k0, k1_pad,
                                                                kc, nch, S, tile_rows, KB, expo, dig);
     } else {
-      oz_expo_kernel<double, true><<<ge, 256, 0, st>>>((const double*)X, ld, rows, K, kc, c0, nch, expo);
+      oz_expo_kernel<double, true><<<ge, 256, 0, st>>>((const double*)X, ld, rows, K, kc, c0, nch, expo, nonfinite);
       oz_slice_kernel<double, true><<<gs, dim3(32, 8), 0, st>>>((const double*)X, ld, rows, rows_pad, K, k0,
                                                                 k1_pad, kc, nch, S, tile_rows, KB, expo, dig);
     }
@@ -465,11 +529,11 @@ int launch_oz_slice(const void* X, int fp32, long long ld, int colmajor, int row
     dim3 ge((rows + 7) / 8, c1 - c0);
     dim3 gs((rows_pad + 7) / 8, (groups + 31) / 32);
     if (fp32) {
-      oz_expo_kernel<float, false><<<ge, 256, 0, st>>>((const float*)X, ld, rows, K, kc, c0, nch, expo);
+      oz_expo_kernel<float, false><<<ge, 256, 0, st>>>((const float*)X, ld, rows, K, kc, c0, nch, expo, nonfinite);
       oz_slice_kernel<float, false><<<gs, dim3(32, 8), 0, st>>>((const float*)X, ld, rows, rows_pad, K, k0, k1_pad,
                                                                 kc, nch, S, tile_rows, KB, expo, dig);
     } else {
-      oz_expo_kernel<double, false><<<ge, 256, 0, st>>>((const double*)X, ld, rows, K, kc, c0, nch, expo);
+      oz_expo_kernel<double, false><<<ge, 256, 0, st>>>((const double*)X, ld, rows, K, kc, c0, nch, expo, nonfinite);
       oz_slice_kernel<double, false><<<gs, dim3(32, 8), 0, st>>>((const double*)X, ld, rows, rows_pad, K, k0,
                                                                  k1_pad, kc, nch, S, tile_rows, KB, expo, dig);
     }
@@ -481,8 +545,8 @@ int launch_oz_slice(const void* X, int fp32, long long ld, int colmajor, int row
 int launch_oz_gemm(int M, int N, int K, int kc, int mode, double alpha, const int8_t* adig, const int* aexp, int SA,
                    const int8_t* bdig, const int* bexp, int SB, double beta, const double* Cin, long long ldcin,
                    double* C, long long ldc, double* slots, int* tickets, int nslots, cudaStream_t st) {
-  if (M < 0 || N < 0 || K < 0 || SA < 1 || SB < 1 || SA > OZ_MAXS || SB > OZ_MAXS || kc % OZ_BK || kc <= 0 ||
-      kc > 16384)
+  // G = SB accumulators and SA <= SB, so the s = 0 products touch every accumulator
+  if (M < 0 || N < 0 || K < 0 || SA < 1 || SB < SA || SB > OZ_MAXS || kc % OZ_BK || kc <= 0 || kc > 16384)
     return RS_ERR_ARG;
   if (mode != RS_GEMM_PLAIN && mode != RS_GEMM_FOLD) return RS_ERR_ARG;
   if ((mode == RS_GEMM_FOLD || beta != 0.0) && Cin == nullptr) return RS_ERR_ARG;
@@ -495,7 +559,7 @@ int launch_oz_gemm(int M, int N, int K, int kc, int mode, double alpha, const in
   p.M = M; p.N = N; p.K = K;
   p.adig = adig; p.aexp = aexp; p.SA = SA;
   p.bdig = bdig; p.bexp = bexp; p.SB = SB;
-  p.G = std::max(SA, SB);
+  p.G = SB;
   p.KB = (K + OZ_BK - 1) / OZ_BK;
   p.kbc = kc / OZ_BK;
   p.nch = std::max(1, (K + kc - 1) / kc);

@@ -10,8 +10,8 @@
 Skeleton gathers (`a[row_idx]`, `a[:, col_idx]`, `a[ix_(I, J)]`) run on the
 gather kernel; column skeletons come from LUPP of ``a[row_idx].T`` on the
 T-form engine; the 1-norm condition number of the skeleton submatrix is
-computed exactly from its device LU (the reference's LAPACK dgecon estimate
-is a lower bound of it, so the flag can only turn on earlier, never later).
+estimated from its device LU with LAPACK dgecon's algorithm (Hager/Higham
+dlacn2), as the reference's flag does.
 """
 
 from dataclasses import dataclass
@@ -218,7 +218,15 @@ def _column_skeletons_from_rows(A, row_idx, k):
 
 
 def _cond1(S):
-    """Exact 1-norm condition number of the k x k device Matrix S (inf if singular)."""
+    """LAPACK-style 1-norm condition estimate of the k x k device Matrix S
+    (`_condition_estimate_1norm`, skeleton.py:592-603: dgetrf + dgecon).
+
+    The LU is the device LUPP (the same partial-pivoting rule as dgetrf);
+    ||S^-1||_1 is estimated by Hager/Higham's dlacn2 iteration (at most five
+    sign-vector steps plus the alternating-sign safeguard), every solve with
+    the LU factors on the device TRSM, so the flag follows the reference's
+    *estimate* rather than the exact condition number it bounds from below.
+    Returns 1/rcond (inf for an exactly singular S or a zero S)."""
     k = S.rows
     dev = _device.device()
     out = torch.empty(1, dtype=torch.float64, device=dev)
@@ -229,23 +237,63 @@ def _cond1(S):
         return np.inf
     A = Sr.copy()
     try:
-        perm, _ = dense._lupp_device(A, allow_partial=False)
+        dense._lupp_device(A, allow_partial=False)
     except RankDeficientError:
-        return np.inf
+        return np.inf  # dgetrf info > 0
     L, U = dense._split_lu(A, k)
-    # S^{-1} = U^{-1} L^{-1} P
-    eye_p = torch.zeros((k, k), dtype=torch.float64, device=dev)
-    eye_p[torch.arange(k, device=dev), perm] = 1.0
-    Y = dense._trsm_left(dense._mat(L.contiguous()), dense._mat(eye_p), lower=True, unit=True)
-    d = U.diagonal()
-    if bool((d == 0).any()):
+    Lm, Um = dense._mat(L.contiguous()), dense._mat(U.contiguous())
+
+    def solve(x, kase):
+        """kase 1: x <- U^-1 L^-1 x ; kase 2: x <- L^-T U^-T x (dgecon's two dlatrs pairs)."""
+        X = dense._mat(x.reshape(k, 1).contiguous())
+        if kase == 1:
+            y = dense._trsm_left(Lm, X, lower=True, unit=True)
+            y = dense._trsm_left(Um, y, lower=False, unit=False)
+        else:
+            y = dense._trsm_left(Um.T, X, lower=True, unit=False)
+            y = dense._trsm_left(Lm.T, y, lower=False, unit=True)
+        return y.tensor().reshape(k)
+
+    def sgn(x):
+        return torch.where(x >= 0, 1.0, -1.0).to(torch.float64)
+
+    # dlacn2 (Higham 1988, LAPACK): reverse communication unrolled
+    x = solve(torch.full((k,), 1.0 / k, dtype=torch.float64, device=dev), 1)
+    if k == 1:
+        est = float(x.abs()[0])
+    else:
+        est = float(x.abs().sum())
+        isgn = sgn(x)
+        x = solve(isgn, 2)
+        j = int(torch.argmax(x.abs()))
+        it = 2
+        while True:
+            e = torch.zeros(k, dtype=torch.float64, device=dev)
+            e[j] = 1.0
+            x = solve(e, 1)
+            estold, est = est, float(x.abs().sum())
+            xs = sgn(x)
+            if bool(torch.equal(xs, isgn)) or est <= estold:
+                break  # repeated sign vector / cycling
+            isgn = xs
+            x = solve(isgn, 2)
+            jlast, j = j, int(torch.argmax(x.abs()))
+            if float(x[jlast]) != float(x[j].abs()) and it < 5:
+                it += 1
+                continue
+            break
+        alt = torch.arange(k, dtype=torch.float64, device=dev)
+        alt = (1.0 + alt / (k - 1)) * torch.where(alt % 2 == 0, 1.0, -1.0).to(torch.float64)
+        x = solve(alt, 1)
+        temp = 2.0 * (float(x.abs().sum()) / (3 * k))
+        if temp > est:
+            est = temp
+    if not np.isfinite(est):
         return np.inf
-    X = dense._trsm_left(dense._mat(U.contiguous()), Y, lower=False, unit=False)
-    _lib.call("rs_norm1", X.ptr, X.ld, k, k, out.data_ptr(), _st())
-    inorm = float(out.item())
-    if not np.isfinite(inorm):
+    if est == 0.0:
         return np.inf
-    return anorm * inorm
+    rcond = (1.0 / est) / anorm
+    return np.inf if rcond == 0.0 else 1.0 / rcond
 
 
 def two_sided_id(a, k, spec, rng):

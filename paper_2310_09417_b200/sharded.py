@@ -33,7 +33,7 @@ import math
 import torch
 import torch.distributed as dist
 
-from . import _device, _lib
+from . import _device, _lib, _ozaki
 from .errors import DimensionError, RankDeficientError
 from .skeleton import (
     STATUS_NOT_CONVERGED,
@@ -66,6 +66,9 @@ class DeviceShardOps:
         self.st = _device.stream_handle()
         self.host_rng = _device.host_rng()
         self.rng_status = torch.zeros(4096, dtype=torch.int32, device=self.dev)
+        # tensor-core sketch: the local candidates' digit planes, cut once
+        self.ap = _ozaki.Planes.of_matrix(a_local) if _ozaki.sketch_engine() == "ozaki" else None
+        self.bp = None
 
     def f64(self, n):
         return torch.empty(max(int(n), 1), dtype=torch.float64, device=self.dev)
@@ -95,6 +98,11 @@ class DeviceShardOps:
 
     def sketch(self, om, b, out):
         m, n = self.a.shape
+        if self.ap is not None:
+            if self.bp is None:
+                self.bp = _ozaki.Planes(b, n, _ozaki.OMEGA_PLANES, 64, self.dev)
+            _ozaki.Planes.of_omega(om, out=self.bp)
+            return _ozaki.sketch(self.ap, self.bp, out.data_ptr(), b)
         _lib.call("rs_sketch_gemm", m, n, b, self.a.ptr, self.a.ld, int(self.a.colmajor), om.data_ptr(), b,
                   out.data_ptr(), b, self.ws.data_ptr(), self.st)
 
@@ -190,6 +198,12 @@ def rand_lupp_adaptive_sharded(a_local, b, tau, spec, rng, max_rank=None, group=
     if ops is None:
         a_local = _device.as_matrix(a_local)
         ops = DeviceShardOps(a_local)
+        if ops.ap is not None:  # the digit planes drop NaN/inf: check the slicer's flag on every rank
+            bad = ops.ap.nonfinite.clone()
+            if _world(group)[0] > 1:
+                dist.all_reduce(bad, op=dist.ReduceOp.MAX, group=group)
+            if int(bad.item()):
+                raise ValueError("matrix contains non-finite entries")
     m_loc, n = ops.a.shape
     counts = _row_counts(m_loc, group, ops.dev)
     rank = _world(group)[1]

@@ -16,7 +16,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from . import _device, _engine, _lib, _omega, dense
+from . import _device, _engine, _lib, _omega, _ozaki, dense
 from .errors import DimensionError, RankDeficientError
 from .sketching import make_sketch
 
@@ -172,6 +172,12 @@ def rand_lupp_adaptive(a, b, tau, spec, rng, max_rank=None):
     if max_rank is None:
         max_rank = max(b, min(m, n) - b)
     max_rank = min(max_rank, min(m, n))
+    if _ozaki.sketch_engine() == "ozaki":
+        arr = _streamable(a)
+        if arr is not None:  # H2D overlapped with the slicing of A into digit planes
+            A, planes = _streamed_planes(arr)
+            return _AdaptiveDriver(A, b, tau, rng, max_rank, spec=spec, planes=planes).run()
+        return _AdaptiveDriver(_device.as_matrix(a), b, tau, rng, max_rank, spec=spec).run()
     pre = _presketch(a, b, rng, max_rank, spec)
     if pre is not None:
         A, yb, nb = pre
@@ -235,6 +241,32 @@ def _streamed_sketch(arr, om, transpose=False):
     _device.h2d_rows(under, on_chunk, out=U, align=kc)
     A = _device.Matrix(U, m, n, m if a_colmajor else n, a_colmajor, "numpy")
     return A, Y.t
+
+
+def _streamed_planes(arr):
+    """Copy the host array to the device in chunks and cut every chunk into
+    the tensor-core sketch's digit planes as it lands (the copy engine and
+    the slicing kernels overlap).  Chunks are aligned to the planes' K-chunks
+    (column-major candidates) or row tiles, so the planes -- and every sketch
+    bit -- equal those of a device-resident A."""
+    dev = _device.device()
+    m, n = arr.shape
+    a_colmajor = not arr.flags.c_contiguous
+    under = arr.T if a_colmajor else arr       # C-ordered host rows
+    U = torch.empty(under.shape, dtype=torch.float64, device=dev)
+    planes = _ozaki.Planes(m, n, _ozaki.A_PLANES[torch.float64], 128, dev)
+    compute = torch.cuda.current_stream(dev)
+
+    def on_chunk(r0, r1, ev):
+        compute.wait_event(ev)
+        if a_colmajor:   # rows r0..r1 of `under` are K-columns r0..r1 of the candidates
+            planes.fill(U.data_ptr(), False, m, True, r0, r1)
+        else:            # rows r0..r1 of `under` are candidate rows
+            planes.fill_rows(U.data_ptr() + 8 * r0 * n, False, n, r0, r1)
+
+    _device.h2d_rows(under, on_chunk, out=U, align=planes.kc if a_colmajor else 128)
+    A = _device.Matrix(U, m, n, m if a_colmajor else n, a_colmajor, "numpy")
+    return A, planes
 
 
 def _presketch(a, b, rng, max_rank, spec):
@@ -314,7 +346,7 @@ class _AdaptiveDriver:
     one pinned readback) while the GPU keeps the next sketch GEMM running.
     """
 
-    def __init__(self, a, b, tau, rng, max_rank, host=False, spec=None, presketch=None):
+    def __init__(self, a, b, tau, rng, max_rank, host=False, spec=None, presketch=None, planes=None):
         self.prof = _PHASE_TIMER or _NullTimer()
         self.a, self.b, self.tau, self.rng, self.max_rank = a, b, tau, rng, max_rank
         m, n = a.shape
@@ -345,6 +377,11 @@ class _AdaptiveDriver:
         # the first block is always absorbed whole (adaptive_init), so the
         # rank can reach b even when max_rank < b (`skeleton.py:435-441`)
         self.st = _engine.TFormState(m, max(max_rank, b), min(b, _engine.MAX_BLOCK))
+        # tensor-core sketch: A's digit planes once, Omega_t's per block
+        self.ozaki = _ozaki.sketch_engine() == "ozaki" and self.yb is None
+        if self.ozaki:
+            self.ap = planes if planes is not None else _ozaki.Planes.of_matrix(a)
+            self.bp = _ozaki.Planes(b, n, _ozaki.OMEGA_PLANES, 64, dev)
         self.stream = _device.stream_handle()
         self.ws = _device.workspace()
         self._issued = set()
@@ -389,9 +426,13 @@ class _AdaptiveDriver:
         self._issue_copy(t)
         self.compute.wait_event(self.om_ready[slot])
         tok = self.prof.start("sketch_gemm")
-        _lib.call("rs_sketch_gemm", self.m, self.n, self.b, self.a.ptr, self.a.ld, int(self.a.colmajor),
-                  self.om[slot].data_ptr(), self.b, self.y[slot].data_ptr(), self.b,
-                  self.ws.data_ptr(), self.stream)
+        if self.ozaki:
+            _ozaki.Planes.of_omega(self.om[slot], out=self.bp)
+            _ozaki.sketch(self.ap, self.bp, self.y[slot].data_ptr(), self.b)
+        else:
+            _lib.call("rs_sketch_gemm", self.m, self.n, self.b, self.a.ptr, self.a.ld, int(self.a.colmajor),
+                      self.om[slot].data_ptr(), self.b, self.y[slot].data_ptr(), self.b,
+                      self.ws.data_ptr(), self.stream)
         self.prof.stop(tok)
         ev = torch.cuda.Event()
         ev.record(self.compute)
@@ -434,6 +475,8 @@ class _AdaptiveDriver:
             self._sketch(0)
             y0 = self._y(0)
             st.schur(y0[0], y0[1], min(b, _engine.MAX_BLOCK), self.e2)
+            if self.ozaki and int(self.ap.nonfinite.item()):
+                raise ValueError("matrix contains non-finite entries")
             if wide or not math.isfinite(float(self.e2.item())):
                 if self.nb_pre:
                     _finite_or_raise(_device.Matrix(self.yb, self.m, b, b * self.nb_pre, False, self.a.kind))

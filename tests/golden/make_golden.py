@@ -147,6 +147,21 @@ def main():
         u_mid=cur.u_mid, status=cur.status)
     r = rs.two_sided_id(np.diag([1.0] * 5 + [1e-16] * 5), 8, spec(10), rs.RngStream(57))
     put("two_sided_illcond", row_idx=r.row_idx, col_idx=r.col_idx, status=r.status)
+    # cond_1 flag: a matrix whose dgecon estimate (7.4e13) and exact 1-norm condition
+    # number (1.03e14) straddle the 1e14 limit (skeleton.py:592-603)
+    from randskel.skeleton import _condition_estimate_1norm
+    g = np.random.default_rng(0)
+    for _ in range(4000):
+        n = int(g.integers(20, 60))
+        q1, _ = np.linalg.qr(g.standard_normal((n, n)))
+        q2, _ = np.linalg.qr(g.standard_normal((n, n)))
+        c = 10 ** g.uniform(12.5, 14.5)
+        smat = (q1 * np.logspace(0, -np.log10(c), n)) @ q2.T
+        est = _condition_estimate_1norm(smat)
+        kappa = np.abs(smat).sum(0).max() * np.abs(np.linalg.inv(smat)).sum(0).max()
+        if est < 1e14 < kappa:
+            put("cond1_straddle", s=smat, est=est, exact=kappa)
+            break
     # adaptive-CUR composition (cfg3 recipe at 1024 x 512)
     g = np.random.default_rng(0)
     wmat = g.random((1024, 100))

@@ -318,3 +318,18 @@ def test_structured_embeddings_vs_reference(kind):
     res = rs.rand_lupp_adaptive(b_exact, 8, 1e-9, rs.SketchSpec(kind, 90, 8, **kw), rs.RngStream(85))
     assert res.rank == int(ga["rank"]) and res.status == str(ga["status"])
     assert np.array_equal(res.row_idx[: res.rank - 8], ga["row_idx"][: res.rank - 8])
+
+
+def test_cond1_is_dgecon_estimate_not_exact():
+    """rs's cond_1 flag follows LAPACK dgecon's Hager/Higham estimate on the device LU
+    (skeleton.py:592-603): on a matrix whose estimate (7.4e13) and exact condition number
+    (1.03e14) straddle the 1e14 limit, the flag must not turn on."""
+    import torch
+
+    from paper_2310_09417_b200 import cur, dense
+
+    g = golden("cond1_straddle")
+    s = torch.from_numpy(g["s"]).cuda()
+    est = cur._cond1(dense._mat(s.contiguous()))
+    assert abs(est - float(g["est"])) <= 1e-6 * float(g["est"])
+    assert est < cur.COND_LIMIT < float(g["exact"])

@@ -206,3 +206,12 @@ def test_oracle_structured_embeddings(kind):
     np.testing.assert_allclose(om, g["dense"], rtol=0, atol=1e-14)
     a = np.random.default_rng(80).standard_normal((90, 70))
     np.testing.assert_allclose(a @ om, g["y"], rtol=0, atol=1e-12)
+
+
+def test_cond1_estimate_straddles_limit():
+    """The oracle's cond_1 is dgecon's estimate (skeleton.py:592-603), not the exact
+    1-norm condition number: on this matrix they fall on opposite sides of 1e14."""
+    g = golden("cond1_straddle")
+    est = orc.cond1(g["s"])
+    assert abs(est - float(g["est"])) <= 1e-10 * float(g["est"])
+    assert est < 1e14 < float(g["exact"])
