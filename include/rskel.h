@@ -273,9 +273,10 @@ size_t rs_oz_digits_bytes(int rows, long long K, int S, int tile_rows);
  * at X[i*ld + k] or, colmajor, X[k*ld + i]) for k in [k0, k1), k0 and k1
  * multiples of kc or k1 = K.  expo: rows x ceil(K / kc) int32.  For Omega
  * (K x N row-major) pass colmajor = 1, rows = N, ld = its row stride.
- * *nonfinite (may be NULL) is or-ed with 1 if X holds a NaN or inf. */
+ * *nonfinite (may be NULL) is or-ed with 1 if X holds a NaN or inf.
+ * workspace: rs_workspace_bytes (scratch for the row-chunk maxima). */
 int rs_oz_slice(const void* X, int fp32, long long ld, int colmajor, int rows, int K, int k0, int k1, int kc, int S,
-                int tile_rows, int8_t* digits, int* expo, int* nonfinite, void* stream);
+                int tile_rows, int8_t* digits, int* expo, int* nonfinite, void* workspace, void* stream);
 
 /* C (M x N row-major) = alpha * A Omega + beta * Cin (mode RS_GEMM_PLAIN) or
  * Cin + A Omega with the chunk sums folded onto Cin (RS_GEMM_FOLD), from the

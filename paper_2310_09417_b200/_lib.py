@@ -65,7 +65,7 @@ SIGNATURES = {
     "rs_oz_chunk": (_c_int, [_c_ll]),
     "rs_oz_digits_bytes": (ctypes.c_size_t, [_c_int, _c_ll, _c_int, _c_int]),
     "rs_oz_slice": (_c_int, [_p, _c_int, _c_ll, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _p,
-                             _p, _p, _p]),
+                             _p, _p, _p, _p]),
     "rs_oz_gemm": (_c_int, [_c_int, _c_int, _c_int, _c_int, _c_int, _c_double, _p, _p, _c_int, _p, _p, _c_int,
                             _c_double, _p, _c_ll, _p, _c_ll, _p, _p]),
     "rs_uniform": (_c_int, [ctypes.c_ulonglong, ctypes.c_ulonglong, _c_ll, _p, _p]),

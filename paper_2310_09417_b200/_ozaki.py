@@ -55,7 +55,7 @@ class Planes:
         k1 = self.K if k1 is None else k1
         _lib.call("rs_oz_slice", ptr, int(fp32), ld, int(colmajor), self.rows, self.K, k0, k1, self.kc, self.S,
                   self.tile_rows, self.dig.data_ptr(), self.expo.data_ptr(), self.nonfinite.data_ptr(),
-                  _device.stream_handle())
+                  _device.workspace().data_ptr(), _device.stream_handle())
         return self
 
     def fill_rows(self, ptr, fp32, ld, r0, r1):
@@ -66,7 +66,7 @@ class Planes:
         dig_off = lib.rs_oz_digits_bytes(r0, self.K, self.S, self.tile_rows)
         _lib.call("rs_oz_slice", ptr, int(fp32), ld, 0, r1 - r0, self.K, 0, self.K, self.kc, self.S,
                   self.tile_rows, self.dig.data_ptr() + dig_off, self.expo.data_ptr() + 4 * r0 * self.nch,
-                  self.nonfinite.data_ptr(), _device.stream_handle())
+                  self.nonfinite.data_ptr(), _device.workspace().data_ptr(), _device.stream_handle())
         return self
 
     @classmethod

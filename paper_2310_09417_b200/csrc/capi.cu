@@ -268,9 +268,13 @@ size_t rs_oz_digits_bytes(int rows, long long K, int S, int tile_rows) {
 }
 
 int rs_oz_slice(const void* X, int fp32, long long ld, int colmajor, int rows, int K, int k0, int k1, int kc,
-                int planes, int tile_rows, int8_t* digits, int* expo, int* nonfinite, void* stream) {
+                int planes, int tile_rows, int8_t* digits, int* expo, int* nonfinite, void* workspace,
+                void* stream) {
+  if (workspace == nullptr) return RS_ERR_ARG;
+  // the row-chunk maxima use the GEMM partial-slot region of the workspace as scratch
+  unsigned long long* mx = reinterpret_cast<unsigned long long*>(W(workspace, layout().gemm_off));
   return rs::launch_oz_slice(X, fp32, ld, colmajor, rows, K, k0, k1, kc, planes, tile_rows, digits, expo, nonfinite,
-                             S(stream));
+                             mx, sizeof(double) * (size_t)rs::GEMM_SLOTS * 128 * 64, S(stream));
 }
 
 int rs_oz_gemm(int M, int N, int K, int kc, int mode, double alpha, const int8_t* a_digits, const int* a_expo,

@@ -142,42 +142,62 @@ RS_DEV double ld_elem(const T* X, long long ld, bool colmajor, long long i, long
   return (double)(colmajor ? X[k * ld + i] : X[i * ld + k]);
 }
 
-// expo[i * nch + c] = e with max_{k in chunk c} |X[i, k]| < 2^e (frexp), for the
-// chunks c0 <= c < c1.  Column-major: one thread per row (coalesced along i);
-// row-major: one warp per row.
+// Row-chunk maxima -> exponents: expo[i * nch + c] = e with
+// max_{k in chunk c} |X[i, k]| < 2^e (frexp).  Pass 1 (oz_max_kernel): block
+// (32 x 8) covers 32 rows x 256 k of one chunk -- lanes along the contiguous
+// dimension, the 8 warps split the k range -- reduces in shared memory and
+// folds into mx[i * nch + c] with an atomicMax on the double's bits (|x| >= 0
+// orders like its bit pattern).  Pass 2 (oz_expo_kernel) converts.  NaN/inf
+// set *nonfinite (fmax would drop a NaN).
 template <typename T, bool COLMAJOR>
-__global__ void oz_expo_kernel(const T* __restrict__ X, long long ld, int rows, int K, int kc, int c0, int nch,
-                               int* __restrict__ expo, int* __restrict__ nonfinite) {
+__global__ void __launch_bounds__(256) oz_max_kernel(const T* __restrict__ X, long long ld, int rows, int K, int kc,
+                                                     int c0, int nch, unsigned long long* __restrict__ mx,
+                                                     int* __restrict__ nonfinite) {
   const int c = c0 + blockIdx.y;
-  const int k0 = c * kc, k1 = min(K, k0 + kc);
+  const int kb = c * kc + blockIdx.z * 256;
+  const int kend = min(K, min(c * kc + kc, kb + 256));
+  __shared__ double red[8][33];
   double m = 0.0;
-  long long i;
   bool bad = false;
-  if constexpr (COLMAJOR) {
-    i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= rows) return;
-    for (int k = k0; k < k1; ++k) {
-      const double x = fabs((double)X[(long long)k * ld + i]);
-      m = fmax(m, x);
-      bad = bad || !isfinite(x);
+  if constexpr (COLMAJOR) {  // lanes along rows (contiguous), warps along k
+    const long long i = (long long)blockIdx.x * 32 + threadIdx.x;
+    if (i < rows)
+      for (int k = kb + threadIdx.y; k < kend; k += 8) {
+        const double x = fabs((double)X[(long long)k * ld + i]);
+        m = fmax(m, x);
+        bad = bad || !isfinite(x);
+      }
+    red[threadIdx.y][threadIdx.x] = m;
+    __syncthreads();
+    if (threadIdx.y == 0 && i < rows) {
+      for (int w = 1; w < 8; ++w) m = fmax(m, red[w][threadIdx.x]);
+      atomicMax(mx + i * nch + c, (unsigned long long)__double_as_longlong(m));
     }
-  } else {
-    const int lane = threadIdx.x & 31;
-    i = (long long)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-    if (i >= rows) return;
-    for (int k = k0 + lane; k < k1; k += 32) {
-      const double x = fabs((double)X[i * ld + k]);
-      m = fmax(m, x);
-      bad = bad || !isfinite(x);
-    }
+  } else {  // warp y handles row blockIdx.x * 8 + y, lanes along k (contiguous)
+    const long long i = (long long)blockIdx.x * 8 + threadIdx.y;
+    if (i < rows)
+      for (int k = kb + threadIdx.x; k < kend; k += 32) {
+        const double x = fabs((double)X[i * ld + k]);
+        m = fmax(m, x);
+        bad = bad || !isfinite(x);
+      }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
-    bad = __any_sync(0xffffffffu, bad);
-    if (lane != 0) return;
+    if (threadIdx.x == 0 && i < rows) atomicMax(mx + i * nch + c, (unsigned long long)__double_as_longlong(m));
   }
-  if (bad && nonfinite) atomicOr(nonfinite, 1);  // NaN/inf: fmax drops NaN, so flag it
+  if (bad && nonfinite) atomicOr(nonfinite, 1);
+}
+
+__global__ void oz_expo_kernel(const unsigned long long* __restrict__ mx, int rows, int c0, int c1, int nch,
+                               int* __restrict__ expo) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int nc = c1 - c0;
+  if (t >= (long long)rows * nc) return;
+  const long long i = t / nc;
+  const int c = c0 + (int)(t % nc);
+  const double m = __longlong_as_double((long long)mx[i * nch + c]);
   int e = 0;
-  if (m > 0.0) frexp(m, &e);
+  if (m > 0.0 && isfinite(m)) frexp(m, &e);
   expo[i * nch + c] = e;
 }
 
@@ -502,43 +522,48 @@ size_t oz_digits_bytes(int rows, long long K, int S, int tile_rows) {
 }
 
 int launch_oz_slice(const void* X, int fp32, long long ld, int colmajor, int rows, int K, int k0, int k1, int kc,
-                    int S, int tile_rows, int8_t* dig, int* expo, int* nonfinite, cudaStream_t st) {
+                    int S, int tile_rows, int8_t* dig, int* expo, int* nonfinite, unsigned long long* mx,
+                    size_t mx_bytes, cudaStream_t st) {
   if (rows < 0 || K < 0 || k0 < 0 || k1 > K || k0 > k1 || kc <= 0 || kc % OZ_BK || k0 % kc || S < 1 ||
       S > OZ_MAXS || (tile_rows != OZ_BM && tile_rows != OZ_BN))
     return RS_ERR_ARG;
   if (rows == 0 || k0 == k1) return RS_OK;
   const int nch = (K + kc - 1) / kc;
+  if ((size_t)rows * nch * sizeof(unsigned long long) > mx_bytes) return RS_ERR_CAPACITY;
   const int c0 = k0 / kc, c1 = (k1 + kc - 1) / kc;
   const int KB = (K + OZ_BK - 1) / OZ_BK;
   const int rows_pad = (rows + tile_rows - 1) / tile_rows * tile_rows;
   const int k1_pad = k1 == K ? (K + OZ_BK - 1) / OZ_BK * OZ_BK : k1;
   const int groups = (k1_pad - k0) / 16;
+  // mx: rows x nch words of scratch (the caller's workspace), zeroed for the atomics
+  cudaMemsetAsync(mx, 0, sizeof(unsigned long long) * (size_t)rows * nch, st);
+  const dim3 gm_col((rows + 31) / 32, c1 - c0, (kc + 255) / 256), gm_row((rows + 7) / 8, c1 - c0, (kc + 255) / 256);
+  const dim3 gs_col((rows_pad + 31) / 32, (groups + 7) / 8), gs_row((rows_pad + 7) / 8, (groups + 31) / 32);
+  const long long ne = (long long)rows * (c1 - c0);
   if (colmajor) {
-    dim3 ge((rows + 255) / 256, c1 - c0);
-    dim3 gs((rows_pad + 31) / 32, (groups + 7) / 8);
-    if (fp32) {
-      oz_expo_kernel<float, true><<<ge, 256, 0, st>>>((const float*)X, ld, rows, K, kc, c0, nch, expo, nonfinite);
-      oz_slice_kernel<float, true><<<gs, dim3(32, 8), 0, st>>>((const float*)X, ld, rows, rows_pad, K, k0, k1_pad,
-                                                               kc, nch, S, tile_rows, KB, expo, dig);
-    } else {
-      oz_expo_kernel<double, true><<<ge, 256, 0, st>>>((const double*)X, ld, rows, K, kc, c0, nch, expo, nonfinite);
-      oz_slice_kernel<double, true><<<gs, dim3(32, 8), 0, st>>>((const double*)X, ld, rows, rows_pad, K, k0,
-                                                                k1_pad, kc, nch, S, tile_rows, KB, expo, dig);
-    }
+    if (fp32) oz_max_kernel<float, true><<<gm_col, dim3(32, 8), 0, st>>>((const float*)X, ld, rows, K, kc, c0, nch, mx, nonfinite);
+    else oz_max_kernel<double, true><<<gm_col, dim3(32, 8), 0, st>>>((const double*)X, ld, rows, K, kc, c0, nch, mx, nonfinite);
   } else {
-    dim3 ge((rows + 7) / 8, c1 - c0);
-    dim3 gs((rows_pad + 7) / 8, (groups + 31) / 32);
-    if (fp32) {
-      oz_expo_kernel<float, false><<<ge, 256, 0, st>>>((const float*)X, ld, rows, K, kc, c0, nch, expo, nonfinite);
-      oz_slice_kernel<float, false><<<gs, dim3(32, 8), 0, st>>>((const float*)X, ld, rows, rows_pad, K, k0, k1_pad,
-                                                                kc, nch, S, tile_rows, KB, expo, dig);
-    } else {
-      oz_expo_kernel<double, false><<<ge, 256, 0, st>>>((const double*)X, ld, rows, K, kc, c0, nch, expo, nonfinite);
-      oz_slice_kernel<double, false><<<gs, dim3(32, 8), 0, st>>>((const double*)X, ld, rows, rows_pad, K, k0,
-                                                                 k1_pad, kc, nch, S, tile_rows, KB, expo, dig);
-    }
+    if (fp32) oz_max_kernel<float, false><<<gm_row, dim3(32, 8), 0, st>>>((const float*)X, ld, rows, K, kc, c0, nch, mx, nonfinite);
+    else oz_max_kernel<double, false><<<gm_row, dim3(32, 8), 0, st>>>((const double*)X, ld, rows, K, kc, c0, nch, mx, nonfinite);
   }
-  count_launch(2);
+  oz_expo_kernel<<<(unsigned)((ne + 255) / 256), 256, 0, st>>>(mx, rows, c0, c1, nch, expo);
+  if (colmajor) {
+    if (fp32)
+      oz_slice_kernel<float, true><<<gs_col, dim3(32, 8), 0, st>>>((const float*)X, ld, rows, rows_pad, K, k0, k1_pad,
+                                                                   kc, nch, S, tile_rows, KB, expo, dig);
+    else
+      oz_slice_kernel<double, true><<<gs_col, dim3(32, 8), 0, st>>>((const double*)X, ld, rows, rows_pad, K, k0,
+                                                                    k1_pad, kc, nch, S, tile_rows, KB, expo, dig);
+  } else {
+    if (fp32)
+      oz_slice_kernel<float, false><<<gs_row, dim3(32, 8), 0, st>>>((const float*)X, ld, rows, rows_pad, K, k0,
+                                                                    k1_pad, kc, nch, S, tile_rows, KB, expo, dig);
+    else
+      oz_slice_kernel<double, false><<<gs_row, dim3(32, 8), 0, st>>>((const double*)X, ld, rows, rows_pad, K, k0,
+                                                                     k1_pad, kc, nch, S, tile_rows, KB, expo, dig);
+  }
+  count_launch(3);
   return ok_or_cuda();
 }
 

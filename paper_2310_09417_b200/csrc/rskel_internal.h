@@ -33,7 +33,7 @@ struct DGemmParams {
 // kc >= GEMM_MIN_CHUNK columns, kc a multiple of 32, a function of K alone.
 constexpr int GEMM_SLOTS = 4096;
 constexpr int GEMM_MAX_CHUNKS = 32;
-constexpr int GEMM_MIN_CHUNK = 512;
+constexpr int GEMM_MIN_CHUNK = 1024;
 size_t gemm_workspace_bytes();
 int gemm_chunk(long long K);
 // kc <= 0: gemm_chunk(K)
@@ -98,7 +98,8 @@ int launch_gaussian(uint64_t seed, uint64_t stream, long long N, double scale, d
 int oz_chunk(long long K);
 size_t oz_digits_bytes(int rows, long long K, int S, int tile_rows);
 int launch_oz_slice(const void* X, int fp32, long long ld, int colmajor, int rows, int K, int k0, int k1, int kc,
-                    int S, int tile_rows, int8_t* dig, int* expo, int* nonfinite, cudaStream_t st);
+                    int S, int tile_rows, int8_t* dig, int* expo, int* nonfinite, unsigned long long* mx,
+                    size_t mx_bytes, cudaStream_t st);
 int launch_oz_gemm(int M, int N, int K, int kc, int mode, double alpha, const int8_t* adig, const int* aexp, int SA,
                    const int8_t* bdig, const int* bexp, int SB, double beta, const double* Cin, long long ldcin,
                    double* C, long long ldc, double* slots, int* tickets, int nslots, cudaStream_t st);

@@ -5,9 +5,9 @@ The full-size tolerance of DESIGN.md section 5: pivots identical up to the first
 tie below the rounding level of the Schur block; over the blocks before it the e_schur trace
 agrees to 1e-12 * ||A||_F while e_schur >= 1e-6 ||A||_F and to 1e-3 relative below (where the
 Schur block is at the fp64 noise floor of the cancellation); once the paths part, rank within +-b, same status; residual
-||A - W A[I]|| / ||A|| within 1% of the oracle's when no pivot parted (25% once they part: a
-different but equally good skeleton set), and within 2 tau / ||A|| (the stop rule's contract)
-for both.  (At n=20000 the first tie is at pivot
+||A - W A[I]|| / ||A|| within 1% of the oracle's when no pivot parted (at most 25% above it
+once they part at equal rank: a different but equally good skeleton set), and within
+2 tau / ||A|| (the stop rule's contract) for both.  (At n=20000 the first tie is at pivot
 12529: profiles/r01_cfg2_full_parity.json, profiles/r01_cfg2_divergence.json.)
 """
 import os
@@ -84,8 +84,10 @@ def test_cfg2_recipe_n6000_vs_oracle():
           f"tau/||A|| {tau / norm_a:.4e}, last e/tau {g_tr[-1][1] / tau:.4f}/{r_tr[-1][1] / tau:.4f}")
     if d.size == 0:  # same skeletons: same residual up to rounding
         assert abs(r_gpu - r_ref) <= 0.01 * r_ref
-    else:  # the paths parted at a near-tie: equally good skeletons, not the same ones
-        assert abs(r_gpu - r_ref) <= 0.25 * r_ref
+    elif res.rank == ref["rank"]:  # parted at a near-tie: equally good skeletons, not the same ones
+        assert r_gpu <= 1.25 * r_ref
+    # (different ranks: the one-block-earlier or -later stop is the estimator's call; the
+    # contract below is what both must meet)
     # the stop rule's contract: e_schur (an unbiased estimate of the squared residual
     # from b Gaussian samples) <= tau; the true residual stays within 2 tau
     assert r_gpu * norm_a <= 2 * tau and r_ref * norm_a <= 2 * tau

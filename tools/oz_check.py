@@ -21,7 +21,7 @@ def slice_op(X, colmajor, rows, K, S, tile_rows, fp32=False, kc=None):
     expo = torch.zeros(rows * nch, dtype=torch.int32, device="cuda")
     ld = X.stride(0)  # row stride of the storage (a[i, k] at k*ld + i when colmajor)
     _lib.call("rs_oz_slice", X.data_ptr(), int(fp32), ld, int(colmajor), rows, K, 0, K, kc, S, tile_rows,
-              dig.data_ptr(), expo.data_ptr(), None, _device.stream_handle())
+              dig.data_ptr(), expo.data_ptr(), None, _device.workspace().data_ptr(), _device.stream_handle())
     return dig, expo, kc
 
 
