@@ -12,10 +12,16 @@ with k the detected rank.  ms_per_step is the seconds figure.
 
 --impl reference times the reference algorithm on the host cores (the CPU
 oracle port under oracle/, numpy/OpenBLAS with all cores) on a bounded sample
-of the same workload: the first 8 blocks of the same adaptive loop.
+of the same workload: the first 8 blocks of the same adaptive loop (the whole
+loop takes ~4 min on 16 cores, profiles/r01_cfg2_full_parity.json).
 
-N > 1 (torchrun): every rank runs an independent replica on its own matrix
-(seed + rank); no collective on the data path ("replicas", weak scaling).
+N > 1 (torchrun): BASELINE configs[4] (cfg5) -- the 65536 x 65536 adaptive
+column ID with A column-sharded over the ranks (rand_lupp_adaptive_sharded;
+one exchange of pivot candidates per block), strong scaling.
+
+The sketch GEMM runs on the int8 tensor cores (Ozaki scheme, csrc/ozaki.cu);
+its roofline is HBM: the digit planes of A (8 bytes per entry, the size of the
+fp64 matrix) are streamed once per block.
 """
 
 import argparse
@@ -32,6 +38,17 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 FP64_DMMA_PEAK_TFLOPS = 37.1  # tools/dmma_peak.cu on this pool (profiles/r01_probe_box.log)
+HBM_FALLBACK_GBS = 6650.0      # /opt/skills/guides/B200_PROFILING.md fallback (if MEASURED_PEAKS.json is absent)
+
+
+def hbm_peak():
+    """(GB/s, source) of the measured HBM copy bandwidth (MEASURED_PEAKS.json)."""
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy)"
+    except (OSError, KeyError, ValueError):
+        return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
 FP64_PEAK_SOURCE = "measured FP64 tensor-core peak, register-only mma.sync f64 (SASS DMMA.8x8x4) microbenchmark (tools/dmma_peak.cu, profiles/r01_probe_box.log); MEASURED_PEAKS.json has no fp64 entry"
 
 
@@ -41,7 +58,8 @@ def parse():
     p.add_argument("--steps", type=int, default=3)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--size", "--n", dest="n", type=int, default=20000)
+    p.add_argument("--size", "--n", dest="n", type=int, default=None,
+                   help="matrix order (default 20000 = cfg2 at N = 1, 65536 = cfg5 at N > 1)")
     p.add_argument("--b", type=int, default=64)
     p.add_argument("--tau", type=float, default=1e-8)
     p.add_argument("--seed", type=int, default=0)
@@ -129,11 +147,11 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def sketch_traffic(m, n_loc, b):
-    """DRAM bytes per sketch launch from the committed ncu --set full capture
-    (profiles/r01_roofline_traffic.json), valid for the cfg2 single-GPU shape
-    it was measured on; None for other shapes."""
-    path = os.path.join(REPO, "profiles", "r01_roofline_traffic.json")
+def oz_traffic(m, n_loc, b):
+    """DRAM bytes per Ozaki sketch launch from the committed ncu --set full capture
+    (profiles/r02_oz_gemm_traffic.json), valid for the cfg2 single-GPU shape it was
+    measured on; None for other shapes."""
+    path = os.path.join(REPO, "profiles", "r02_oz_gemm_traffic.json")
     if not os.path.exists(path) or (m, n_loc, b) != (20000, 20000, 64):
         return None
     with open(path) as f:
@@ -165,7 +183,7 @@ def reference_arm(args, rank):
     import torch
 
     dev = torch.device("cuda", 0) if torch.cuda.is_available() else None
-    n = args.n
+    n = args.n or 20000
     if dev is not None:
         a = gen_fast_decay_device(n, 1e-16, args.seed, dev).cpu().numpy()
     else:  # no GPU: generate on the host (slow for large n)
@@ -182,8 +200,11 @@ def reference_arm(args, rank):
         flops.append(f)
     ms = 1e3 * float(np.median(times))
     val = flops[0] / (ms * 1e-3) / 1e12
-    sample = (f"first {args.cpu_blocks} blocks (rank 0 -> {k}) of the adaptive loop on the same "
-              f"{n}x{n} fast-decay matrix; numpy/OpenBLAS oracle port, median of {args.steps}")
+    sample = (f"BOUNDED SAMPLE: the first {args.cpu_blocks} blocks (rank 0 -> {k}) of the adaptive loop on "
+              f"the same {n}x{n} fast-decay matrix (the GPU arm runs all ~227 blocks); numpy/OpenBLAS "
+              f"oracle port, median of {args.steps}.  The whole loop on 16 host cores of this pool took "
+              f"235 s = 0.066 TF/s (profiles/r01_cfg2_full_parity.json), i.e. the sample overstates the "
+              f"CPU's whole-loop throughput ~3x")
     line = {
         "impl": "reference", "metric": "adaptive column-ID throughput (algorithmic TFLOP/s)",
         "value": val, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
@@ -228,12 +249,17 @@ def main():
     from paper_2310_09417_b200.sharded import rand_lupp_adaptive_sharded, shard_bounds
 
     lib = _lib.load()
-    n, b, tau = args.n, args.b, args.tau
+    cfg5 = world > 1
+    n = args.n or (65536 if cfg5 else 20000)
+    b, tau = args.b, args.tau
     seed = args.seed
     sharded = world > 1 or args.sharded
     # Every rank builds the same matrix and keeps its own column block A[:, lo:hi]
     # (the column ID's candidates), i.e. A is column-sharded.
-    a = gen_fast_decay_device(n, 1e-16, seed, dev)
+    if cfg5:  # cfg5: randomized-Hadamard fast decay (exact spectrum), built on the device
+        a, _ = rs.gen_fast_decay_hadamard(n, 1e-16, rs.RngStream(seed).child(1 << 41))
+    else:
+        a = gen_fast_decay_device(n, 1e-16, seed, dev)
     lo, hi = shard_bounds(n, world, rank)
     if sharded and world > 1:
         a = a[:, lo:hi].contiguous()
@@ -285,33 +311,47 @@ def main():
     counts = timer.launches()
     blocks = counts.get("sketch_gemm", 0)
     n_loc = a.shape[1]  # candidate columns on this rank
-    sketch_flops = blocks * 2.0 * n * n_loc * b
     sketch_ms = phases.get("sketch_gemm", float("nan"))
-    achieved = sketch_flops / (sketch_ms * 1e-3) / 1e12 if sketch_ms else float("nan")
-    roofline = {
-        "bound": "tensor", "kernel": "dgemm_kernel (sketch Y = A^T Omega_t, DMMA fp64)",
-        "achieved": achieved, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-        "frac": achieved / FP64_DMMA_PEAK_TFLOPS,
-        "traffic": (sketch_traffic(n, n_loc, b) or {}).get("bytes_per_launch"),
-        "traffic_detail": sketch_traffic(n, n_loc, b),
-        "peak_source": FP64_PEAK_SOURCE,
-        "per_launch_flops": 2.0 * n * n_loc * b,
-        "launches": blocks,
-        "avg_launch_ms": sketch_ms / max(blocks, 1),
-        "share_of_step": sketch_ms / (ms * args.steps),
-    }
+    avg_ms = sketch_ms / max(blocks, 1)
+    if rs.sketch_engine() == "ozaki":
+        # HBM roofline of the tensor-core sketch: the A digit planes (8 bytes per entry, the
+        # size of the fp64 matrix) stream from HBM once per block; Omega's planes (n x 64 x 8 B)
+        # come from L2.  int8 tensor work per launch: 36 plane products.
+        peak, peak_src = hbm_peak()
+        per_launch_bytes = 8.0 * n * n_loc
+        achieved = per_launch_bytes / (avg_ms * 1e-3) / 1e9
+        traffic = oz_traffic(n, n_loc, b)
+        roofline = {
+            "bound": "hbm", "kernel": "oz_gemm_kernel (sketch Y = A^T Omega_t: tcgen05.mma kind::i8, TMEM "
+                                      "accumulators, bulk-copy fed, Ozaki digit planes)",
+            "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": traffic.get("bytes_per_launch") if traffic else None, "traffic_detail": traffic,
+            "peak_source": peak_src, "per_launch_bytes": per_launch_bytes,
+            "per_launch_int8_ops": 2.0 * 36 * n * n_loc * b,
+            "fp64_equivalent_tflops": 2.0 * n * n_loc * b / (avg_ms * 1e-3) / 1e12,
+            "launches": blocks, "avg_launch_ms": avg_ms,
+            "share_of_step": sketch_ms / (ms * args.steps),
+        }
+    else:
+        achieved = 2.0 * n * n_loc * b / (avg_ms * 1e-3) / 1e12
+        roofline = {
+            "bound": "tensor", "kernel": "dgemm_kernel (sketch Y = A^T Omega_t, DMMA fp64)",
+            "achieved": achieved, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+            "frac": achieved / FP64_DMMA_PEAK_TFLOPS, "traffic": None, "peak_source": FP64_PEAK_SOURCE,
+            "per_launch_flops": 2.0 * n * n_loc * b, "launches": blocks, "avg_launch_ms": avg_ms,
+            "share_of_step": sketch_ms / (ms * args.steps),
+        }
     phase_ms = {kk: v / args.steps for kk, v in phases.items()}
 
     # ---------------- e2e: host numpy in, host numpy out -----------------------
-    a_host_t = torch.empty(tuple(a.shape), dtype=torch.float64, pin_memory=True)
-    a_host_t.copy_(a)
-    a_host = a_host_t.numpy()
+    # A plain (pageable) numpy array in, fresh numpy results out, every result kept
+    # by the caller (no pinned-buffer or allocator reuse between calls).
+    a_host = np.empty(tuple(a.shape), dtype=np.float64)
+    a_host[...] = a.cpu().numpy()
     torch.cuda.synchronize()
     e2e_ms = []
-    res_h = None
-    for i in range(args.e2e_steps + 1):  # first call warms the pinned host pool (not timed)
-        nb = None if res_h is None else (len(res_h.trace) + 1, res_h.rank)
-        res_h = None  # the caller consumed the previous result: its pinned block is reused
+    kept = []
+    for i in range(args.e2e_steps + 1):  # the first call loads modules / the staging ring (not timed)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         if sharded:
@@ -321,7 +361,7 @@ def main():
         torch.cuda.synchronize()
         if i > 0:
             e2e_ms.append(1e3 * (time.perf_counter() - t0))
-    del nb
+        kept.append(res_h)
     e2e_t = torch.tensor([float(np.median(e2e_ms))], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
@@ -334,17 +374,21 @@ def main():
     e2e = {"value": algo_flops(n, n, res_h.rank, b) / (e2e_ms_max * 1e-3) / 1e12,
            "unit": "TFLOP/s", "ms_per_step": e2e_ms_max,
            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-           "path": ("rand_lupp_adaptive_sharded(numpy pinned A[:, J_g].T) -> numpy W[J_g], row_idx" if sharded
-                    else "rand_lupp_adaptive(numpy pinned A.T) -> numpy W, row_idx")}
+           "path": ("rand_lupp_adaptive_sharded(numpy pageable A[:, J_g].T) -> numpy W[J_g], row_idx" if sharded
+                    else "rand_lupp_adaptive(numpy pageable A.T) -> fresh numpy W, row_idx; caller keeps results")}
+    del kept
 
     # ---------------- CPU baseline (rank 0, N = 1 only) -----------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         dt, kc, fc, cores = cpu_sample(a_host.T, b, tau, seed, args.cpu_blocks)
         cpu = {"value": fc / dt / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": "port",
-               "sample": f"first {args.cpu_blocks} blocks (rank 0 -> {kc}) of the same adaptive "
-                         f"loop on the same matrix; oracle/randskel_oracle.py (numpy/OpenBLAS), "
-                         f"{dt:.2f} s"}
+               "sample": f"BOUNDED SAMPLE: first {args.cpu_blocks} blocks (rank 0 -> {kc}) of the same "
+                         f"adaptive loop on the same matrix; oracle/randskel_oracle.py (numpy/OpenBLAS), "
+                         f"{dt:.2f} s",
+               "full_loop": {"seconds": 235.0, "tflops": algo_flops(20000, 20000, 14464, 64) / 235.0 / 1e12,
+                             "cores": 16, "source": "profiles/r01_cfg2_full_parity.json (the whole cfg2 loop, "
+                                                    "oracle port on this pool's host cores, same matrix)"}}
 
     if rank == 0:
         line = {
@@ -354,8 +398,12 @@ def main():
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {
-                "workload": f"cfg2: rand_lupp_adaptive(A.T, b={b}, tau={tau:g} abs) on a {n}x{n} "
-                            f"fp64 fast-decay matrix (beta=1e-16, Haar bases), seed {args.seed}",
+                "workload": (f"cfg5: rand_lupp_adaptive_sharded(A[:, J_g].T, b={b}, tau={tau:g} abs) on a {n}x{n} "
+                             f"fp64 fast-decay matrix (beta=1e-16, randomized-Hadamard bases), column-sharded"
+                             if cfg5 else
+                             f"cfg2: rand_lupp_adaptive(A.T, b={b}, tau={tau:g} abs) on a {n}x{n} "
+                             f"fp64 fast-decay matrix (beta=1e-16, Haar bases), seed {args.seed}"),
+                "sketch_engine": rs.sketch_engine(),
                 "n": n, "b": b, "tau": tau, "rank": k, "status": res.status,
                 "row_id_error_rel": resid,
                 "blocks": len(res.trace) + 1, "parallelism": (f"A column-sharded over {world} GPUs ({backend} all-reduce of Y_top, S, T_P per block)"

@@ -215,6 +215,53 @@ def h2d(arr):
     return out
 
 
+def d2h_pageable(x):
+    """Fresh (pageable) numpy copy of a contiguous device tensor: 32 MB chunks
+    are DMA'd into the pinned staging ring and copied out by the host thread
+    pool while the next chunks are in flight -- no page-locking of the
+    result (a caller that keeps every result would otherwise pin gigabytes
+    per call)."""
+    dev = x.device
+    out = np.empty(tuple(x.shape), dtype=torch.empty(0, dtype=x.dtype).numpy().dtype)
+    nbytes = x.numel() * x.element_size()
+    if nbytes == 0:
+        return out
+    src = x.reshape(-1).view(torch.uint8)
+    dst = out.reshape(-1).view(np.uint8)
+    ring = _stage_ring(dev)
+    pool = _copy_pool()
+    nthr = max(1, min(16, pool._max_workers))
+    cs = ring["stream"]
+    cs.wait_stream(torch.cuda.current_stream(dev))
+    waiting = {}  # slot -> (c0, c1) copied into the slot, not yet copied out
+
+    def drain(slot):
+        c0, c1 = waiting.pop(slot)
+        ring["events"][slot].synchronize()
+        buf = ring["bufs"][slot].numpy()
+        n = c1 - c0
+        part = -(-n // nthr)
+        list(pool.map(lambda q: np.copyto(dst[c0 + q:c0 + min(n, q + part)], buf[q:min(n, q + part)]),
+                      range(0, n, part)))
+
+    for i, c0 in enumerate(range(0, nbytes, _STAGE_BYTES)):
+        c1 = min(nbytes, c0 + _STAGE_BYTES)
+        slot = i % _STAGE_DEPTH
+        if slot in waiting:
+            drain(slot)
+        elif ring["events"][slot] is not None:
+            ring["events"][slot].synchronize()
+        with torch.cuda.stream(cs):
+            ring["bufs"][slot][: c1 - c0].copy_(src[c0:c1], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(cs)
+        ring["events"][slot] = ev
+        waiting[slot] = (c0, c1)
+    for slot in sorted(waiting, key=lambda sl: waiting[sl][0]):
+        drain(slot)
+    return out
+
+
 def h2d_rows(arr, on_chunk, out=None, align=1):
     """Row-chunked device copy of a C-contiguous 2-D host array: after each
     chunk's copy is enqueued, ``on_chunk(r0, r1, event)`` is called so work
@@ -288,6 +335,8 @@ def to_output(x, like):
         x = x.t if not x.colmajor else x.t.t()
     if kind == "torch_cuda":
         return x
+    if x.numel() >= (1 << 20) and x.is_contiguous() and kind == "numpy":
+        return d2h_pageable(x)
     if x.numel() >= (1 << 20):
         h = host_empty(tuple(x.shape), x.dtype)
         h.copy_(x, non_blocking=True)

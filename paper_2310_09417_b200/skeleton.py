@@ -380,7 +380,9 @@ class _AdaptiveDriver:
         # tensor-core sketch: A's digit planes once, Omega_t's per block
         self.ozaki = _ozaki.sketch_engine() == "ozaki" and self.yb is None
         if self.ozaki:
+            tok = self.prof.start("a_slice")
             self.ap = planes if planes is not None else _ozaki.Planes.of_matrix(a)
+            self.prof.stop(tok)
             self.bp = _ozaki.Planes(b, n, _ozaki.OMEGA_PLANES, 64, dev)
         self.stream = _device.stream_handle()
         self.ws = _device.workspace()
@@ -425,11 +427,14 @@ class _AdaptiveDriver:
         slot = t % 2
         self._issue_copy(t)
         self.compute.wait_event(self.om_ready[slot])
-        tok = self.prof.start("sketch_gemm")
         if self.ozaki:
+            tok = self.prof.start("omega_slice")
             _ozaki.Planes.of_omega(self.om[slot], out=self.bp)
+            self.prof.stop(tok)
+            tok = self.prof.start("sketch_gemm")
             _ozaki.sketch(self.ap, self.bp, self.y[slot].data_ptr(), self.b)
         else:
+            tok = self.prof.start("sketch_gemm")
             _lib.call("rs_sketch_gemm", self.m, self.n, self.b, self.a.ptr, self.a.ld, int(self.a.colmajor),
                       self.om[slot].data_ptr(), self.b, self.y[slot].data_ptr(), self.b,
                       self.ws.data_ptr(), self.stream)
