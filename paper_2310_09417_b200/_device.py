@@ -41,11 +41,14 @@ class Matrix:
     (row-major) or ``base[j*ld + i]`` (column-major).  ``kind`` records the
     caller's container so results can be returned the same way."""
 
-    __slots__ = ("t", "rows", "cols", "ld", "colmajor", "kind", "off")
+    __slots__ = ("t", "rows", "cols", "ld", "colmajor", "kind", "off", "src32")
 
     def __init__(self, t, rows, cols, ld, colmajor, kind, off=0):
         self.t, self.rows, self.cols, self.ld, self.colmajor, self.kind = t, rows, cols, ld, colmajor, kind
         self.off = off  # element offset of (0, 0) from t.data_ptr()
+        # fp32 input: the caller's values as fp32 on the device (same layout and ld),
+        # read directly by the tensor-core sketch; t holds the exact fp64 upcast
+        self.src32 = None
 
     @property
     def ptr(self):
@@ -57,7 +60,9 @@ class Matrix:
 
     @property
     def T(self):
-        return Matrix(self.t, self.cols, self.rows, self.ld, not self.colmajor, self.kind, self.off)
+        m = Matrix(self.t, self.cols, self.rows, self.ld, not self.colmajor, self.kind, self.off)
+        m.src32 = self.src32.T if self.src32 is not None else None
+        return m
 
     def sub(self, r0, c0, rows, cols):
         """View of the block [r0:r0+rows, c0:c0+cols] (no copy)."""
@@ -137,9 +142,15 @@ def as_matrix(a, name="matrix"):
                 a = h2d(a.t().numpy()).t()
             else:
                 a = h2d(a.contiguous().numpy())
+        a32 = a if a.dtype == torch.float32 else None
         if a.dtype != torch.float64:
             a = a.to(torch.float64)
-        return _from_tensor_2d(a, kind)
+        m = _from_tensor_2d(a, kind)
+        if a32 is not None:
+            m.src32 = _from_tensor_2d(a32, kind)
+            if (m.src32.colmajor, m.src32.ld) != (m.colmajor, m.ld):  # layouts must agree
+                m.src32 = None
+        return m
     arr = np.asarray(a)
     if arr.dtype not in (np.float32, np.float64):
         arr = arr.astype(np.float64)
@@ -149,10 +160,16 @@ def as_matrix(a, name="matrix"):
         arr = np.ascontiguousarray(arr)
     colmajor = not arr.flags.c_contiguous
     t = h2d(arr.T if colmajor else arr)
+    t32 = None
     if t.dtype != torch.float64:  # fp32 input: upcast on the device (half the H2D bytes)
+        t32 = t
         t = t.to(torch.float64)
     rows, cols = arr.shape
-    return Matrix(t, rows, cols, max(rows if colmajor else cols, 1), colmajor, "numpy")
+    ld = max(rows if colmajor else cols, 1)
+    m = Matrix(t, rows, cols, ld, colmajor, "numpy")
+    if t32 is not None:
+        m.src32 = Matrix(t32, rows, cols, ld, colmajor, "numpy")
+    return m
 
 
 # ------------------------------------------------------------- host -> device --

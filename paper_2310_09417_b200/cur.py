@@ -90,7 +90,7 @@ def _jacobi_svd_t(Xt):
     return Vt
 
 
-def _pinv_apply_dev(A, B):
+def _pinv_apply_dev(A, B, b_planes=None):
     """x = A^+ B (A: Matrix p x q, B: Matrix p x r, any layouts) -> row-major tensor q x r.
 
     Tall A (p > 2q, q <= 1024) is first compressed to q x q: LUPP of A gives the
@@ -102,13 +102,13 @@ def _pinv_apply_dev(A, B):
     badly conditioned W falls back to Jacobi on A itself."""
     p, q = A.shape
     if p > 2 * q and 2 <= q <= 1024:
-        x = _pinv_apply_compressed(A, B)
+        x = _pinv_apply_compressed(A, B, b_planes)
         if x is not None:
             return x
     return _pinv_apply_jacobi(A, B)
 
 
-def _pinv_apply_compressed(A, B):
+def _pinv_apply_compressed(A, B, b_planes=None):
     p, q = A.shape
     r = B.cols
     dev = _device.device()
@@ -128,7 +128,15 @@ def _pinv_apply_compressed(A, B):
     M = torch.empty((q, q), dtype=torch.float64, device=dev)
     dense._gemm(dense._mat(M), Rw, A_I)                  # M = R_W A[I]
     # H = W^T B (q x r) without transposing a large column-major B
-    if B.colmajor:
+    if B.colmajor and b_planes is not None and b_planes.rows == r and b_planes.K == p:
+        # B^T is the sketched matrix itself: H^T = B^T W on the int8 tensor cores,
+        # from the digit planes the sketches already used (csrc/ozaki.cu)
+        from . import _ozaki
+
+        Ht = torch.empty((r, q), dtype=torch.float64, device=dev)
+        _ozaki.sketch(b_planes, _ozaki.Planes.of_omega(W), Ht.data_ptr(), q)
+        H = dense._mat(Ht).T.row_major()
+    elif B.colmajor:
         Ht = torch.empty((r, q), dtype=torch.float64, device=dev)
         dense._gemm(dense._mat(Ht), B.T, Wm)             # H^T = B^T W
         H = dense._mat(Ht).T.row_major()
@@ -319,12 +327,12 @@ def cur_decompose(a, k, spec, rng):
     return _cur_from_rows(A, ridx, k, r.row_idx)
 
 
-def _cur_from_rows(A, ridx, k, row_idx_out):
+def _cur_from_rows(A, ridx, k, row_idx_out, planes=None):
     cidx, _ = _column_skeletons_from_rows(A, ridx, k)
     C = _cols(A, cidx)                   # m x k
     R = _rows(A, ridx)                   # k x n
     # a R^+ = pinv_apply(R^T, a^T)^T ;  u_mid = pinv_apply(C, a R^+)
-    arp_t = _pinv_apply_dev(R.T, A.T)    # k x m  (= (a R^+)^T)
+    arp_t = _pinv_apply_dev(R.T, A.T, b_planes=planes)    # k x m  (= (a R^+)^T)
     u_mid = _pinv_apply_dev(C, dense._mat(arp_t).T)
     S = _cols(R, cidx)
     status = STATUS_ILL_CONDITIONED if _cond1(S) > COND_LIMIT else STATUS_OK
@@ -342,10 +350,13 @@ def cur_decompose_adaptive(a, b, tau, spec, rng, max_rank=None):
     detected rank).  fp32 inputs are upcast to fp64 like the reference
     (`skeleton.py:200-204`).  Returns ``(CurFactors, SkeletonResult)``.
     """
-    from .skeleton import rand_lupp_adaptive
+    from . import _ozaki
+    from .skeleton import _adaptive_device
 
     A = _device.as_matrix(a)
-    res = rand_lupp_adaptive(A, b, tau, spec, rng, max_rank=max_rank)
+    # the digit planes of A serve both the sketches and the A R^+ product
+    planes = _ozaki.Planes.of_matrix(A) if _ozaki.sketch_engine() == "ozaki" else None
+    res = _adaptive_device(A, b, tau, spec, rng, max_rank=max_rank, planes=planes)
     ridx = _idx(res.row_idx)
-    cur = _cur_from_rows(A, ridx, res.rank, res.row_idx)
+    cur = _cur_from_rows(A, ridx, res.rank, res.row_idx, planes=planes)
     return cur, res

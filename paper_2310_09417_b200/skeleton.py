@@ -154,6 +154,24 @@ def column_id(a, k, spec, rng):
     return SkeletonResult(rank=k, col_idx=_device.to_host_index(idx, a.kind), x=x.T)
 
 
+def _checked_max_rank(m, n, b, tau, max_rank):
+    if tau <= 0:
+        raise ValueError(f"tau must be positive, got {tau}")
+    if not 1 <= b <= min(m, n):
+        raise DimensionError(f"block size must be in [1, {min(m, n)}], got {b}")
+    if max_rank is None:
+        max_rank = max(b, min(m, n) - b)
+    return min(max_rank, min(m, n))
+
+
+def _adaptive_device(A, b, tau, spec, rng, max_rank=None, planes=None):
+    """`rand_lupp_adaptive` on a device Matrix, optionally with its digit
+    planes already cut (cur.cur_decompose_adaptive reuses them)."""
+    m, n = A.shape
+    max_rank = _checked_max_rank(m, n, b, tau, max_rank)
+    return _AdaptiveDriver(A, b, tau, rng, max_rank, spec=spec, planes=planes).run()
+
+
 def rand_lupp_adaptive(a, b, tau, spec, rng, max_rank=None):
     """Adaptive blockwise LUPP row skeletons to absolute Frobenius tolerance tau.
 
