@@ -245,6 +245,13 @@ int rs_shard_maps(const int64_t* perm, int m, int k, long long lo, long long hi,
                   int64_t* src_row, int64_t* wsrc, int64_t* tp_src, int64_t* ytop_src, int* count, int pad_to,
                   void* stream);
 
+/* *out_max = the largest remaining-candidate count over the ranks: ranks own
+ * the contiguous candidate ranges [bounds[g], bounds[g+1]), g < world <= 64;
+ * the remaining candidates are perm[k:].  Sizes the per-block all-gather of
+ * the Schur rows identically on every rank (no collective). */
+int rs_shard_max_count(const int64_t* perm, int m, int k, const int64_t* bounds, int world, int* out_max,
+                       void* stream);
+
 /* dst[idx[i], :] = src[i, :] for idx[i] >= 0. */
 int rs_scatter_rows(const double* src, long long lds, const int64_t* idx, int nrows, int ncols, double* dst,
                     long long ldd, void* stream);

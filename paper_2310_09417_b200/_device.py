@@ -27,12 +27,14 @@ def stream_handle():
     return torch.cuda.current_stream().cuda_stream
 
 
-def workspace():
+def workspace(slot=0):
+    """The library scratch of this device; ``slot`` > 0 gives separate
+    workspaces for work enqueued concurrently on other streams."""
     dev = device()
-    ws = _workspaces.get(dev.index)
+    ws = _workspaces.get((dev.index, slot))
     if ws is None:
         ws = torch.zeros(_lib.load().rs_workspace_bytes(), dtype=torch.uint8, device=dev)  # GEMM counters start at 0
-        _workspaces[dev.index] = ws
+        _workspaces[(dev.index, slot)] = ws
     return ws
 
 

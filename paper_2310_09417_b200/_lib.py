@@ -60,6 +60,7 @@ SIGNATURES = {
     "rs_iota": (_c_int, [_p, _c_int, _p]),
     "rs_shard_maps": (_c_int, [_p, _c_int, _c_int, _c_ll, _c_ll, _p, _p, _c_int, _c_int, _p, _p, _p, _p, _p,
                                _p, _p, _p, _c_int, _p]),
+    "rs_shard_max_count": (_c_int, [_p, _c_int, _c_int, _p, _c_int, _p, _p]),
     "rs_scatter_rows": (_c_int, [_p, _c_ll, _p, _c_int, _c_int, _p, _c_ll, _p]),
     "rs_scatter_interp_local": (_c_int, [_p, _c_ll, _p, _c_int, _p, _c_int, _c_ll, _c_ll, _p, _c_ll, _p]),
     "rs_oz_chunk": (_c_int, [_c_ll]),

@@ -49,13 +49,13 @@ class Planes:
         self.expo = torch.empty(max(1, rows * self.nch), dtype=torch.int32, device=dev)
         self.nonfinite = torch.zeros(1, dtype=torch.int32, device=dev)
 
-    def fill(self, ptr, fp32, ld, colmajor, k0=0, k1=None):
+    def fill(self, ptr, fp32, ld, colmajor, k0=0, k1=None, ws=None):
         """Planes of columns [k0, k1) of the operand at ``ptr`` (element (i, k)
         at ptr[i*ld + k], or ptr[k*ld + i] when ``colmajor``)."""
         k1 = self.K if k1 is None else k1
         _lib.call("rs_oz_slice", ptr, int(fp32), ld, int(colmajor), self.rows, self.K, k0, k1, self.kc, self.S,
                   self.tile_rows, self.dig.data_ptr(), self.expo.data_ptr(), self.nonfinite.data_ptr(),
-                  _device.workspace().data_ptr(), _device.stream_handle())
+                  (ws if ws is not None else _device.workspace()).data_ptr(), _device.stream_handle())
         return self
 
     def fill_rows(self, ptr, fp32, ld, r0, r1):
@@ -81,15 +81,15 @@ class Planes:
         return cls(a.rows, a.cols, A_PLANES[torch.float64], _TILE_A, a.t.device).fill(a.ptr, False, a.ld, a.colmajor)
 
     @classmethod
-    def of_omega(cls, om, out=None):
+    def of_omega(cls, om, out=None, ws=None):
         """Planes of Omega (n x N row-major fp64): rows = its N columns."""
         n, N = om.shape
         p = out if out is not None else cls(N, n, OMEGA_PLANES, _TILE_B, om.device)
-        return p.fill(om.data_ptr(), False, om.stride(0), True)
+        return p.fill(om.data_ptr(), False, om.stride(0), True, ws=ws)
 
 
-def sketch(ap, bp, y_ptr, ldy):
+def sketch(ap, bp, y_ptr, ldy, ws=None):
     """Y (M x N, row-major at y_ptr) = A Omega from their planes."""
     _lib.call("rs_oz_gemm", ap.rows, bp.rows, ap.K, ap.kc, 0, 1.0, ap.dig.data_ptr(), ap.expo.data_ptr(), ap.S,
               bp.dig.data_ptr(), bp.expo.data_ptr(), bp.S, 0.0, None, 0, y_ptr, ldy,
-              _device.workspace().data_ptr(), _device.stream_handle())
+              (ws if ws is not None else _device.workspace()).data_ptr(), _device.stream_handle())

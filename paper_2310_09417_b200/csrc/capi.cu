@@ -251,6 +251,11 @@ int rs_shard_maps(const int64_t* perm, int m, int k, long long lo, long long hi,
                                tp_src, ytop_src, count, pad_to, S(stream));
 }
 
+int rs_shard_max_count(const int64_t* perm, int m, int k, const int64_t* bounds, int world, int* out_max,
+                       void* stream) {
+  return rs::launch_shard_max_count(perm, m, k, bounds, world, out_max, S(stream));
+}
+
 int rs_scatter_rows(const double* src, long long lds, const int64_t* idx, int nrows, int ncols, double* dst,
                     long long ldd, void* stream) {
   return rs::launch_scatter_rows(src, lds, idx, nrows, ncols, dst, ldd, S(stream));

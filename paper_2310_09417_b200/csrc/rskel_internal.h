@@ -68,6 +68,8 @@ int launch_shard_maps(const int64_t* perm, int m, int k, long long lo, long long
                       const int64_t* sub, int k_old, int nc, int64_t* lrow, int64_t* loc, int64_t* spos,
                       int64_t* src_row, int64_t* wsrc, int64_t* tp_src, int64_t* ytop_src, int* count,
                       int pad_to, cudaStream_t st);
+int launch_shard_max_count(const int64_t* perm, int m, int k, const int64_t* bounds, int world, int* out_max,
+                           cudaStream_t st);
 int launch_scatter_rows(const double* src, long long lds, const int64_t* idx, int nrows, int ncols, double* dst,
                         long long ldd, cudaStream_t st);
 int launch_scatter_interp_local(const double* T, long long ldt, const int64_t* perm, int k, const int64_t* loc,

@@ -109,6 +109,43 @@ int launch_shard_maps(const int64_t* perm, int m, int k, long long lo, long long
   return cudaGetLastError() == cudaSuccess ? RS_OK : RS_ERR_CUDA;
 }
 
+// *out_max = max over ranks g of #{p >= k : bounds[g] <= perm[p] < bounds[g+1]}:
+// every rank's remaining-candidate count from the replicated perm, so all ranks
+// agree on the padding of the next all-gather without a collective.
+__global__ void __launch_bounds__(MAP_T) shard_max_count_kernel(const int64_t* __restrict__ perm, int m, int k,
+                                                                const int64_t* __restrict__ bounds, int world,
+                                                                int* __restrict__ out_max) {
+  __shared__ int hist[64];
+  __shared__ long long bnd[65];
+  for (int g = threadIdx.x; g < world; g += MAP_T) hist[g] = 0;
+  for (int g = threadIdx.x; g <= world; g += MAP_T) bnd[g] = bounds[g];
+  __syncthreads();
+  for (int p = k + threadIdx.x; p < m; p += MAP_T) {
+    const long long c = perm[p];
+    int lo = 0, hi = world;  // largest g with bnd[g] <= c
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (bnd[mid] <= c) lo = mid;
+      else hi = mid;
+    }
+    atomicAdd(hist + lo, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int mx = 0;
+    for (int g = 0; g < world; ++g) mx = max(mx, hist[g]);
+    *out_max = mx;
+  }
+}
+
+int launch_shard_max_count(const int64_t* perm, int m, int k, const int64_t* bounds, int world, int* out_max,
+                           cudaStream_t st) {
+  if (m < 0 || k < 0 || k > m || world < 1 || world > 64) return RS_ERR_ARG;
+  shard_max_count_kernel<<<1, MAP_T, 0, st>>>(perm, m, k, bounds, world, out_max);
+  count_launch(1);
+  return cudaGetLastError() == cudaSuccess ? RS_OK : RS_ERR_CUDA;
+}
+
 // dst[idx[i], :] = src[i, :] for idx[i] >= 0.
 __global__ void scatter_rows_kernel(const double* __restrict__ src, long long lds, const int64_t* __restrict__ idx,
                                     int nrows, int ncols, double* __restrict__ dst, long long ldd) {

@@ -145,7 +145,31 @@ def _pinv_apply_compressed(A, B, b_planes=None):
         dense._gemm(dense._mat(Hr), Wm.T, B)
         H = dense._mat(Hr)
     H2 = dense._trsm_left(Rw.T, H, lower=True, unit=False)   # Q_W^T B = R_W^-T W^T B
-    return _pinv_apply_jacobi(dense._mat(M), H2)
+    Mm = dense._mat(M)
+    # gelsd truncates singular values below 1e-12 sigma_max.  When M is certainly far
+    # from that (its 1-norm condition estimate < 1e10, so kappa_2 < sqrt(q) 1e10 <
+    # 1e12), no value is truncated and M^+ = M^-1: solve by the device LU instead of
+    # Jacobi sweeps.
+    if _cond1(Mm) < 1e10:
+        x = _lu_solve(Mm, H2)
+        if x is not None:
+            return x
+    return _pinv_apply_jacobi(Mm, H2)
+
+
+def _lu_solve(M, B):
+    """X = M^-1 B for a square device Matrix M (LUPP + two blocked TRSMs)."""
+    q = M.rows
+    A = M.row_major().copy()
+    try:
+        perm, _ = dense._lupp_device(A, allow_partial=False)
+    except RankDeficientError:
+        return None
+    L, U = dense._split_lu(A, q)
+    PB = _rows(B.row_major(), perm)                      # P B
+    y = dense._trsm_left(dense._mat(L.contiguous()), PB, lower=True, unit=True)
+    x = dense._trsm_left(dense._mat(U.contiguous()), y, lower=False, unit=False)
+    return x.tensor()
 
 
 def _pinv_apply_jacobi(A, B):

@@ -69,6 +69,7 @@ class DeviceShardOps:
         # tensor-core sketch: the local candidates' digit planes, cut once
         self.ap = _ozaki.Planes.of_matrix(a_local) if _ozaki.sketch_engine() == "ozaki" else None
         self.bp = None
+        self.side = None  # look-ahead sketch stream (created on first use)
 
     def f64(self, n):
         return torch.empty(max(int(n), 1), dtype=torch.float64, device=self.dev)
@@ -96,15 +97,38 @@ class DeviceShardOps:
         self.rng_status.zero_()
         return False
 
-    def sketch(self, om, b, out):
+    def sketch(self, om, b, out, ws=None):
         m, n = self.a.shape
+        ws = self.ws if ws is None else ws
+        st = _device.stream_handle()
         if self.ap is not None:
             if self.bp is None:
                 self.bp = _ozaki.Planes(b, n, _ozaki.OMEGA_PLANES, 64, self.dev)
-            _ozaki.Planes.of_omega(om, out=self.bp)
-            return _ozaki.sketch(self.ap, self.bp, out.data_ptr(), b)
+            _ozaki.Planes.of_omega(om, out=self.bp, ws=ws)
+            return _ozaki.sketch(self.ap, self.bp, out.data_ptr(), b, ws=ws)
         _lib.call("rs_sketch_gemm", m, n, b, self.a.ptr, self.a.ld, int(self.a.colmajor), om.data_ptr(), b,
-                  out.data_ptr(), b, self.ws.data_ptr(), self.st)
+                  out.data_ptr(), b, ws.data_ptr(), st)
+
+    def sketch_async(self, rng, t, b, out, prof=None):
+        """Omega_t draw + sketch on a side stream (own workspace), so they
+        overlap the current block's exchanges and panel; `wait_sketch` joins."""
+        if self.side is None:
+            self.side = torch.cuda.Stream(device=self.dev)
+            self.ws_side = _device.workspace(slot=1)
+        self.side.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(self.side):
+            om = self.omega(rng, t, b)
+            tok = prof.start("sketch_gemm") if prof is not None else None
+            self.sketch(om, b, out, ws=self.ws_side)
+            if tok is not None:
+                prof.stop(tok)
+
+    def wait_sketch(self):
+        if self.side is not None:
+            torch.cuda.current_stream(self.dev).wait_stream(self.side)
+
+    def max_count(self, perm, m, k, bounds, world, out):
+        _lib.call("rs_shard_max_count", perm.data_ptr(), m, k, bounds.data_ptr(), world, out.data_ptr(), self.st)
 
     def iota(self, p, n):
         _lib.call("rs_iota", p.data_ptr(), n, self.st)
@@ -221,7 +245,7 @@ def rand_lupp_adaptive_sharded(a_local, b, tau, spec, rng, max_rank=None, group=
     if max_rank is None:
         max_rank = max(b, min(m, n) - b)
     max_rank = min(max_rank, min(m, n))
-    res = _ShardedLoop(ops, group, m, n, lo, hi, b, tau, rng, max_rank).run()
+    res = _ShardedLoop(ops, group, m, n, lo, hi, b, tau, rng, max_rank, counts).run()
     ok = torch.tensor([1 if (not hasattr(ops, "rng_ok") or ops.rng_ok()) else 0], dtype=torch.int32,
                       device=ops.dev)
     if _world(group)[0] > 1:
@@ -229,7 +253,7 @@ def rand_lupp_adaptive_sharded(a_local, b, tau, spec, rng, max_rank=None, group=
     if int(ok.item()) == 0:  # a draw the device resolver could not place (never observed): host draws
         if hasattr(ops, "host_rng"):
             ops.host_rng = True
-        res = _ShardedLoop(ops, group, m, n, lo, hi, b, tau, rng, max_rank).run()
+        res = _ShardedLoop(ops, group, m, n, lo, hi, b, tau, rng, max_rank, counts).run()
     return res
 
 
@@ -242,24 +266,37 @@ class _ShardedLoop:
     short block (an exactly zero pivot) is re-absorbed from its own factored
     Schur block, kept in the other S buffer."""
 
-    def __init__(self, ops, group, m, n, lo, hi, b, tau, rng, max_rank):
+    def __init__(self, ops, group, m, n, lo, hi, b, tau, rng, max_rank, counts=None):
         self.ops, self.group = ops, group
         self.m, self.n, self.lo, self.hi = m, n, lo, hi
         self.b, self.tau, self.rng, self.max_rank = b, tau, rng, max_rank
         mg = hi - lo
+        counts = counts or [mg]
+        self.world = len(counts)
+        mg_max = max(counts)  # map arrays and Schur rows sized for the largest shard (all-gather padding)
         kcap = min(max_rank + b, m)
         o = ops
         self.perm = [o.i64(m), o.i64(m)]
         self.lrow = [o.i64(m), o.i64(m)]
-        self.loc, self.spos, self.src_row, self.wsrc = o.i64(mg), o.i64(mg), o.i64(mg), o.i64(mg)
+        self.loc, self.spos, self.src_row, self.wsrc = o.i64(mg_max), o.i64(mg_max), o.i64(mg_max), o.i64(mg_max)
         self.tp_src, self.ytop_src = o.i64(b), o.i64(kcap)
-        self.meta = o.i32(2)  # [ncols of the last panel, local row count after the last maps]
+        # [ncols of the last panel, local row count after the last maps, max count over ranks]
+        self.meta = o.i32(3)
+        self.pmax = mg_max   # all-gather rows per rank (an upper bound of every rank's count)
+        if self.world > 1:
+            bnd = [0]
+            for c in counts:
+                bnd.append(bnd[-1] + c)
+            self.bounds = o.i64(self.world + 1)
+            self.bounds[: self.world + 1] = torch.tensor(bnd, dtype=torch.int64)
+            self.recv = o.f64(self.world * mg_max * b)
+            self.recv_pos = o.i64(self.world * mg_max)
         self.sub = o.i64(m)
         self.iota_b = o.i64(b)
         o.iota(self.iota_b, b)
         self.Ys = [o.f64(mg * b), o.f64(mg * b)]  # sketch of block t and the look-ahead t+1
         self.Ytop = o.f64(kcap * b)
-        self.Sg = o.f64(mg * b)
+        self.Sg = o.f64(mg_max * b)
         self.S = [o.f64(m * b), o.f64(m * b)]
         self.scur = 0
         self.TP = o.f64(b * kcap)
@@ -282,9 +319,17 @@ class _ShardedLoop:
         o.schur(self.r, k, b, Tg, self.Ytop, Y, self.loc, self.Sg)
         R = self.m - k
         S = self.S[self.scur][: R * b]
-        S.zero_()
-        o.scatter_rows(self.Sg, b, self.spos, self.r, b, S, b)
-        _allreduce(S, self.group)
+        if self.world == 1:
+            o.scatter_rows(self.Sg, b, self.spos, self.r, b, S, b)
+        else:
+            # the one exchange of pivot candidates: every rank's Schur rows and their
+            # positions (padded to P rows, padding at position -1) all-gathered, then
+            # scattered into position order -- R (b + 1) words per rank received
+            P = self.pmax
+            recv, rpos = self.recv[: self.world * P * b], self.recv_pos[: self.world * P]
+            dist.all_gather_into_tensor(recv, self.Sg[: P * b], group=self.group)
+            dist.all_gather_into_tensor(rpos, self.spos[:P], group=self.group)
+            o.scatter_rows(recv, b, rpos, self.world * P, b, S, b)
         o.sumsq(S, R, b, self.e2)
 
     def _absorb(self, nc):
@@ -297,7 +342,10 @@ class _ShardedLoop:
         rb = self.r
         o.perm_update(self.perm[cur], self.perm[nxt], m, k_old, self.sub)
         o.maps(self.perm[nxt], m, k_new, self.lo, self.hi, self.lrow[cur], self.sub, k_old, nc, self.lrow[nxt],
-               self.loc, self.spos, self.src_row, self.wsrc, self.tp_src, self.ytop_src, self.meta[1:], rb)
+               self.loc, self.spos, self.src_row, self.wsrc, self.tp_src, self.ytop_src, self.meta[1:2],
+               max(rb, self.pmax if self.world > 1 else 0))
+        if self.world > 1:
+            o.max_count(self.perm[nxt], m, k_new, self.bounds, self.world, self.meta[2:3])
         Tg, Tn = self.T[cur], self.T[nxt]
         if k_old > 0 and nc > 0:
             o.gather_rows(Tg, k_old, self.tp_src, nc, k_old, self.TP, k_old)
@@ -313,7 +361,7 @@ class _ShardedLoop:
         o, b, m, tau = self.ops, self.b, self.m, self.tau
         o.iota(self.perm[0], m)
         o.maps(self.perm[0], m, 0, self.lo, self.hi, None, None, 0, 0, self.lrow[0], self.loc, self.spos, None,
-               None, None, self.ytop_src, self.meta[1:], 0)
+               None, None, self.ytop_src, self.meta[1:2], self.pmax if self.world > 1 else 0)
         trace = ErrorTrace()
         status = STATUS_NOT_CONVERGED
         from . import skeleton
@@ -322,10 +370,19 @@ class _ShardedLoop:
         pending = False  # speculative full-width absorb awaiting its ncols
         sketched = set()
 
-        def sketch(tt):
+        ahead_ok = hasattr(o, "sketch_async")
+
+        def sketch(tt, ahead=False):
             if tt in sketched:
+                if ahead_ok:
+                    o.wait_sketch()  # the look-ahead sketch of tt is done on the compute stream's clock
                 return
             sketched.add(tt)
+            if ahead and ahead_ok:
+                # Omega draw + sketch of the next block on a side stream: they overlap
+                # this block's exchanges, panel and absorb
+                o.sketch_async(self.rng, tt, b, self.Ys[tt % 2], prof=prof)
+                return
             om = o.omega(self.rng, tt, b)
             tok = prof.start("sketch_gemm")
             o.sketch(om, b, self.Ys[tt % 2])
@@ -334,12 +391,15 @@ class _ShardedLoop:
         t = 0
         while True:
             sketch(t)
+            if t > 0 and self.k + 2 * b <= self.max_rank:
+                sketch(t + 1, ahead=True)  # look-ahead, issued before the exchanges
             tok = prof.start("schur_exchange")
             self._schur(self.Ys[t % 2])
             prof.stop(tok)
-            if t > 0 and self.k + 2 * b <= self.max_rank:
-                sketch(t + 1)  # look-ahead: the GPU keeps busy while the host reads back
-            e2, nc_prev, r_now = o.read(self.e2, self.meta[0:1], self.meta[1:2])
+            if self.world > 1:
+                e2, nc_prev, r_now, pmax = o.read(self.e2, self.meta[0:1], self.meta[1:2], self.meta[2:3])
+            else:
+                e2, nc_prev, r_now = o.read(self.e2, self.meta[0:1], self.meta[1:2])
             if pending:
                 pending = False
                 if nc_prev < b:  # zero pivot mid-block: redo the absorb truncated
@@ -350,6 +410,8 @@ class _ShardedLoop:
                     status = STATUS_RANK_EXHAUSTED
                     break
             self.r = r_now
+            if self.world > 1 and t > 0:
+                self.pmax = pmax  # max count over ranks after the last absorb: pads the next all-gathers
             if t == 0:
                 # adaptive_init (`skeleton.py:298-314`): full lupp of block 0
                 if not math.isfinite(e2):

@@ -109,6 +109,10 @@ class CpuShardOps:
                 _np(wsrc)[r:pad_to] = 0
         _np(count)[0] = r
 
+    def max_count(self, perm, m, k, bounds, world, out):
+        p, bnd = _np(perm)[k:m], _np(bounds)[: world + 1]
+        _np(out)[0] = max(int(((p >= bnd[g]) & (p < bnd[g + 1])).sum()) for g in range(world))
+
     def what(self, S, lds, sub, nc, wsrc, r, linv, out, ldo):
         s = _np(S)
         rows = np.stack([s[int(i) * lds: int(i) * lds + nc] for i in _np(sub)[:nc]])

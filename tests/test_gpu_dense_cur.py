@@ -331,5 +331,7 @@ def test_cond1_is_dgecon_estimate_not_exact():
     g = golden("cond1_straddle")
     s = torch.from_numpy(g["s"]).cuda()
     est = cur._cond1(dense._mat(s.contiguous()))
-    assert abs(est - float(g["est"])) <= 1e-6 * float(g["est"])
+    # same iteration path; the solves with a 1e14-conditioned LU differ from LAPACK's at
+    # the kappa * eps level (measured 1.5e-5 relative)
+    assert abs(est - float(g["est"])) <= 1e-3 * float(g["est"])
     assert est < cur.COND_LIMIT < float(g["exact"])
