@@ -38,13 +38,15 @@ def oz(A, colmajor, om, SA=8, SB=8, fp32=False):
 
 def main():
     torch.manual_seed(0)
-    for (M, K, N, colmajor) in [(300, 1000, 64, False), (300, 1000, 64, True), (1000, 5000, 128, True),
-                                (2000, 20000, 64, True)]:
+    for (M, K, N, colmajor, SA, SB) in [(300, 1000, 64, False, 8, 8), (300, 1000, 64, True, 8, 8),
+                                        (1000, 5000, 128, True, 8, 8), (2000, 20000, 64, True, 8, 8),
+                                        (2000, 20000, 64, True, 7, 7), (2000, 20000, 64, True, 7, 8),
+                                        (2000, 65536, 64, True, 8, 8), (2000, 65536, 64, True, 7, 7)]:
         A = torch.randn(M, K, dtype=torch.float64, device="cuda")
         if colmajor:
             A = A.t().contiguous()  # K x M storage: a[i, k] at k*M + i
         om = torch.randn(K, N, dtype=torch.float64, device="cuda") / 8
-        Y, _ = oz(A, colmajor, om)
+        Y, _ = oz(A, colmajor, om, SA=SA, SB=SB)
         torch.cuda.synchronize()
         a = (A.t() if colmajor else A).cpu().numpy()
         o = om.cpu().numpy()
@@ -55,26 +57,26 @@ def main():
         scale = np.abs(a[rows]) @ np.abs(o)
         e_oz = np.max(np.abs(np.longdouble(y) - ref) / scale)
         e_dg = np.max(np.abs(np.longdouble(yd) - ref) / scale)
-        print(f"M={M} K={K} N={N} colmajor={colmajor}: max |err|/(|A||O|): ozaki {float(e_oz):.3e}  openblas {float(e_dg):.3e}",
-              flush=True)
+        print(f"M={M} K={K} N={N} colmajor={colmajor} SA={SA} SB={SB}: max |err|/(|A||O|): ozaki {float(e_oz):.3e}  "
+              f"openblas {float(e_dg):.3e}", flush=True)
     # timing at the cfg2 sketch shape
     n = 20000
     A = torch.randn(n, n, dtype=torch.float64, device="cuda")
     om = torch.randn(n, 64, dtype=torch.float64, device="cuda")
     Y, (ad, ae, bd, be, kc) = oz(A, True, om)
-    for SA in (8, 7):
+    for SA, SB in ((8, 8), (7, 7), (7, 8)):
         for rep in range(2):
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             for _ in range(10):
                 _lib.call("rs_oz_gemm", n, 64, n, kc, 0, 1.0, ad.data_ptr(), ae.data_ptr(), SA, bd.data_ptr(),
-                          be.data_ptr(), 8, 0.0, None, 0, Y.data_ptr(), 64, _device.workspace().data_ptr(),
+                          be.data_ptr(), SB, 0.0, None, 0, Y.data_ptr(), 64, _device.workspace().data_ptr(),
                           _device.stream_handle())
             e1.record()
             torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / 10
-        print(f"oz_gemm 20000x20000x64 SA={SA}: {ms:.3f} ms, {2 * n * n * 64 / ms / 1e9:.1f} fp64-equiv TF/s, "
+        print(f"oz_gemm 20000x20000x64 SA={SA} SB={SB}: {ms:.3f} ms, {2 * n * n * 64 / ms / 1e9:.1f} fp64-equiv TF/s, "
               f"A-plane bytes {SA * n * n / ms / 1e6:.0f} GB/s", flush=True)
     t0 = time.time()
     torch.cuda.synchronize()
