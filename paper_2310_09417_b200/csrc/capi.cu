@@ -39,10 +39,13 @@ rs::DGemmParams gemm_params(int M, int N, int K, double alpha, const double* A, 
                             const double* B, long long ldb, const int64_t* bidx, double beta, const double* Cin,
                             long long ldcin, const int64_t* cidx, double* C, long long ldc, int mode, void* ws) {
   rs::DGemmParams p{M, N, K, A, lda, aidx, B, ldb, bidx, Cin, ldcin, cidx, C, ldc, alpha, beta, mode,
-                    nullptr, nullptr, 0};
+                    nullptr, nullptr, 0, nullptr, nullptr};
   if (ws) {
+    // [slots | boundary slots | tickets | boundary flags]
     p.slots = reinterpret_cast<double*>(W(ws, layout().gemm_off));
-    p.tickets = reinterpret_cast<int*>(p.slots + (size_t)rs::GEMM_SLOTS * 128 * 64);
+    p.bslots = p.slots + (size_t)rs::GEMM_SLOTS * 128 * 64;
+    p.tickets = reinterpret_cast<int*>(p.bslots + (size_t)rs::GEMM_MAX_CTAS * 128 * 64);
+    p.bflags = reinterpret_cast<unsigned*>(p.tickets + rs::GEMM_SLOTS);
     p.nslots = rs::GEMM_SLOTS;
   }
   return p;

@@ -13,6 +13,7 @@
 // Tiling: CTA 128 x 64, DMMA m16n8k4, cp.async multi-stage pipeline, 2 CTAs
 // per SM; the summation order is fixed by K alone (see below).
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -62,12 +63,22 @@ static_assert(CfgRow::THREADS * CfgRow::ACC == SLOT_DOUBLES && CfgCol::THREADS *
 // its row of A, B and K: a row gives the same bits whether it is one of
 // 20000 candidates on one GPU or one of 2500 on rank 3 of 8, whether A is
 // column- or row-major, and whether the K range arrives in one call or in
-// kc-aligned pieces (mode RS_GEMM_FOLD below).  Work units are (tile, chunk)
-// pairs spread over a persistent grid; each writes its partial tile to a
-// slot and the last unit of a tile to arrive (ticket counter) folds the slots
-// in chunk order and applies the epilogue.
+// kc-aligned pieces (mode RS_GEMM_FOLD below).
+//
+// Scheduling (chained stream-K): the tiles x k-tiles work is cut into G equal
+// contiguous ranges, one per persistent CTA, at k-tile granularity -- no wave
+// quantisation whatever M is.  A range cuts chunks at its two ends; the head
+// of a cut chunk belongs to CTA g-1, its tail to CTA g, and the tail must
+// continue the head's DMMA chain.  Each CTA therefore walks its range
+// BACKWARDS: its last piece (a chunk head it hands to g+1) is computed first
+// and published to a boundary slot with a release flag, its first piece (the
+// tail of g-1's head) is computed last, by which time g-1's boundary value is
+// long published.  A completed chunk goes to its (tile, chunk) slot; the last
+// chunk of a tile to arrive (ticket counter) folds the slots in chunk order
+// and applies the epilogue.
 size_t gemm_workspace_bytes() {
-  return sizeof(double) * (size_t)GEMM_SLOTS * SLOT_DOUBLES + sizeof(int) * (size_t)GEMM_SLOTS;
+  return sizeof(double) * (size_t)(GEMM_SLOTS + GEMM_MAX_CTAS) * SLOT_DOUBLES +
+         sizeof(int) * (size_t)(GEMM_SLOTS + GEMM_MAX_CTAS);
 }
 
 int gemm_chunk(long long K) {
@@ -82,7 +93,8 @@ struct ChunkPlan {
   int KT;          // k-tiles of K
   int kct;         // k-tiles per chunk
   int nch;         // chunks
-  int units;       // (tiles of this launch) x nch
+  long long U;     // (tiles of this launch) x KT k-tile units, split over gridDim.x CTAs
+  unsigned epoch;  // boundary-flag value of this launch (flags are never reset)
 };
 
 // Fragment coordinates (within the tile) of accumulator element e of this thread.
@@ -270,9 +282,8 @@ __device__ __forceinline__ void mainloop(const DGemmParams& p, double* As, doubl
   __syncthreads();  // stage buffers are reused by the next unit of this CTA
 }
 
-// Persistent grid over the (tile, chunk) units of one launch: unit u is tile
-// tile0 + u / nch, chunk u % nch; CTA c takes units c, c + G, c + 2G, ...,
-// so the chunks of a tile run side by side and their slots stay in L2.
+// One persistent CTA per range of the tiles x k-tiles work (see "Scheduling"
+// above); pieces are walked backwards.
 template <class C, bool A_COL, bool VEC2>
 __global__ void __launch_bounds__(C::THREADS, C::MINB) dgemm_kernel(DGemmParams p, ChunkPlan pl) {
   extern __shared__ __align__(16) double smem[];
@@ -282,20 +293,50 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) dgemm_kernel(DGemmParams 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int wm = (warp % C::WARPS_M) * C::WTM, wn = (warp / C::WARPS_M) * C::WTN;
+  const int G = gridDim.x, cta = blockIdx.x;
+  const long long u0 = pl.U * cta / G, u1 = pl.U * (cta + 1) / G;
   double acc[C::ACC];
 
-  for (int u = blockIdx.x; u < pl.units; u += gridDim.x) {
-    const int lt = u / pl.nch, ch = u - lt * pl.nch;
+  long long u = u1;
+  while (u > u0) {
+    const int lt = (int)((u - 1) / pl.KT);
+    const int ke = (int)(u - (long long)lt * pl.KT);              // piece end (k-tiles, exclusive)
+    const int ch = (ke - 1) / pl.kct;
+    const int cs = ch * pl.kct, ce = min(pl.KT, cs + pl.kct);
+    const int kb = (int)max((long long)cs, u0 - (long long)lt * pl.KT);  // piece begin
+    u = (long long)lt * pl.KT + kb;
     const int tile = pl.tile0 + lt;
     const int m0 = (tile / pl.tiles_n) * C::BM, n0 = (tile % pl.tiles_n) * C::BN;
-    const int kt0 = ch * pl.kct, kt1 = min(pl.KT, kt0 + pl.kct);
-    if (p.mode == RS_GEMM_CHAIN) {
+
+    if (kb > cs) {
+      // tail of a chunk whose head CTA cta - 1 computed first: continue its chain
+      if (tid == 0) {
+        while (ld_acquire_gpu(p.bflags + cta - 1) != pl.epoch) {
+        }
+      }
+      __syncthreads();
+      const double* src = p.bslots + (size_t)(cta - 1) * SLOT_DOUBLES + tid;
+#pragma unroll
+      for (int e = 0; e < C::ACC; ++e) acc[e] = __ldcg(src + (size_t)e * C::THREADS);
+    } else if (p.mode == RS_GEMM_CHAIN) {
       load_cin<C>(p, m0, n0, wm, wn, g, t, acc);
     } else {
 #pragma unroll
       for (int e = 0; e < C::ACC; ++e) acc[e] = 0.0;
     }
-    mainloop<C, A_COL, VEC2>(p, As, Bs, m0, n0, kt0, kt1, acc);
+    mainloop<C, A_COL, VEC2>(p, As, Bs, m0, n0, kb, ke, acc);
+
+    if (ke < ce) {
+      // head of a chunk continued by CTA cta + 1: publish the chain value
+      double* dst = p.bslots + (size_t)cta * SLOT_DOUBLES + tid;
+#pragma unroll
+      for (int e = 0; e < C::ACC; ++e) __stcg(dst + (size_t)e * C::THREADS, acc[e]);
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) st_release_gpu(p.bflags + cta, pl.epoch);
+      continue;
+    }
+    // the chunk is complete
     if (pl.nch == 1) {
       if (p.mode == RS_GEMM_FOLD) {
         double v[C::ACC];
@@ -309,7 +350,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) dgemm_kernel(DGemmParams 
       continue;
     }
     // element-major slot layout: coalesced stores here and loads in the fold
-    double* slot = p.slots + (size_t)u * SLOT_DOUBLES + tid;
+    double* slot = p.slots + ((size_t)lt * pl.nch + ch) * SLOT_DOUBLES + tid;
 #pragma unroll
     for (int e = 0; e < C::ACC; ++e) __stcg(slot + (size_t)e * C::THREADS, acc[e]);
     __threadfence();
@@ -318,7 +359,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) dgemm_kernel(DGemmParams 
     __syncthreads();
     if (!s_last) continue;
     __threadfence();
-    // last unit of the tile to arrive: fold the chunk partials in chunk order
+    // last chunk of the tile to arrive: fold the chunk partials in chunk order
     const double* base = p.slots + (size_t)lt * pl.nch * SLOT_DOUBLES + tid;
     if (p.mode == RS_GEMM_FOLD) {
       load_cin<C>(p, m0, n0, wm, wn, g, t, acc);
@@ -338,6 +379,14 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) dgemm_kernel(DGemmParams 
   }
 }
 
+// Boundary-flag values: one process-wide counter shared by every kernel
+// instantiation (they share the flag words), never 0 (the zeroed workspace).
+static std::atomic<unsigned> g_epoch{1};
+static unsigned next_epoch() {
+  unsigned e = g_epoch.fetch_add(1);
+  return e != 0 ? e : g_epoch.fetch_add(1);
+}
+
 template <class C, bool A_COL, bool VEC2>
 static int launch_dgemm_t(const DGemmParams& p, int kc, cudaStream_t st) {
   constexpr size_t smem = C::template smem<A_COL>();
@@ -350,18 +399,19 @@ static int launch_dgemm_t(const DGemmParams& p, int kc, cudaStream_t st) {
   pl.tiles_n = (p.N + C::BN - 1) / C::BN;
   const int tiles_m = (p.M + C::BM - 1) / C::BM;
   const long long tiles = (long long)pl.tiles_n * tiles_m;
-  pl.KT = (p.K + C::BK - 1) / C::BK;
+  pl.KT = std::max(1, (p.K + C::BK - 1) / C::BK);  // K = 0: one empty k-tile, so the epilogue runs
   pl.kct = kc / C::BK;
   pl.nch = std::max(1, (pl.KT + pl.kct - 1) / pl.kct);
-  const int slots = nsm * C::MINB;
+  const int slots = std::min(nsm * C::MINB, GEMM_MAX_CTAS);
   // tile groups: as many tiles per launch as the partial slots hold, balanced
   const long long per = pl.nch == 1 ? tiles : std::max<long long>(1, p.nslots / pl.nch);
   const long long ngroups = (tiles + per - 1) / per;
   for (long long gi = 0; gi < ngroups; ++gi) {
     const long long t0 = tiles * gi / ngroups, t1 = tiles * (gi + 1) / ngroups;
     pl.tile0 = (int)t0;
-    pl.units = (int)((t1 - t0) * pl.nch);
-    const int G = std::min(pl.units, slots);
+    pl.U = (t1 - t0) * pl.KT;
+    pl.epoch = next_epoch();
+    const int G = (int)std::min<long long>(std::max<long long>(pl.U, 1), slots);
     dgemm_kernel<C, A_COL, VEC2><<<G, C::THREADS, smem, st>>>(p, pl);
     count_launch(1);
   }

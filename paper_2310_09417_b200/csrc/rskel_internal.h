@@ -27,11 +27,14 @@ struct DGemmParams {
   double* slots;     // partial-tile slots (GEMM_SLOTS x 128 x 64 doubles)
   int* tickets;      // per-tile arrival counters (GEMM_SLOTS ints, zero between launches)
   int nslots;
+  double* bslots;    // chain values handed from CTA g to g + 1 (GEMM_MAX_CTAS slots)
+  unsigned* bflags;  // their release flags (launch epochs)
 };
 
 // Deterministic chunking of K (gemm_f64.cu): at most GEMM_MAX_CHUNKS chunks of
 // kc >= GEMM_MIN_CHUNK columns, kc a multiple of 32, a function of K alone.
 constexpr int GEMM_SLOTS = 4096;
+constexpr int GEMM_MAX_CTAS = 512;  // >= persistent CTAs of one GEMM launch
 constexpr int GEMM_MAX_CHUNKS = 32;
 constexpr int GEMM_MIN_CHUNK = 1024;
 size_t gemm_workspace_bytes();
