@@ -7,6 +7,7 @@ cfg3  adaptive CUR of a 32768 x 16384 fp32 nonnegative low-rank(200)+noise
       matrix, b = 64, tau = 1e-5 ||A||_F (relative; absolute 1e-5 is below the
       fp32 floor)
 cfg4  column_id / rand_lupp of the Kahan 16384^2 matrix (zeta 0.99), k = 1024
+cfg5  adaptive column ID of the 65536^2 randomized-Hadamard fast-decay matrix at 1 GPU
 
 GPU times are CUDA-event times with A resident on the device (median of 3
 after a warm-up) and end-to-end times through the numpy API.  --cpu adds the
@@ -85,15 +86,7 @@ def cfg3(do_cpu):
     import randskel_oracle as orc
 
     m, n, r0, b = 32768, 16384, 200, 64
-    g = torch.Generator(device="cuda")
-    g.manual_seed(0)
-    w = torch.rand(m, r0, generator=g, dtype=torch.float64, device="cuda")
-    h = torch.rand(r0, n, generator=g, dtype=torch.float64, device="cuda")
-    low = w @ h
-    noise = torch.rand(m, n, generator=g, dtype=torch.float64, device="cuda")
-    eta = 1e-6 * torch.linalg.norm(low) / torch.linalg.norm(noise)
-    a32 = (low + eta * noise).to(torch.float32)
-    del low, noise, w, h
+    a32 = rs.gen_nonneg_lowrank(m, n, r0, 1e-6, rs.RngStream(0).child(1 << 41))
     na = float(torch.linalg.norm(a32.double()))
     tau = 1e-5 * na
     spec = rs.SketchSpec("gaussian", n, b)
@@ -136,50 +129,11 @@ def cfg4(do_cpu):
     return line
 
 
-def _fwht_rows_(x, chunk=4096):
-    """x <- H x / sqrt(n) in place (H the n x n Walsh-Hadamard matrix, n a
-    power of two), column chunk by column chunk."""
-    n = x.shape[0]
-    for c0 in range(0, x.shape[1], chunk):
-        y = x[:, c0:c0 + chunk].contiguous()
-        cw = y.shape[1]
-        h = 1
-        while h < n:
-            v = y.view(n // (2 * h), 2, h, cw)
-            a, b = v[:, 0].clone(), v[:, 1]
-            v[:, 0].add_(b)
-            v[:, 1].neg_().add_(a)
-            h *= 2
-        y.mul_(1.0 / np.sqrt(n))
-        x[:, c0:c0 + chunk] = y
-
-
-def gen_fast_decay_hadamard(n, beta, seed):
-    """cfg5 input (device generator with an exact spectrum):
-    A = U diag(d) V^T, d_i = beta^((i-1)/(n-1)), with orthogonal
-    U = H S1 H S2 and V = H S3 H S4 (H Walsh-Hadamard, S random signs)."""
-    g = torch.Generator(device="cuda")
-    g.manual_seed(seed)
-    signs = [torch.randint(0, 2, (n, 1), generator=g, device="cuda").double() * 2 - 1 for _ in range(4)]
-    d = beta ** (torch.arange(n, dtype=torch.float64, device="cuda") / (n - 1))
-    x = torch.eye(n, dtype=torch.float64, device="cuda")   # V^T = S4 H S3 H
-    _fwht_rows_(x)
-    x.mul_(signs[2])
-    _fwht_rows_(x)
-    x.mul_(signs[3])
-    x.mul_(d[:, None])                                     # D V^T
-    x.mul_(signs[1])                                       # U = H S1 H S2
-    _fwht_rows_(x)
-    x.mul_(signs[0])
-    _fwht_rows_(x)
-    return x
-
-
 def cfg5(do_cpu):
     """cfg5 at one GPU (the sharded form runs this loop split over ranks):
     adaptive column ID of a 65536^2 fp64 fast-decay matrix, b=64, tau=1e-8."""
     n, b, tau = int(os.environ.get("CFG5_N", 65536)), 64, 1e-8
-    a = gen_fast_decay_hadamard(n, 1e-16, 0)
+    a, _ = rs.gen_fast_decay_hadamard(n, 1e-16, rs.RngStream(0).child(1 << 41))
     torch.cuda.synchronize()
     spec = rs.SketchSpec("gaussian", n, b)
     ms, res = dev_time(lambda: rs.rand_lupp_adaptive(a.T, b, tau, spec, rs.RngStream(0)), reps=1)

@@ -116,17 +116,38 @@ def _finite_or_raise(y, name="matrix"):
         raise ValueError(f"{name} contains non-finite entries")
 
 
+def _fixed_rank_sketch(a, sp, rng, transpose=False):
+    """(device Matrix of a, Y) with Y = target @ Omega, target = a or a.T.
+    Tensor-core engine: the target's digit planes (host input: cut as it
+    lands) times Omega's; DMMA engine: the fp64 GEMM (host input: row chunks
+    multiplied as they land)."""
+    arr = _streamable(a)
+    if _ozaki.sketch_engine() == "ozaki":
+        om = _device.omega_dense(sp, rng)
+        if arr is not None:
+            tgt, planes = _streamed_planes(arr.T if transpose else arr)
+            A = tgt.T if transpose else tgt
+        else:
+            A = _device.as_matrix(a)
+            tgt = A.T if transpose else A
+            planes = _ozaki.Planes.of_matrix(tgt)
+        yt = torch.empty((tgt.rows, om.shape[1]), dtype=torch.float64, device=om.device)
+        _ozaki.sketch(planes, _ozaki.Planes.of_omega(om), yt.data_ptr(), om.shape[1])
+        if int(planes.nonfinite.item()):
+            raise ValueError("matrix contains non-finite entries")
+        return A, yt
+    if arr is not None:  # H2D overlapped with the sketch, chunk by chunk
+        return _streamed_sketch(arr, _device.omega_dense(sp, rng), transpose=transpose)
+    A = _device.as_matrix(a)
+    return A, _device.sketch_omega(A.T if transpose else A, sp, rng)
+
+
 def rand_lupp(a, k, spec, rng):
     """Row skeletons by LUPP of ``a @ Omega`` (fixed rank k)."""
     m, n = _device.shape_of(a)
     _check_rank(k, m, n)
     sp = spec.with_dims(n, k)
-    arr = _streamable(a)
-    if arr is not None:  # H2D overlapped with the sketch, chunk by chunk
-        a, yt = _streamed_sketch(arr, _device.omega_dense(sp, rng))
-    else:
-        a = _device.as_matrix(a)
-        yt = _device.sketch_omega(a, sp, rng)
+    a, yt = _fixed_rank_sketch(a, sp, rng)
     y = _device.Matrix(yt, m, k, k, False, a.kind)
     _finite_or_raise(y)
     st, w = _factor_sketch(y, a.kind)
@@ -140,12 +161,7 @@ def column_id(a, k, spec, rng):
     m, n = _device.shape_of(a)
     _check_rank(k, m, n)
     sp = spec.with_dims(m, k)
-    arr = _streamable(a)
-    if arr is not None:  # H2D overlapped with the sketch, chunk by chunk
-        a, yt = _streamed_sketch(arr, _device.omega_dense(sp, rng), transpose=True)
-    else:
-        a = _device.as_matrix(a)
-        yt = _device.sketch_omega(a.T, sp, rng)
+    a, yt = _fixed_rank_sketch(a, sp, rng, transpose=True)
     y = _device.Matrix(yt, n, k, k, False, a.kind)
     _finite_or_raise(y)
     st, w = _factor_sketch(y, a.kind)
