@@ -240,6 +240,7 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         if backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")  # logs comm_nranks / the transport chosen
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
