@@ -83,6 +83,12 @@ RS_DEV void mb_wait(uint64_t* b, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// One lane polls, the warp follows (fewer barrier probes competing with the
+// tensor core's shared-memory traffic).
+RS_DEV void mb_wait_warp(uint64_t* b, uint32_t parity) {
+  if ((threadIdx.x & 31) == 0) mb_wait(b, parity);
+  __syncwarp();
+}
 RS_DEV void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(su32(dst)),
@@ -336,14 +342,14 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(OzParams p) {
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
       const int lt = u / p.nch, ch = u - lt * p.nch;
       const int kb0 = ch * p.kbc, kb1 = min(p.KB, kb0 + p.kbc);
-      mb_wait(tm_empty, tph ^ 1);  // the epilogue has drained the previous unit
+      mb_wait_warp(tm_empty, tph ^ 1);  // the epilogue has drained the previous unit
       tph ^= 1;
       tc_fence_after();
       for (int kb = kb0; kb < kb1; ++kb) {
-        mb_wait(full_b + bi, bph);
+        mb_wait_warp(full_b + bi, bph);
         const uint8_t* bst = sb + (size_t)bi * OZ_MAXS * OZ_BTILE;
         for (int s = 0; s < p.SA; ++s) {
-          mb_wait(full_a + ai, aph);
+          mb_wait_warp(full_a + ai, aph);
           tc_fence_after();
           if (lane == 0) {
             // A plane s times Omega planes t = 0..G-1-s in MMAs of up to 4 planes
