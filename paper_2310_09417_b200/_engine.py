@@ -128,6 +128,18 @@ class TFormState:
         self._scur = 1 - self._scur
         self.k += nc
 
+    def schur_next(self, y_ptr, ldy, e2_out, w=MAX_BLOCK):
+        """After `absorb`: the next block's Schur block S' = Y'[perm'[k:]] -
+        T' Y'[perm'[:k]] into the other S buffer (the absorbed block's factored
+        S stays intact for a rollback) -- the second half of `absorb_schur`."""
+        s_next = self._s_next()
+        _lib.call(
+            "rs_schur_block", self.m, self.k, w, y_ptr, ldy, self.perm.data_ptr(), self.T.data_ptr(),
+            max(self.k, 1), s_next.data_ptr(), w, e2_out.data_ptr() if e2_out is not None else None,
+            self.ws.data_ptr(), self.stream,
+        )
+        self._scur = 1 - self._scur  # (_prev, set by absorb, keeps the factored S)
+
     def rollback(self):
         """Undo the last absorb (its inputs are intact in the other buffers):
         used when a speculative absorb assumed a full-width elimination."""

@@ -418,6 +418,9 @@ class _AdaptiveDriver:
             self.ap = planes if planes is not None else _ozaki.Planes.of_matrix(a)
             self.prof.stop(tok)
             self.bp = _ozaki.Planes(b, n, _ozaki.OMEGA_PLANES, 64, dev)
+            self.sketch_stream = torch.cuda.Stream(device=dev)
+            self.ws_ahead = _device.workspace(slot=1)
+        self.y_ready = [None, None]
         self.stream = _device.stream_handle()
         self.ws = _device.workspace()
         self._issued = set()
@@ -454,12 +457,32 @@ class _AdaptiveDriver:
             return self.yb.data_ptr() + 8 * self.b * t, self.b * self.nb_pre
         return self.y[t % 2].data_ptr(), self.b
 
-    def _sketch(self, t):
+    def _sketch(self, t, ahead=False):
+        """Sketch of block t into Y slot t % 2.  ``ahead``: the look-ahead block
+        on the tensor cores, on its own stream and workspace, so it runs beside
+        the current block's panel and absorb (`_wait_y` joins before use)."""
         from . import _lib
         if t < self.nb_pre:
             return
         slot = t % 2
         self._issue_copy(t)
+        if ahead and self.ozaki:
+            ss = self.sketch_stream
+            ss.wait_stream(self.compute)        # the slot's previous readers are enqueued on compute
+            ss.wait_event(self.om_ready[slot])
+            with torch.cuda.stream(ss):
+                tok = self.prof.start("omega_slice")
+                _ozaki.Planes.of_omega(self.om[slot], out=self.bp, ws=self.ws_ahead)
+                self.prof.stop(tok)
+                tok = self.prof.start("sketch_gemm")
+                _ozaki.sketch(self.ap, self.bp, self.y[slot].data_ptr(), self.b, ws=self.ws_ahead)
+                self.prof.stop(tok)
+                ev = torch.cuda.Event()
+                ev.record(ss)
+            self.y_ready[slot] = ev
+            self.om_free[slot] = ev
+            self._issue_copy(t + 2)
+            return
         self.compute.wait_event(self.om_ready[slot])
         if self.ozaki:
             tok = self.prof.start("omega_slice")
@@ -476,7 +499,12 @@ class _AdaptiveDriver:
         ev = torch.cuda.Event()
         ev.record(self.compute)
         self.om_free[slot] = ev
+        self.y_ready[slot] = None
         self._issue_copy(t + 2)
+
+    def _wait_y(self, t):
+        if t >= self.nb_pre and self.y_ready[t % 2] is not None:
+            self.compute.wait_event(self.y_ready[t % 2])
 
     # -- blocks ------------------------------------------------------------------
     def _absorb_block(self, y, first):
@@ -527,7 +555,7 @@ class _AdaptiveDriver:
             trace = ErrorTrace()
             status = STATUS_NOT_CONVERGED
             t = 1
-            self._sketch(1)
+            self._sketch(1, ahead=not wide)
             pending = False  # speculative full-width absorb awaiting its ncols
             # b == 64: absorb(t) and the Schur block of t+1 run as one fused
             # pass over T (rs_absorb_schur); S/e2 of block t are then ready.
@@ -535,6 +563,7 @@ class _AdaptiveDriver:
             have_schur = False
             while True:
                 y = self._y(t)
+                self._wait_y(t)
                 if not wide and not have_schur:
                     tok = self.prof.start("schur")
                     st.schur(y[0], y[1], b, self.e2)
@@ -548,8 +577,9 @@ class _AdaptiveDriver:
                     ev = None
                 else:
                     ev = self._readback(pending)
-                # speculative: next block's sketch runs while the host waits
-                self._sketch(t + 1)
+                # speculative: next block's sketch runs while the host waits (tensor-core
+                # engine: on its own stream, beside this block's panel and absorb)
+                self._sketch(t + 1, ahead=not wide)
                 if ev is not None:
                     ev.synchronize()
                     e2 = float(self.h_e2[0])
@@ -577,7 +607,9 @@ class _AdaptiveDriver:
                     tok = self.prof.start("absorb")
                     if fused:
                         yn = self._y(t + 1)
-                        st.absorb_schur(b, b, yn[0], self.e2, ldy=yn[1])
+                        st.absorb(b, b)
+                        self._wait_y(t + 1)
+                        st.schur_next(yn[0], yn[1], self.e2)  # into the other S buffer (rollback keeps S)
                         have_schur = True
                     else:
                         st.absorb(b, b)
@@ -593,8 +625,10 @@ class _AdaptiveDriver:
         finally:
             if self.src is not None:
                 self.src.close()
-            # speculative draws may still be in flight on the side stream
+            # speculative draws / sketches may still be in flight on the side streams
             self.compute.wait_stream(self.copy_stream)
+            if self.ozaki:
+                self.compute.wait_stream(self.sketch_stream)
         if self.dev_rng and bool(self.rng_status.any()):
             # a block the parallel ziggurat resolver could not place (never
             # observed): redo the whole loop with the host draw, same bits
