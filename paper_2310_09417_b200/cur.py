@@ -330,8 +330,8 @@ def _cond1(S):
 
 def two_sided_id(a, k, spec, rng):
     """Row skeletons by sketched LUPP, columns from the rows (reference `skeleton.py:606-625`)."""
-    r = rand_lupp(a, k, spec, rng)
-    A = _device.as_matrix(a)
+    A = _device.as_matrix(a)          # one H2D of a host input, shared by every stage
+    r = rand_lupp(A, k, spec, rng)
     ridx = _idx(r.row_idx)
     cidx, w = _column_skeletons_from_rows(A, ridx, k)
     S = _cols(_rows(A, ridx), cidx)
@@ -345,8 +345,8 @@ def two_sided_id(a, k, spec, rng):
 def cur_decompose(a, k, spec, rng):
     """CUR with skeletons from sketched LUPP and ``u_mid = C^+ a R^+``
     (reference `skeleton.py:628-647`)."""
-    r = rand_lupp(a, k, spec, rng)
-    A = _device.as_matrix(a)
+    A = _device.as_matrix(a)          # one H2D of a host input, shared by every stage
+    r = rand_lupp(A, k, spec, rng)
     ridx = _idx(r.row_idx)
     return _cur_from_rows(A, ridx, k, r.row_idx)
 
