@@ -46,10 +46,15 @@ struct GemmCfg {
 // Production configurations (measured on B200, tools/tune_gemm.sh: the
 // column-major sketch operand prefers 64x32 warp tiles, the gathered
 // row-major Schur / interpolation operands the 32x32 tiles).
-#ifndef RS_ROW_CFG  // experiment switch for tools/ builds only
-#define RS_ROW_CFG 128, 64, 16, 4, 2, 3, 2
+#if !defined(RS_ROW_VARIANT) || RS_ROW_VARIANT == 0  // (other variants: tools/build_row_cfg.sh experiments)
+using CfgRow = GemmCfg<128, 64, 16, 4, 2, 3, 2>;  // row-major A: 8 warps of 32x32, BK 16
+#elif RS_ROW_VARIANT == 1
+using CfgRow = GemmCfg<128, 64, 32, 4, 2, 2, 2>;
+#elif RS_ROW_VARIANT == 2
+using CfgRow = GemmCfg<128, 64, 16, 2, 2, 4, 2>;
+#else
+using CfgRow = GemmCfg<128, 64, 32, 2, 2, 2, 2>;
 #endif
-using CfgRow = GemmCfg<RS_ROW_CFG>;  // row-major A: 8 warps of 32x32, BK 16
 using CfgCol = GemmCfg<128, 64, 32, 2, 2, 2, 2>;  // column-major A: 4 warps of 64x32, BK 32
 constexpr int SLOT_DOUBLES = 128 * 64;            // one BM x BN partial tile
 static_assert(CfgRow::THREADS * CfgRow::ACC == SLOT_DOUBLES && CfgCol::THREADS * CfgCol::ACC == SLOT_DOUBLES,
