@@ -147,6 +147,32 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def isolated_sketch_ms(a, b, reps=5):
+    """Average duration of the tensor-core sketch kernel launched alone (CUDA events on
+    the launching stream), on the bench matrix's planes and a fresh Omega block."""
+    import torch
+
+    from paper_2310_09417_b200 import _device, _ozaki
+
+    A = _device.as_matrix(a.T)
+    ap = _ozaki.Planes.of_matrix(A)
+    om = torch.randn(A.cols, b, dtype=torch.float64, device=a.device) / b ** 0.5
+    bp = _ozaki.Planes.of_omega(om)
+    y = torch.empty(A.rows, b, dtype=torch.float64, device=a.device)
+    _ozaki.sketch(ap, bp, y.data_ptr(), b)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        _ozaki.sketch(ap, bp, y.data_ptr(), b)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    del ap, bp, y
+    torch.cuda.empty_cache()
+    return ms
+
+
 def oz_traffic(m, n_loc, b):
     """DRAM bytes per Ozaki sketch launch from the committed ncu --set full capture
     (profiles/r02_oz_gemm_traffic.json), valid for the cfg2 single-GPU shape it was
@@ -322,10 +348,16 @@ def main():
         per_launch_bytes = 8.0 * n * n_loc
         achieved = per_launch_bytes / (avg_ms * 1e-3) / 1e9
         traffic = oz_traffic(n, n_loc, b)
+        iso_ms = isolated_sketch_ms(a, b)
         roofline = {
             "bound": "hbm", "kernel": "oz_gemm_kernel (sketch Y = A^T Omega_t: tcgen05.mma kind::i8, TMEM "
                                       "accumulators, bulk-copy fed, Ozaki digit planes)",
             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            # in the step the look-ahead sketch shares the SMs with the panel / absorb of the
+            # current block (its launches last longer, the step gets shorter); alone:
+            "achieved_isolated": per_launch_bytes / (iso_ms * 1e-3) / 1e9,
+            "frac_isolated": per_launch_bytes / (iso_ms * 1e-3) / 1e9 / peak,
+            "avg_launch_ms_isolated": iso_ms,
             "traffic": traffic.get("bytes_per_launch") if traffic else None, "traffic_detail": traffic,
             "peak_source": peak_src, "per_launch_bytes": per_launch_bytes,
             "per_launch_int8_ops": 2.0 * 36 * n * n_loc * b,
