@@ -336,7 +336,11 @@ int launch_panel(double* S, long long lds, int R, int w, int64_t* perm_out, int*
   if (smem + static_smem > (size_t)max_smem) return RS_ERR_CAPACITY;
   // Polled record slots per lane: G <= 32 * QMAX (a small QMAX keeps the
   // exchange loop short).
-  const int q = G <= 32 ? 0 : G <= 64 ? 1 : G <= 128 ? 2 : 3;
+#ifndef RS_PANEL_QMIN  // smallest polling width used (experiment builds vary it)
+#define RS_PANEL_QMIN 0
+#endif
+  int q = G <= 32 ? 0 : G <= 64 ? 1 : G <= 128 ? 2 : 3;
+  if (q < RS_PANEL_QMIN) q = RS_PANEL_QMIN;
   static const void* const kernels[2][4] = {
       {(const void*)panel_kernel<1, false>, (const void*)panel_kernel<2, false>, (const void*)panel_kernel<4, false>,
        (const void*)panel_kernel<8, false>},

@@ -31,8 +31,8 @@ def main():
     tau = 1e-5 * na
     spec = rs.SketchSpec("gaussian", n, b)
     cur, res = rs.cur_decompose_adaptive(a32, b, tau, spec, rs.RngStream(0))
-    g_row, g_col = np.asarray(res.row_idx), np.asarray(cur.col_idx)
-    u = np.asarray(cur.u_mid)
+    g_row, g_col = np.asarray(res.row_idx.cpu()), np.asarray(cur.col_idx.cpu())
+    u = cur.u_mid.cpu().numpy()
     with threadpool_limits(limits=os.cpu_count()):
         t0 = time.perf_counter()
         ref = orc.rand_lupp_adaptive(a, b, tau, 0, want_w=False)
