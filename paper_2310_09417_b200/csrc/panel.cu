@@ -320,7 +320,7 @@ int launch_panel(double* S, long long lds, int R, int w, int64_t* perm_out, int*
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   // Small panels: fewer CTAs (cheaper exchange).  Large: one CTA per SM.
 #ifndef RS_PANEL_ROWS  // rows per CTA before the grid grows (tools/ experiment builds vary it)
-#define RS_PANEL_ROWS 128
+#define RS_PANEL_ROWS 64
 #endif
   int G = (R + RS_PANEL_ROWS - 1) / RS_PANEL_ROWS;
   if (G > nsm) G = nsm;
