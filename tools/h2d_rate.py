@@ -1,0 +1,27 @@
+"""Host->device and device->host rates: pinned DMA, the pageable staging ring, and the pageable
+readback.  python tools/h2d_rate.py"""
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+from paper_2310_09417_b200 import _device  # noqa: E402
+
+n = 20000
+h = np.random.default_rng(0).standard_normal((n, n))
+pin = torch.from_numpy(h).pin_memory()
+dev = torch.empty((n, n), dtype=torch.float64, device="cuda")
+gb = h.nbytes / 1e9
+for rep in range(3):
+    torch.cuda.synchronize(); t0 = time.perf_counter()
+    dev.copy_(pin, non_blocking=True); torch.cuda.synchronize(); t1 = time.perf_counter()
+    _device.h2d_rows(h, lambda r0, r1, ev: None, out=dev); torch.cuda.synchronize(); t2 = time.perf_counter()
+    out = _device.d2h_pageable(dev); t3 = time.perf_counter()
+    pin.copy_(dev, non_blocking=True); torch.cuda.synchronize(); t4 = time.perf_counter()
+    print(f"rep {rep}: pinned H2D {gb / (t1 - t0):.1f} GB/s, pageable ring H2D {gb / (t2 - t1):.1f} GB/s, "
+          f"pageable D2H {gb / (t3 - t2):.1f} GB/s, pinned D2H {gb / (t4 - t3):.1f} GB/s", flush=True)
+    del out
