@@ -25,3 +25,20 @@ for rep in range(3):
     print(f"rep {rep}: pinned H2D {gb / (t1 - t0):.1f} GB/s, pageable ring H2D {gb / (t2 - t1):.1f} GB/s, "
           f"pageable D2H {gb / (t3 - t2):.1f} GB/s, pinned D2H {gb / (t4 - t3):.1f} GB/s", flush=True)
     del out
+
+# in-place page-locking of the caller's arrays instead of staging
+cudart = torch.cuda.cudart()
+for rep in range(3):
+    t0 = time.perf_counter()
+    rc = cudart.cudaHostRegister(h.ctypes.data, h.nbytes, 0)
+    t1 = time.perf_counter()
+    hv = torch.from_numpy(h)
+    dev.copy_(hv, non_blocking=True); torch.cuda.synchronize(); t2 = time.perf_counter()
+    cudart.cudaHostUnregister(h.ctypes.data); t3 = time.perf_counter()
+    o = np.empty((n, n)); t4 = time.perf_counter()
+    cudart.cudaHostRegister(o.ctypes.data, o.nbytes, 0); t5 = time.perf_counter()
+    torch.from_numpy(o).copy_(dev, non_blocking=True); torch.cuda.synchronize(); t6 = time.perf_counter()
+    cudart.cudaHostUnregister(o.ctypes.data); t7 = time.perf_counter()
+    print(f"rep {rep}: rc {rc} register {1e3*(t1-t0):.1f} ms, H2D {1e3*(t2-t1):.1f} ms, unregister {1e3*(t3-t2):.1f} ms | "
+          f"fresh out: register {1e3*(t5-t4):.1f} ms, D2H {1e3*(t6-t5):.1f} ms, unregister {1e3*(t7-t6):.1f} ms", flush=True)
+    del o
