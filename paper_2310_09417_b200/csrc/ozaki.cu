@@ -41,12 +41,15 @@
 //           lane = one output row per thread), fp64 combination, chunk slot
 //           or direct store, last-arriving unit folds the chunk slots.
 #include <algorithm>
+#include <cstdio>
 #include <cstdint>
 
 #include "common.cuh"
 #include "rskel_internal.h"
 
-#ifndef OZ_DBG  // experiment switch for tools/oz_prof.py builds only (0 in the library)
+#ifndef OZ_DBG  // experiment switch for tools/oz_prof.py builds only (0 in the library):
+// 1 no MMAs, 2 no epilogue TMEM reads, 3 no loads (barriers arrive without data),
+// 5 = 3 without the epilogue, 6 = 3 with an empty epilogue, 7 = time the MMA issuer's waits
 #define OZ_DBG 0
 #endif
 
@@ -58,7 +61,10 @@ constexpr int OZ_BM = 128, OZ_BN = 64, OZ_BK = 128;  // rows of A tile, rows of 
 constexpr int OZ_ATILE = OZ_BM * OZ_BK;               // 16 KB
 constexpr int OZ_BTILE = OZ_BN * OZ_BK;               // 8 KB
 constexpr int OZ_MAXS = 8;
-constexpr int OZ_NA = 6;                              // A plane stages
+#ifndef OZ_NA_STAGES
+#define OZ_NA_STAGES 6
+#endif
+constexpr int OZ_NA = OZ_NA_STAGES;                   // A plane stages
 constexpr int OZ_NB = 2;                              // Omega k-block stages (SB planes each)
 constexpr int OZ_THREADS = 192;
 constexpr size_t OZ_SMEM = 1024 + (size_t)OZ_NA * OZ_ATILE + (size_t)OZ_NB * OZ_MAXS * OZ_BTILE + 512;
@@ -321,15 +327,23 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(OzParams p) {
         const int kb0 = ch * p.kbc, kb1 = min(p.KB, kb0 + p.kbc);
         for (int kb = kb0; kb < kb1; ++kb) {
           mb_wait(empty_b + bi, bph ^ 1);
-          mb_expect_tx(full_b + bi, (uint32_t)(p.SB * OZ_BTILE));
-          bulk_load(sb + (size_t)bi * OZ_MAXS * OZ_BTILE,
-                    p.bdig + ((size_t)tn * p.KB + kb) * p.SB * OZ_BTILE, p.SB * OZ_BTILE, full_b + bi);
+          if (OZ_DBG >= 3) {
+            mb_arrive(full_b + bi);
+          } else {
+            mb_expect_tx(full_b + bi, (uint32_t)(p.SB * OZ_BTILE));
+            bulk_load(sb + (size_t)bi * OZ_MAXS * OZ_BTILE,
+                      p.bdig + ((size_t)tn * p.KB + kb) * p.SB * OZ_BTILE, p.SB * OZ_BTILE, full_b + bi);
+          }
           if (++bi == OZ_NB) { bi = 0; bph ^= 1; }
           const int8_t* asrc = p.adig + ((size_t)tm * p.KB + kb) * p.SA * OZ_ATILE;
           for (int s = 0; s < p.SA; ++s) {
             mb_wait(empty_a + ai, aph ^ 1);
-            mb_expect_tx(full_a + ai, OZ_ATILE);
-            bulk_load(sa + (size_t)ai * OZ_ATILE, asrc + (size_t)s * OZ_ATILE, OZ_ATILE, full_a + ai);
+            if (OZ_DBG >= 3) {
+              mb_arrive(full_a + ai);
+            } else {
+              mb_expect_tx(full_a + ai, OZ_ATILE);
+              bulk_load(sa + (size_t)ai * OZ_ATILE, asrc + (size_t)s * OZ_ATILE, OZ_ATILE, full_a + ai);
+            }
             if (++ai == OZ_NA) { ai = 0; aph ^= 1; }
           }
         }
@@ -339,17 +353,32 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(OzParams p) {
     // ---------------------------------------------------------- MMA issuer --
     int ai = 0, bi = 0;
     uint32_t aph = 0, bph = 0, tph = 0;
+#if OZ_DBG == 7  // where the MMA issuer waits (printf per 37th CTA)
+    unsigned long long w_tm = 0, w_b = 0, w_a = 0, t_mark = 0;
+    const unsigned long long t_start = clock64();
+#define OZ_T0() (t_mark = clock64())
+#define OZ_T1(acc) (acc += clock64() - t_mark)
+#else
+#define OZ_T0() ((void)0)
+#define OZ_T1(acc) ((void)0)
+#endif
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
       const int lt = u / p.nch, ch = u - lt * p.nch;
       const int kb0 = ch * p.kbc, kb1 = min(p.KB, kb0 + p.kbc);
-      mb_wait_warp(tm_empty, tph ^ 1);  // the epilogue has drained the previous unit
+      OZ_T0();
+      if (OZ_DBG != 5) mb_wait_warp(tm_empty, tph ^ 1);  // the epilogue has drained the previous unit
+      OZ_T1(w_tm);
       tph ^= 1;
       tc_fence_after();
       for (int kb = kb0; kb < kb1; ++kb) {
+        OZ_T0();
         mb_wait_warp(full_b + bi, bph);
+        OZ_T1(w_b);
         const uint8_t* bst = sb + (size_t)bi * OZ_MAXS * OZ_BTILE;
         for (int s = 0; s < p.SA; ++s) {
+          OZ_T0();
           mb_wait_warp(full_a + ai, aph);
+          OZ_T1(w_a);
           tc_fence_after();
           if (lane == 0) {
             // A plane s times Omega planes t = 0..G-1-s in MMAs of up to 4 planes
@@ -380,10 +409,15 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(OzParams p) {
         __syncwarp();
         if (++bi == OZ_NB) { bi = 0; bph ^= 1; }
       }
-      if (lane == 0) tc_commit(tm_full);
+      if (lane == 0 && OZ_DBG != 5) tc_commit(tm_full);
       __syncwarp();
     }
-  } else {
+#if OZ_DBG == 7
+    if (lane == 0 && blockIdx.x % 37 == 0)
+      printf("cta %d: total %llu cycles, wait tm_empty %llu, full_b %llu, full_a %llu\n", blockIdx.x,
+             clock64() - t_start, w_tm, w_b, w_a);
+#endif
+  } else if (OZ_DBG != 5) {
     // ------------------------------------------------------------ epilogue --
     const int q = warp & 3;              // TMEM lane quadrant this warp may read
     const int r = q * 32 + lane;         // output row within the tile
@@ -397,6 +431,10 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(OzParams p) {
       mb_wait(tm_full, tph);
       tph ^= 1;
       tc_fence_after();
+      if (OZ_DBG == 6) {
+        mb_arrive(tm_empty);
+        continue;
+      }
       double* slot = p.slots + (size_t)u * (OZ_BM * OZ_BN);
       // this unit's column exponents, staged once in shared memory
       named_sync(1, 128);

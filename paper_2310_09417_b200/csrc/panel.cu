@@ -31,7 +31,12 @@
 // (ROWS_GLOBAL; R x 64 fp64 is 51 MB at R = 100,000 and stays in the 126 MB
 // L2), the position map in shared memory.  Same arithmetic, same pivots.
 #include <atomic>
+#include <cstdio>
 #include <cstdlib>
+
+#ifndef PANEL_DBG  // experiment switch: 1 = per-phase clock64 totals of CTA 0 (printf)
+#define PANEL_DBG 0
+#endif
 
 #include "common.cuh"
 #include "rskel_internal.h"
@@ -39,6 +44,9 @@
 namespace rs {
 
 constexpr int PTHREADS = 256;
+#if PANEL_DBG
+__device__ unsigned long long tp_late_out[256];
+#endif
 constexpr int PWARPS = PTHREADS / 32;
 constexpr int PMAXW = 64;
 constexpr int PMAXG = 256;  // >= CTAs of the cooperative grid (one per SM)
@@ -143,6 +151,8 @@ __global__ void __launch_bounds__(PTHREADS, 1)
   }
   block_best(bv, bp, br, red_v, red_p, red_r);
 
+  unsigned long long tp[6] = {0, 0, 0, 0, 0, 0}, tm0 = clock64(), tm1, tlate = 0;
+#define PMARK(k) if (PANEL_DBG && tid == 0) { tm1 = clock64(); tp[k] += tm1 - tm0; tm0 = tm1; }
   int ncols = w;
   int late_j = -1;   // step whose columns late_j+2.. still need the rank-1 update
   int late_skip = -1;
@@ -165,6 +175,11 @@ __global__ void __launch_bounds__(PTHREADS, 1)
           st_v4(&ws->rowdata[par][cta][c], (unsigned)x, f, (unsigned)(x >> 32), f);
         }
       }
+      PMARK(0);  // publish
+#if PANEL_DBG
+      unsigned long long gt_pub = 0, gt_poll = 0;
+      if (lane == 0 && j == 10) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_pub));
+#endif
       // ---- reduce the G candidates: every CTA polls all records itself
       // (all-to-all, one hop; identical reduction order on every CTA) ----
       double v = -1.0;
@@ -206,6 +221,13 @@ __global__ void __launch_bounds__(PTHREADS, 1)
         }
       }
       if (lane == 0) { s_val = rr >= 0 ? v : 0.0; s_pos = pp; s_row = rr; }
+      PMARK(1);  // poll + reduce (hop 1)
+#if PANEL_DBG
+      if (lane == 0 && j == 10) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_poll));
+        printf("step10 cta %d pub %llu poll_end %llu\n", cta, gt_pub, gt_poll);
+      }
+#endif
       // ---- pivot row (U row j) straight from the winner's published copy ----
       if (rr >= 0 && v > 0.0) {
         const int c0 = j + lane, c1 = j + lane + 32;
@@ -224,6 +246,7 @@ __global__ void __launch_bounds__(PTHREADS, 1)
       // most two columns (u0, u1 in registers) and walks 4 rows per trip so
       // the smem load -> dmul -> dsub -> store chains overlap.
       const int jl = late_j;
+      const unsigned long long tl0 = PANEL_DBG ? clock64() : 0;
       const int c0 = jl + 2 + lane, c1 = c0 + 32;
       if (c0 < w) {
         const bool h1 = c1 < w;
@@ -256,8 +279,11 @@ __global__ void __launch_bounds__(PTHREADS, 1)
           if (h1) at(i, c1) = __dsub_rn(at(i, c1), __dmul_rn(l, u1));
         }
       }
+      if (PANEL_DBG && tid == 32) tlate += clock64() - tl0;
     }
+    PMARK(2);  // pivot row (hop 2)
     __syncthreads();
+    PMARK(3);  // wait for the late update
     if (!(s_val > 0.0)) { ncols = j; break; }  // exactly-zero pivot column
     const int ppos = s_pos, prow = s_row;
 
@@ -281,6 +307,7 @@ __global__ void __launch_bounds__(PTHREADS, 1)
       }
     }
     block_best(bv, bp, br, red_v, red_p, red_r);
+    PMARK(4);  // early update + block argmax
     // The new local best row is published next step: bring it fully up to date.
     if (warp == 0 && br >= 0) {
       const double l = at(br, j);
@@ -292,7 +319,15 @@ __global__ void __launch_bounds__(PTHREADS, 1)
     }
     late_j = j;
     late_skip = br;
+    PMARK(5);  // best row update
   }
+#if PANEL_DBG
+  if (PANEL_DBG && tid == 32 && (cta == 0 || cta == G / 2)) tp_late_out[cta] = tlate;
+  __syncthreads();
+  if (PANEL_DBG && tid == 0 && (cta == 0 || cta == G / 2))
+    printf("panel cta %d/%d rows %d: publish %llu poll %llu row %llu sync %llu early %llu best %llu late(warp 1) %llu (cycles, %d cols)\n",
+           cta, G, nloc, tp[0], tp[1], tp[2], tp[3], tp[4], tp[5], tp_late_out[cta], w);
+#endif
   __syncthreads();
 
   // ---- write back factors (physical row order) and the position map ----

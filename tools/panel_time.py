@@ -14,12 +14,12 @@ for path in sys.argv[1:] or [""]:
         _lib.load(path)
     ws, st = _device.workspace().data_ptr(), _device.stream_handle()
     row = []
-    for R in (2000, 6000, 10000, 16000, 20000, 40000, 65000):
+    for R in [int(x) for x in os.environ.get("PANEL_RS", "2000,6000,10000,16000,20000,40000,65000").split(",")]:
         S0 = torch.randn(R, 64, dtype=torch.float64, device="cuda")
         S = S0.clone()
         perm = torch.empty(R, dtype=torch.int64, device="cuda")
         nc = torch.zeros(1, dtype=torch.int32, device="cuda")
-        Ss = [S0.clone() for _ in range(20)]
+        Ss = [S0.clone() for _ in range(int(os.environ.get("PANEL_REPS", 20)))]
         _lib.call("rs_panel_lupp", S.data_ptr(), 64, R, 64, perm.data_ptr(), nc.data_ptr(), ws, st)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
