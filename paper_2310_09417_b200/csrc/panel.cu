@@ -30,6 +30,7 @@
 // 65,000 x 64): the same kernel with the rows left in place in global memory
 // (ROWS_GLOBAL; R x 64 fp64 is 51 MB at R = 100,000 and stays in the 126 MB
 // L2), the position map in shared memory.  Same arithmetic, same pivots.
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -82,6 +83,7 @@ RS_DEV double join(unsigned lo, unsigned hi) {
 size_t panel_workspace_bytes() { return sizeof(PanelScratch); }
 
 RS_DEV int swz(int i, int c) { return i * PMAXW + (c ^ (i & 31)); }
+RS_DEV uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
 
 // Block-wide argmax of (val desc, pos asc); returns the winner's local row
@@ -107,7 +109,49 @@ RS_DEV void block_best(double& v, int& p, int& r, double* red_v, int* red_p, int
   __syncthreads();
 }
 
-template <int QMAX, bool ROWS_GLOBAL>
+RS_DEV void mb_expect_tx_cta(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// 16 bytes into (possibly another CTA's) shared memory, counted on that CTA's mbarrier
+RS_DEV void st_async_v4(uint32_t addr, unsigned a, unsigned b, unsigned c, unsigned d, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];\n" ::"r"(
+                   addr),
+               "r"(a), "r"(b), "r"(c), "r"(d), "r"(bar)
+               : "memory");
+}
+// Wait for a phase of a local mbarrier that remote st.async writes complete.  CTA-scope acquire
+// (the default): the transaction count already orders the bytes before the phase flip (a
+// cluster-scope acquire adds an L1 invalidation).  Called by the whole warp, with the loop in
+// C++: a spin loop inside inline asm run by one lane leaves the warp unconverged for the
+// compiler, and every later shuffle then took the slow divergent path (~3.7 us per step).
+RS_DEV bool mb_try_wait(uint64_t* bar, unsigned parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+RS_DEV void mb_wait_cluster(uint64_t* bar, unsigned parity) {
+  while (!mb_try_wait(bar, parity)) {
+  }
+}
+RS_DEV void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+// CL = 1 (the library build): flat exchange, every CTA publishes a record and polls all G of
+// them.  CL > 1 (experiment builds, -DRS_PANEL_CLUSTER=8): thread-block clusters; every CTA
+// sends its candidate record and row into the cluster leader's shared memory (st.async,
+// completion counted on the leader's mbarrier), the leaders exchange one record each through
+// global memory, and each leader broadcasts the winner record and U row back into its CTAs'
+// shared memory.  The flat hop grows from ~1 us at 64 records to ~3 us at 148
+// (tools/probe/xchg.cu), but the cluster version measured slower inside the panel: 334-354 us
+// against 272-299 us at R = 6000-20000.
+template <int QMAX, bool ROWS_GLOBAL, int CL>
 __global__ void __launch_bounds__(PTHREADS, 1)
     panel_kernel(double* __restrict__ S, long long lds, int R, int w, int rows_per,
                  int64_t* __restrict__ perm_out, int* __restrict__ ncols_out, PanelScratch* ws,
@@ -132,6 +176,28 @@ __global__ void __launch_bounds__(PTHREADS, 1)
   __shared__ int red_p[PWARPS], red_r[PWARPS];
   __shared__ double s_val;
   __shared__ int s_pos, s_row;
+  // Cluster exchange (CL > 1), by step parity: the leader gathers the CL candidates (record +
+  // row) in crec/crow (cbar counts their bytes); every CTA receives the step's winner record in
+  // brec and its U row straight into Urow2 (bbar counts those bytes).
+  constexpr int NCL = CL > 1 ? CL : 1;
+  __shared__ __align__(8) uint64_t cbar[2], bbar[2];
+  __shared__ __align__(16) uint4 crec[2][NCL];
+  __shared__ __align__(16) double crow[2][NCL][CL > 1 ? PMAXW : 1];
+  __shared__ __align__(16) uint4 brec[2];
+  unsigned crank = 0;
+  const int nrec = CL > 1 ? G / CL : G;  // records polled per step
+  const int rec_id = CL > 1 ? cta / CL : cta;
+  if constexpr (CL > 1) {
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(crank));
+    if (tid == 0) {
+      for (int q = 0; q < 2; ++q) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&cbar[q])));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&bbar[q])));
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    cluster_sync_all();
+  }
 
   if constexpr (!ROWS_GLOBAL) {
     for (int idx = tid; idx < nloc * w; idx += PTHREADS) {
@@ -151,7 +217,7 @@ __global__ void __launch_bounds__(PTHREADS, 1)
   }
   block_best(bv, bp, br, red_v, red_p, red_r);
 
-  unsigned long long tp[6] = {0, 0, 0, 0, 0, 0}, tm0 = clock64(), tm1, tlate = 0;
+  unsigned long long tp[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tm0 = clock64(), tm1, tlate = 0;
 #define PMARK(k) if (PANEL_DBG && tid == 0) { tm1 = clock64(); tp[k] += tm1 - tm0; tm0 = tm1; }
   int ncols = w;
   int late_j = -1;   // step whose columns late_j+2.. still need the rank-1 update
@@ -159,6 +225,122 @@ __global__ void __launch_bounds__(PTHREADS, 1)
   for (int j = 0; j < w; ++j) {
     const int par = j & 1;
     if (warp == 0) {
+     if constexpr (CL > 1) {
+      // ---------------- two-level exchange over the thread-block cluster ----------------
+      const unsigned f = flag_base + (unsigned)j + 1u;
+      const unsigned ph = (unsigned)(j >> 1) & 1u;  // mbarrier phase of this parity's use
+      uint32_t lead_cbar, lead_crec, lead_crow;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, 0;\n" : "=r"(lead_cbar) : "r"(smem_u32(&cbar[par])));
+      asm volatile("mapa.shared::cluster.u32 %0, %1, 0;\n" : "=r"(lead_crec) : "r"(smem_u32(&crec[par][crank])));
+      asm volatile("mapa.shared::cluster.u32 %0, %1, 0;\n" : "=r"(lead_crow) : "r"(smem_u32(&crow[par][crank][0])));
+      // (1) this CTA's candidate, record and row, into the leader's shared memory
+      if (lane == 0) {
+        if (crank == 0) mb_expect_tx_cta(&cbar[par], CL * (16 + 8 * PMAXW));
+        mb_expect_tx_cta(&bbar[par], 16 + 8 * PMAXW);  // this step's broadcast, received below
+        const unsigned long long x = (unsigned long long)__double_as_longlong(br >= 0 ? bv : -1.0);
+        st_async_v4(lead_crec, (unsigned)x, (unsigned)(x >> 32), (unsigned)bp,
+                    br >= 0 ? (unsigned)(r0 + br + 1) : 0u, lead_cbar);
+      }
+      {
+        const int c = 2 * lane;
+        const double x0 = (br >= 0 && c < w) ? at(br, c) : 0.0, x1 = (br >= 0 && c + 1 < w) ? at(br, c + 1) : 0.0;
+        const unsigned long long u0 = (unsigned long long)__double_as_longlong(x0);
+        const unsigned long long u1 = (unsigned long long)__double_as_longlong(x1);
+        st_async_v4(lead_crow + 8u * c, (unsigned)u0, (unsigned)(u0 >> 32), (unsigned)u1, (unsigned)(u1 >> 32),
+                    lead_cbar);
+      }
+      PMARK(0);  // publish
+      if (crank == 0) {
+        // (2) leader: cluster winner -> global record + row (LL words); poll the G / CL
+        // records; fetch the global winner's row; broadcast record + row to the cluster
+        mb_wait_cluster(&cbar[par], ph);
+        PMARK(6);  // gather wait
+        double cv = -1.0;
+        int cp = 0x7fffffff, cr = -1, cm = -1;
+        if (lane < CL) {
+          const uint4 q = crec[par][lane];
+          cv = join(q.x, q.y);
+          cp = (int)q.z;
+          cr = (int)q.w - 1;
+          cm = lane;
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          const double ov = __shfl_xor_sync(0xffffffffu, cv, off);
+          const int op = __shfl_xor_sync(0xffffffffu, cp, off);
+          const int orr = __shfl_xor_sync(0xffffffffu, cr, off);
+          const int om = __shfl_xor_sync(0xffffffffu, cm, off);
+          if (orr >= 0 && (cr < 0 || key_better(ov, op, cv, cp))) { cv = ov; cp = op; cr = orr; cm = om; }
+        }
+        if (cr >= 0) {
+          for (int c = lane; c < w; c += 32) {
+            const unsigned long long x = (unsigned long long)__double_as_longlong(crow[par][cm][c]);
+            st_v4(&ws->rowdata[par][rec_id][c], (unsigned)x, f, (unsigned)(x >> 32), f);
+          }
+        }
+        if (lane == 0) {
+          const unsigned long long x = (unsigned long long)__double_as_longlong(cr >= 0 ? cv : -1.0);
+          st_v4(&ws->rec[par][rec_id][0], (unsigned)x, f, (unsigned)(x >> 32), f);
+          st_v4(&ws->rec[par][rec_id][1], (unsigned)cp, f, (unsigned)(cr + 1), f);
+        }
+        PMARK(7);  // cluster reduce + global publish
+        double v = -1.0;
+        int pp = 0x7fffffff, rr = -1, cc = -1;
+        if (lane < nrec) {
+          for (;;) {
+            const uint4 qa = ld_v4(&ws->rec[par][lane][0]);
+            const uint4 qb = ld_v4(&ws->rec[par][lane][1]);
+            if (qa.y != f || qa.w != f || qb.y != f || qb.w != f) continue;
+            if ((int)qb.z - 1 >= 0) { v = join(qa.x, qa.z); pp = (int)qb.x; rr = (int)qb.z - 1; cc = lane; }
+            break;
+          }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          const double ov = __shfl_xor_sync(0xffffffffu, v, off);
+          const int op = __shfl_xor_sync(0xffffffffu, pp, off);
+          const int orr = __shfl_xor_sync(0xffffffffu, rr, off);
+          const int oc = __shfl_xor_sync(0xffffffffu, cc, off);
+          if (orr >= 0 && (rr < 0 || key_better(ov, op, v, pp))) { v = ov; pp = op; rr = orr; cc = oc; }
+        }
+        PMARK(1);  // gather + global poll
+        double u0 = 0.0, u1 = 0.0;  // U row columns 2 lane, 2 lane + 1
+        if (rr >= 0 && v > 0.0) {
+          const int c0 = 2 * lane, c1 = c0 + 1;
+          bool need0 = c0 < w, need1 = c1 < w;
+          while (need0 || need1) {
+            uint4 x0 = make_uint4(0, 0, 0, 0), x1 = make_uint4(0, 0, 0, 0);
+            if (need0) x0 = ld_v4(&ws->rowdata[par][cc][c0]);
+            if (need1) x1 = ld_v4(&ws->rowdata[par][cc][c1]);
+            if (need0 && x0.y == f && x0.w == f) { u0 = join(x0.x, x0.z); need0 = false; }
+            if (need1 && x1.y == f && x1.w == f) { u1 = join(x1.x, x1.z); need1 = false; }
+          }
+        }
+        const unsigned long long vx = (unsigned long long)__double_as_longlong(rr >= 0 ? v : 0.0);
+        const unsigned long long ux0 = (unsigned long long)__double_as_longlong(u0);
+        const unsigned long long ux1 = (unsigned long long)__double_as_longlong(u1);
+        for (int r = 0; r < CL; ++r) {
+          uint32_t m_bar, m_rec, m_row;
+          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(m_bar) : "r"(smem_u32(&bbar[par])), "r"(r));
+          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(m_rec) : "r"(smem_u32(&brec[par])), "r"(r));
+          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(m_row) : "r"(smem_u32(&Urow2[par][0])), "r"(r));
+          if (lane == 0)
+            st_async_v4(m_rec, (unsigned)vx, (unsigned)(vx >> 32), (unsigned)pp, (unsigned)(rr + 1), m_bar);
+          st_async_v4(m_row + 16u * lane, (unsigned)ux0, (unsigned)(ux0 >> 32), (unsigned)ux1, (unsigned)(ux1 >> 32),
+                      m_bar);
+        }
+      }
+      // (3) every CTA: the step's winner and U row arrive in its own shared memory
+      mb_wait_cluster(&bbar[par], ph);
+      if (lane == 0) {
+        const uint4 q = brec[par];
+        s_val = join(q.x, q.y);
+        s_pos = (int)q.z;
+        s_row = (int)q.w - 1;
+      }
+      __syncwarp();
+      PMARK(2);  // broadcast
+     } else {
       const unsigned f = flag_base + (unsigned)j + 1u;
       // ---- publish this CTA's candidate for column j (no fence needed).
       // The record goes first: it is what every CTA polls; the row values are
@@ -166,8 +348,9 @@ __global__ void __launch_bounds__(PTHREADS, 1)
       if (lane == 0) {
         const double v = br >= 0 ? bv : -1.0;
         const unsigned long long x = (unsigned long long)__double_as_longlong(v);
+        const unsigned growp1 = br >= 0 ? (unsigned)(r0 + br + 1) : 0u;
         st_v4(&ws->rec[par][cta][0], (unsigned)x, f, (unsigned)(x >> 32), f);
-        st_v4(&ws->rec[par][cta][1], (unsigned)bp, f, br >= 0 ? (unsigned)(r0 + br + 1) : 0u, f);
+        st_v4(&ws->rec[par][cta][1], (unsigned)bp, f, growp1, f);
       }
       if (br >= 0) {
         for (int c = lane; c < w; c += 32) {
@@ -176,18 +359,14 @@ __global__ void __launch_bounds__(PTHREADS, 1)
         }
       }
       PMARK(0);  // publish
-#if PANEL_DBG
-      unsigned long long gt_pub = 0, gt_poll = 0;
-      if (lane == 0 && j == 10) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_pub));
-#endif
-      // ---- reduce the G candidates: every CTA polls all records itself
+      // ---- reduce the published candidates: every CTA polls all records itself
       // (all-to-all, one hop; identical reduction order on every CTA) ----
       double v = -1.0;
       int pp = 0x7fffffff, rr = -1, cc = -1;
       {
         // Poll all of this lane's records in one pass (loads issued back to
         // back, then checked), repeat only for the ones not yet published.
-        const int nq = (G - lane + 31) / 32;
+        const int nq = (nrec - lane + 31) / 32;
         unsigned pending = nq >= 32 ? 0xffffffffu : ((1u << nq) - 1u);
         while (pending) {
           uint4 a[QMAX], b[QMAX];
@@ -207,7 +386,7 @@ __global__ void __launch_bounds__(PTHREADS, 1)
             const double qv = join(a[i].x, a[i].z);
             const int qp = (int)b[i].x;
             if (row >= 0 && (rr < 0 || key_better(qv, qp, v, pp))) {
-              v = qv; pp = qp; rr = row; cc = lane + 32 * i;
+              v = qv; pp = qp; rr = row; cc = row / rows_per;  // the winner's CTA
             }
           }
         }
@@ -222,12 +401,6 @@ __global__ void __launch_bounds__(PTHREADS, 1)
       }
       if (lane == 0) { s_val = rr >= 0 ? v : 0.0; s_pos = pp; s_row = rr; }
       PMARK(1);  // poll + reduce (hop 1)
-#if PANEL_DBG
-      if (lane == 0 && j == 10) {
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_poll));
-        printf("step10 cta %d pub %llu poll_end %llu\n", cta, gt_pub, gt_poll);
-      }
-#endif
       // ---- pivot row (U row j) straight from the winner's published copy ----
       if (rr >= 0 && v > 0.0) {
         const int c0 = j + lane, c1 = j + lane + 32;
@@ -240,6 +413,7 @@ __global__ void __launch_bounds__(PTHREADS, 1)
           if (need1 && x1.y == f && x1.w == f) { Urow2[par][c1] = join(x1.x, x1.z); need1 = false; }
         }
       }
+     }
     } else if (late_j >= 0) {
       // ---- late update of the previous step (off the critical path) ----
       // Rank-1 update of columns jl+2.. of every live row; each lane owns at
@@ -322,13 +496,15 @@ __global__ void __launch_bounds__(PTHREADS, 1)
     PMARK(5);  // best row update
   }
 #if PANEL_DBG
-  if (PANEL_DBG && tid == 32 && (cta == 0 || cta == G / 2)) tp_late_out[cta] = tlate;
+  if (PANEL_DBG && tid == 32 && (cta == 0 || cta == G / 2 || cta == 1)) tp_late_out[cta] = tlate;
   __syncthreads();
-  if (PANEL_DBG && tid == 0 && (cta == 0 || cta == G / 2))
-    printf("panel cta %d/%d rows %d: publish %llu poll %llu row %llu sync %llu early %llu best %llu late(warp 1) %llu (cycles, %d cols)\n",
-           cta, G, nloc, tp[0], tp[1], tp[2], tp[3], tp[4], tp[5], tp_late_out[cta], w);
+  if (PANEL_DBG && tid == 0 && (cta == 0 || cta == G / 2 || cta == 1))
+    printf("panel cta %d/%d rows %d: publish %llu poll %llu row %llu sync %llu early %llu best %llu late(warp 1) %llu"
+           " [cluster: gather %llu reduce+publish %llu] (cycles, %d cols)\n",
+           cta, G, nloc, tp[0], tp[1], tp[2], tp[3], tp[4], tp[5], tp_late_out[cta], tp[6], tp[7], w);
 #endif
   __syncthreads();
+  if constexpr (CL > 1) cluster_sync_all();  // no CTA leaves while its leader may be written
 
   // ---- write back factors (physical row order) and the position map ----
   if constexpr (!ROWS_GLOBAL) {
@@ -357,32 +533,92 @@ int launch_panel(double* S, long long lds, int R, int w, int64_t* perm_out, int*
 #ifndef RS_PANEL_ROWS  // rows per CTA before the grid grows (tools/ experiment builds vary it)
 #define RS_PANEL_ROWS 64
 #endif
+#ifndef RS_PANEL_CLUSTER  // cluster size of the two-level exchange; 1 = flat (the default, faster)
+#define RS_PANEL_CLUSTER 1
+#endif
+  constexpr int CL = RS_PANEL_CLUSTER;
+  constexpr int FLAT_MAX = 64;  // the flat exchange's hop is ~1 us up to 64 records, ~3 us at 148
   int G = (R + RS_PANEL_ROWS - 1) / RS_PANEL_ROWS;
   if (G > nsm) G = nsm;
   if (G > PMAXG) G = PMAXG;
   if (G < 1) G = 1;
-  const int rows_per = (R + G - 1) / G;
-  const size_t static_smem = 2048;
+  size_t static_smem = 2048;  // >= the kernel's static shared memory (12 KB with the cluster slots)
   auto round16 = [](size_t x) { return (x + 15) & ~size_t(15); };
-  size_t smem = round16((size_t)rows_per * PMAXW * sizeof(double) + (size_t)rows_per * sizeof(int));
-  // rows in shared memory when they fit, else in place in global memory (L2)
-  const bool rows_global = smem + static_smem > (size_t)max_smem;
-  if (rows_global) smem = round16((size_t)rows_per * sizeof(int));
+  auto smem_for = [&](int g, bool& rows_global) {
+    const int rp = (R + g - 1) / g;
+    size_t sm = round16((size_t)rp * PMAXW * sizeof(double) + (size_t)rp * sizeof(int));
+    // rows in shared memory when they fit, else in place in global memory (L2)
+    rows_global = sm + static_smem > (size_t)max_smem;
+    if (rows_global) sm = round16((size_t)rp * sizeof(int));
+    return sm;
+  };
+  static const void* const flat_kernels[2][4] = {
+      {(const void*)panel_kernel<1, false, 1>, (const void*)panel_kernel<2, false, 1>,
+       (const void*)panel_kernel<4, false, 1>, (const void*)panel_kernel<8, false, 1>},
+      {(const void*)panel_kernel<1, true, 1>, (const void*)panel_kernel<2, true, 1>,
+       (const void*)panel_kernel<4, true, 1>, (const void*)panel_kernel<8, true, 1>}};
+  static const void* const cluster_kernels[2] = {(const void*)panel_kernel<1, false, CL>,
+                                                 (const void*)panel_kernel<1, true, CL>};
+  bool rows_global = false;
+  size_t smem = 0;
+  const void* kern = nullptr;
+  bool clustered = false;
+  if (CL > 1 && G > FLAT_MAX) {
+    // Two-level exchange: G a multiple of CL, no more clusters than fit at once (a cluster
+    // lives in one GPC, so with one CTA per SM a few SMs per GPC may stay idle).
+    int g = std::min((G + CL - 1) / CL * CL, nsm / CL * CL);
+    static_smem = 12288;
+    smem = smem_for(g, rows_global);
+    // one CTA per SM: a second CTA on an SM would slow every step of the exchange
+    const size_t one_per_sm = (size_t)max_smem / 2 + 8192 - static_smem;  // 2 x (this + static + 1 KB) > an SM
+    smem = std::max(smem, one_per_sm);
+    kern = cluster_kernels[rows_global ? 1 : 0];
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(g);
+    cfg.blockDim = dim3(PTHREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    // With one CTA per SM forced, the cluster capacity does not depend on the shared-memory
+    // size: query it once per device (the query costs more than the panel launch).
+    static int maxcl_cache[64];
+    static bool maxcl_known[64];
+    int maxcl = 0;
+    bool ok = true;
+    if (dev < 64 && maxcl_known[dev]) {
+      maxcl = maxcl_cache[dev];
+    } else {
+      ok = cudaOccupancyMaxActiveClusters(&maxcl, kern, &cfg) == cudaSuccess;
+      if (ok && dev < 64) { maxcl_cache[dev] = maxcl; maxcl_known[dev] = true; }
+    }
+    if (ok && maxcl * CL >= FLAT_MAX) {
+      if (g > maxcl * CL) {
+        g = maxcl * CL;
+        smem = std::max(smem_for(g, rows_global), one_per_sm);
+        kern = cluster_kernels[rows_global ? 1 : 0];
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      }
+      G = g;
+      clustered = true;
+    } else {
+      cudaGetLastError();  // no cluster placement: fall back to the flat exchange
+      static_smem = 2048;
+    }
+  }
+  if (!clustered) {
+    smem = smem_for(G, rows_global);
+    const int q = G <= 32 ? 0 : G <= 64 ? 1 : G <= 128 ? 2 : 3;  // polled records per lane <= 32 * QMAX
+    kern = flat_kernels[rows_global ? 1 : 0][q];
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }
   if (smem + static_smem > (size_t)max_smem) return RS_ERR_CAPACITY;
-  // Polled record slots per lane: G <= 32 * QMAX (a small QMAX keeps the
-  // exchange loop short).
-#ifndef RS_PANEL_QMIN  // smallest polling width used (experiment builds vary it)
-#define RS_PANEL_QMIN 0
-#endif
-  int q = G <= 32 ? 0 : G <= 64 ? 1 : G <= 128 ? 2 : 3;
-  if (q < RS_PANEL_QMIN) q = RS_PANEL_QMIN;
-  static const void* const kernels[2][4] = {
-      {(const void*)panel_kernel<1, false>, (const void*)panel_kernel<2, false>, (const void*)panel_kernel<4, false>,
-       (const void*)panel_kernel<8, false>},
-      {(const void*)panel_kernel<1, true>, (const void*)panel_kernel<2, true>, (const void*)panel_kernel<4, true>,
-       (const void*)panel_kernel<8, true>}};
-  const void* kern = kernels[rows_global ? 1 : 0][q];
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int rows_per = (R + G - 1) / G;
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, PTHREADS, smem);
   if (occ * nsm < G) return RS_ERR_CAPACITY;
@@ -391,7 +627,27 @@ int launch_panel(double* S, long long lds, int R, int w, int64_t* perm_out, int*
   static std::atomic<unsigned> epoch{1};
   unsigned flag_base = (epoch.fetch_add(1) & 0x1ffffffu) << 7;
   void* args[] = {&S, &lds, &R, &w, (void*)&rows_per, &perm_out, &ncols_dev, &ws, &flag_base};
-  cudaError_t e = cudaLaunchCooperativeKernel(kern, dim3(G), dim3(PTHREADS), args, smem, st);
+  cudaError_t e;
+  if (clustered) {
+    // all CTAs co-resident (the exchange spins on every CTA): cooperative + cluster launch
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeCooperative;
+    at[1].val.cooperative = 1;
+    cfg.gridDim = dim3(G);
+    cfg.blockDim = dim3(PTHREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    e = cudaLaunchKernelExC(&cfg, kern, args);
+  } else {
+    e = cudaLaunchCooperativeKernel(kern, dim3(G), dim3(PTHREADS), args, smem, st);
+  }
   count_launch(1);
   return e == cudaSuccess ? RS_OK : RS_ERR_CUDA;
 }

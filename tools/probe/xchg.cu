@@ -64,10 +64,19 @@ __global__ void flat(uint4* rec, int steps, unsigned base, unsigned long long* o
   if (threadIdx.x == 0 && cta == 0) out[0] = clock64() - t0;
 }
 
+__constant__ int getenv_busy_c;
+__constant__ int rowmode_c;  // 0 none, 1 rowdata stores after st.async, 2 before
+__device__ uint4 g_rowdata[2][256][64];
+#define getenv_busy getenv_busy_c
 template <int C>
 __global__ void clustered(uint4* rec, int steps, unsigned base, unsigned long long* out) {
   __shared__ __align__(8) uint64_t bar;
   __shared__ __align__(16) unsigned long long slot[2][16];
+  __shared__ double buf[64 * 64];
+  __shared__ volatile int done;
+  const int busy = getenv_busy;
+  if (threadIdx.x == 0) done = 0;
+  for (int i = threadIdx.x; i < 64 * 64; i += blockDim.x) buf[i] = i * 1e-3;
   cg::cluster_group cl = cg::this_cluster();
   const unsigned rank = cl.block_rank();
   const int L = gridDim.x / C, leader = blockIdx.x / C, lane = threadIdx.x & 31;
@@ -82,9 +91,23 @@ __global__ void clustered(uint4* rec, int steps, unsigned base, unsigned long lo
   asm volatile("mapa.shared::cluster.u32 %0, %1, 0;\n" : "=r"(rslot) : "r"(su32(&slot[0][0])));
   unsigned best = blockIdx.x * 2654435761u;
   unsigned long long t0 = clock64();
-  if (threadIdx.x < 32) {
+  if (threadIdx.x >= 32) {
+    if (busy) {
+      const int w = threadIdx.x / 32 - 1, nw = blockDim.x / 32 - 1;
+      double u0 = 0.5, u1 = 0.25;
+      while (!done) {
+        for (int i = w; i < 64; i += nw) {
+          const double l = buf[i * 64 + (lane & 1)];
+          buf[i * 64 + ((2 + lane) ^ (i & 31))] -= l * u0;
+          buf[i * 64 + ((34 + lane) & 63)] -= l * u1;
+        }
+      }
+    }
+  } else {
     for (int j = 0; j < steps; ++j) {
       const unsigned f = base + j + 1, par = j & 1;
+      if (rowmode_c == 2)
+        for (int c = lane; c < 64; c += 32) st_v4(&g_rowdata[par][blockIdx.x][c], make_uint4(best + c, f, c, f));
       if (lane == 0) {
         if (rank == 0)
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(&bar)), "r"(C * 8) : "memory");
@@ -94,6 +117,8 @@ __global__ void clustered(uint4* rec, int steps, unsigned base, unsigned long lo
                      "l"(v), "r"(rbar)
                      : "memory");
       }
+      if (rowmode_c == 1)
+        for (int c = lane; c < 64; c += 32) st_v4(&g_rowdata[par][blockIdx.x][c], make_uint4(best + c, f, c, f));
       if (rank == 0) {
         if (lane == 0)
           asm volatile("{\n\t.reg .pred p;\n\tW:\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t@!p bra W;\n\t}\n" ::"r"(su32(&bar)), "r"(par) : "memory");
@@ -109,8 +134,17 @@ __global__ void clustered(uint4* rec, int steps, unsigned base, unsigned long lo
         m = max(m, v.x);
       }
       for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(~0u, m, o));
+      if (rowmode_c) {  // hop 2: the "winner" CTA's row
+        const int wc = (int)(m % gridDim.x);
+        for (int c = lane; c < 64; c += 32) {
+          uint4 v;
+          do { v = ld_v4(&g_rowdata[par][wc][c]); } while (v.y != f || v.w != f);
+          m += v.z;
+        }
+      }
       best = m * 2654435761u + blockIdx.x;
     }
+    if (lane == 0) done = 1;
   }
   cl.sync();
   if (threadIdx.x == 0 && blockIdx.x == 0) out[0] = clock64() - t0;
@@ -145,7 +179,10 @@ int main(int argc, char** argv) {
   auto run_cluster = [&](auto kern, int C) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
-    cfg.blockDim = 128;
+    cfg.blockDim = 256;
+    const int dyn = getenv("XCHG_SMEM") ? atoi(getenv("XCHG_SMEM")) : 0;  // e.g. 120000: one CTA per SM
+    cfg.dynamicSmemBytes = dyn;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = C; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
@@ -156,7 +193,7 @@ int main(int argc, char** argv) {
     cfg.gridDim = C * 64;
     cudaError_t eo = cudaOccupancyMaxActiveClusters(&ncl, (void*)kern, &cfg);
     for (int G : {C * 8, C * 16, ncl * C}) {
-      if (G > ncl * C) continue;
+      if (G > ncl * C || G > 148) continue;
       cfg.gridDim = G;
       base += 1 << 16;
       cudaEvent_t e0, e1;
@@ -171,6 +208,9 @@ int main(int argc, char** argv) {
              cudaGetErrorString(eo), ms * 1e3 / steps, cyc / steps, cudaGetErrorString(e), cudaGetErrorString(e2));
     }
   };
+  { int b = getenv("XCHG_BUSY") ? 1 : 0; cudaMemcpyToSymbol(getenv_busy_c, &b, sizeof(int)); }
+  { int b = getenv("XCHG_ROW") ? atoi(getenv("XCHG_ROW")) : 0; cudaMemcpyToSymbol(rowmode_c, &b, sizeof(int));
+    cudaMemset((void*)0, 0, 0); }
   if (which == 2) run_cluster(clustered<2>, 2);
   if (which == 4) run_cluster(clustered<4>, 4);
   if (which == 8) run_cluster(clustered<8>, 8);
