@@ -89,12 +89,6 @@ RS_DEV void mb_wait(uint64_t* b, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-// One lane polls, the warp follows (fewer barrier probes competing with the
-// tensor core's shared-memory traffic).
-RS_DEV void mb_wait_warp(uint64_t* b, uint32_t parity) {
-  if ((threadIdx.x & 31) == 0) mb_wait(b, parity);
-  __syncwarp();
-}
 RS_DEV void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(su32(dst)),
@@ -362,25 +356,28 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(OzParams p) {
 #define OZ_T0() ((void)0)
 #define OZ_T1(acc) ((void)0)
 #endif
-    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-      const int lt = u / p.nch, ch = u - lt * p.nch;
-      const int kb0 = ch * p.kbc, kb1 = min(p.KB, kb0 + p.kbc);
-      OZ_T0();
-      if (OZ_DBG != 5) mb_wait_warp(tm_empty, tph ^ 1);  // the epilogue has drained the previous unit
-      OZ_T1(w_tm);
-      tph ^= 1;
-      tc_fence_after();
-      for (int kb = kb0; kb < kb1; ++kb) {
+    // One thread issues and waits; the other lanes of the warp idle until the end (a
+    // warp-wide wait + __syncwarp per stage made the k-block ~6 % slower in
+    // tools/probe/tc_seq.cu, orders 7 vs 9).
+    if (lane == 0) {
+      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+        const int lt = u / p.nch, ch = u - lt * p.nch;
+        const int kb0 = ch * p.kbc, kb1 = min(p.KB, kb0 + p.kbc);
         OZ_T0();
-        mb_wait_warp(full_b + bi, bph);
-        OZ_T1(w_b);
-        const uint8_t* bst = sb + (size_t)bi * OZ_MAXS * OZ_BTILE;
-        for (int s = 0; s < p.SA; ++s) {
+        if (OZ_DBG != 5) mb_wait(tm_empty, tph ^ 1);  // the epilogue has drained the previous unit
+        OZ_T1(w_tm);
+        tph ^= 1;
+        tc_fence_after();
+        for (int kb = kb0; kb < kb1; ++kb) {
           OZ_T0();
-          mb_wait_warp(full_a + ai, aph);
-          OZ_T1(w_a);
-          tc_fence_after();
-          if (lane == 0) {
+          mb_wait(full_b + bi, bph);
+          OZ_T1(w_b);
+          const uint8_t* bst = sb + (size_t)bi * OZ_MAXS * OZ_BTILE;
+          for (int s = 0; s < p.SA; ++s) {
+            OZ_T0();
+            mb_wait(full_a + ai, aph);
+            OZ_T1(w_a);
+            tc_fence_after();
             // A plane s times Omega planes t = 0..G-1-s in MMAs of up to 4 planes
             // (N <= 256): the planes are consecutive 64-row tiles in shared memory
             // and their accumulators g = s + t consecutive 64-column TMEM blocks, so
@@ -401,17 +398,15 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(OzParams p) {
               }
             }
             tc_commit(empty_a + ai);  // the A stage is free once these MMAs have read it
+            if (++ai == OZ_NA) { ai = 0; aph ^= 1; }
           }
-          __syncwarp();
-          if (++ai == OZ_NA) { ai = 0; aph ^= 1; }
+          tc_commit(empty_b + bi);
+          if (++bi == OZ_NB) { bi = 0; bph ^= 1; }
         }
-        if (lane == 0) tc_commit(empty_b + bi);
-        __syncwarp();
-        if (++bi == OZ_NB) { bi = 0; bph ^= 1; }
+        if (OZ_DBG != 5) tc_commit(tm_full);
       }
-      if (lane == 0 && OZ_DBG != 5) tc_commit(tm_full);
-      __syncwarp();
     }
+    __syncwarp();
 #if OZ_DBG == 7
     if (lane == 0 && blockIdx.x % 37 == 0)
       printf("cta %d: total %llu cycles, wait tm_empty %llu, full_b %llu, full_a %llu\n", blockIdx.x,
