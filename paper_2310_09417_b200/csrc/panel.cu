@@ -218,6 +218,8 @@ __global__ void __launch_bounds__(PTHREADS, 1)
   block_best(bv, bp, br, red_v, red_p, red_r);
 
   unsigned long long tp[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tm0 = clock64(), tm1, tlate = 0;
+  unsigned long long gt0 = 0, ck0 = clock64();
+  if (PANEL_DBG) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
 #define PMARK(k) if (PANEL_DBG && tid == 0) { tm1 = clock64(); tp[k] += tm1 - tm0; tm0 = tm1; }
   int ncols = w;
   int late_j = -1;   // step whose columns late_j+2.. still need the rank-1 update
@@ -498,10 +500,13 @@ __global__ void __launch_bounds__(PTHREADS, 1)
 #if PANEL_DBG
   if (PANEL_DBG && tid == 32 && (cta == 0 || cta == G / 2 || cta == 1)) tp_late_out[cta] = tlate;
   __syncthreads();
+  unsigned long long gt1 = 0;
+  if (PANEL_DBG) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt1));
   if (PANEL_DBG && tid == 0 && (cta == 0 || cta == G / 2 || cta == 1))
     printf("panel cta %d/%d rows %d: publish %llu poll %llu row %llu sync %llu early %llu best %llu late(warp 1) %llu"
-           " [cluster: gather %llu reduce+publish %llu] (cycles, %d cols)\n",
-           cta, G, nloc, tp[0], tp[1], tp[2], tp[3], tp[4], tp[5], tp_late_out[cta], tp[6], tp[7], w);
+           " [cluster: gather %llu reduce+publish %llu] (cycles, %d cols); loop %llu cycles in %llu ns\n",
+           cta, G, nloc, tp[0], tp[1], tp[2], tp[3], tp[4], tp[5], tp_late_out[cta], tp[6], tp[7], w,
+           clock64() - ck0, gt1 - gt0);
 #endif
   __syncthreads();
   if constexpr (CL > 1) cluster_sync_all();  // no CTA leaves while its leader may be written
