@@ -2,26 +2,85 @@
 // deterministic Frobenius reduction, the small triangular inverse used for
 // W_hat = L_r L_1^{-1}, the permutation update and the interpolation-matrix
 // scatter (`skeleton.py:176-182`).
+#include <algorithm>
+#include <cstdint>
+
 #include "common.cuh"
 #include "rskel_internal.h"
 
 
 namespace rs {
 
-// dst[i, c] = src[idx[i], c] (idx == nullptr: identity; idx[i] < 0: a zero
-// row -- the owner-masked gathers of the sharded loop), row-major.
-__global__ void gather_rows_kernel(const double* __restrict__ src, long long lds,
-                                   const int64_t* __restrict__ idx, int nrows, int ncols,
-                                   double* __restrict__ dst, long long ldd) {
-  for (int i = blockIdx.x; i < nrows; i += gridDim.x) {
-    long long r = idx ? idx[i] : i;
+// ---- row gathers ----------------------------------------------------------
+// dst[i, c] = src[idx[i], c] (idx == nullptr: identity; idx[i] < 0: a zero row -- the
+// owner-masked gathers of the sharded loop), row-major.  Rows are copied with 16-byte vector
+// loads and stores whenever every source and destination row starts on a 16-byte boundary
+// (base pointers aligned and both leading dimensions even): a warp moves 512 contiguous
+// bytes per instruction, and a row wider than one CTA's span is split over CTAs (grid.x),
+// so long skeleton rows (`a[row_idx]`, 16384 doubles) use the whole GPU.  Streaming loads
+// bypass L1 (ld.global.nc.L1::no_allocate): every byte is read once.
+constexpr int GR_THREADS = 256;
+
+RS_DEV double2 ldg_stream2(const double2* p) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+
+// one CTA per (column span, row); VEC = 2 doubles per access when aligned
+template <int VEC>
+__global__ void __launch_bounds__(GR_THREADS) gather_rows_vec_kernel(
+    const double* __restrict__ src, long long lds, const int64_t* __restrict__ idx, int nrows, int ncols,
+    double* __restrict__ dst, long long ldd, int span) {
+  const int c0 = blockIdx.x * span, c1 = min(ncols, c0 + span);
+  for (int i = blockIdx.y; i < nrows; i += gridDim.y) {
+    const long long r = idx ? idx[i] : i;
     double* d = dst + (long long)i * ldd;
     if (r < 0) {
-      for (int c = threadIdx.x; c < ncols; c += blockDim.x) d[c] = 0.0;
+      for (int c = c0 + threadIdx.x; c < c1; c += GR_THREADS) d[c] = 0.0;
       continue;
     }
     const double* s = src + r * lds;
-    for (int c = threadIdx.x; c < ncols; c += blockDim.x) d[c] = s[c];
+    if (VEC == 2) {
+      // 4 independent 16-byte loads in flight per thread
+      int c = c0 + threadIdx.x * 2;
+      for (; c + 3 * GR_THREADS * 2 + 1 < c1; c += 4 * GR_THREADS * 2) {
+        double2 v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[q] = ldg_stream2(reinterpret_cast<const double2*>(s + c + q * GR_THREADS * 2));
+#pragma unroll
+        for (int q = 0; q < 4; ++q) *reinterpret_cast<double2*>(d + c + q * GR_THREADS * 2) = v[q];
+      }
+      for (; c < c1; c += GR_THREADS * 2) {
+        if (c + 1 < c1) *reinterpret_cast<double2*>(d + c) = ldg_stream2(reinterpret_cast<const double2*>(s + c));
+        else d[c] = s[c];
+      }
+    } else {
+      for (int c = c0 + threadIdx.x; c < c1; c += GR_THREADS) d[c] = s[c];
+    }
+  }
+}
+
+// Narrow rows (the 64-column sketch blocks Y[perm]): one warp per row, 16 bytes per lane.
+__global__ void __launch_bounds__(GR_THREADS) gather_rows_narrow_kernel(
+    const double* __restrict__ src, long long lds, const int64_t* __restrict__ idx, int nrows, int ncols,
+    double* __restrict__ dst, long long ldd) {
+  const int lane = threadIdx.x & 31;
+  const int wid = blockIdx.x * (GR_THREADS / 32) + (threadIdx.x >> 5);
+  const int nw = gridDim.x * (GR_THREADS / 32);
+  for (int i = wid; i < nrows; i += nw) {
+    const long long r = idx ? idx[i] : i;
+    double* d = dst + (long long)i * ldd;
+    const double* s = r >= 0 ? src + r * lds : nullptr;
+    for (int c = 2 * lane; c < ncols; c += 64) {
+      double2 v = make_double2(0.0, 0.0);
+      if (s) {
+        if (c + 1 < ncols) v = ldg_stream2(reinterpret_cast<const double2*>(s + c));
+        else v.x = s[c];
+      }
+      if (c + 1 < ncols) *reinterpret_cast<double2*>(d + c) = v;
+      else d[c] = v.x;
+    }
   }
 }
 
@@ -29,9 +88,22 @@ int launch_gather_rows(const double* src, long long lds, const int64_t* idx, int
                        double* dst, long long ldd, cudaStream_t st) {
   if (nrows < 0 || ncols < 0) return RS_ERR_ARG;
   if (nrows == 0 || ncols == 0) return RS_OK;
-  int threads = ncols >= 256 ? 256 : ((ncols + 31) / 32) * 32;
-  int grid = nrows < 148 * 16 ? nrows : 148 * 16;
-  gather_rows_kernel<<<grid, threads, 0, st>>>(src, lds, idx, nrows, ncols, dst, ldd);
+  const bool vec = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0 &&
+                   (lds % 2) == 0 && (ldd % 2) == 0;
+  if (vec && ncols <= 256) {
+    const int warps = GR_THREADS / 32;
+    const int grid = std::min((nrows + warps - 1) / warps, 148 * 16);
+    gather_rows_narrow_kernel<<<grid, GR_THREADS, 0, st>>>(src, lds, idx, nrows, ncols, dst, ldd);
+  } else {
+    // column spans of 8 accesses per thread; rows over grid.y, enough CTAs to fill the GPU
+    const int span = GR_THREADS * (vec ? 2 : 1) * 8;
+    const int gx = (ncols + span - 1) / span;
+    const int gy = std::min(nrows, std::min(65535, std::max(1, 148 * 16 / gx)));
+    if (vec)
+      gather_rows_vec_kernel<2><<<dim3(gx, gy), GR_THREADS, 0, st>>>(src, lds, idx, nrows, ncols, dst, ldd, span);
+    else
+      gather_rows_vec_kernel<1><<<dim3(gx, gy), GR_THREADS, 0, st>>>(src, lds, idx, nrows, ncols, dst, ldd, span);
+  }
   count_launch(1);
   return cudaGetLastError() == cudaSuccess ? RS_OK : RS_ERR_CUDA;
 }
@@ -322,13 +394,51 @@ __global__ void gather2d_kernel(const double* __restrict__ src, long long rs_, l
   }
 }
 
+// Column-contiguous source (rs == 1, a column-major a): the gather is a transpose.  32 x 32
+// tiles through shared memory: reads run down the source columns (coalesced along i when
+// ridx is absent or local), writes run along the destination rows.
+__global__ void __launch_bounds__(256) gather2d_colmajor_kernel(
+    const double* __restrict__ src, long long cs_, const int64_t* __restrict__ ridx, int nr,
+    const int64_t* __restrict__ cidx, int nc, double* __restrict__ dst, long long ldd) {
+  __shared__ double tile[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
+  const long long r = i0 + tx < nr ? (ridx ? ridx[i0 + tx] : i0 + tx) : -1;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int j = j0 + ty + 8 * q;
+    double v = 0.0;
+    if (r >= 0 && j < nc) {
+      const long long c = cidx ? cidx[j] : j;
+      v = src[r + c * cs_];
+    }
+    tile[ty + 8 * q][tx] = v;  // tile[j][i]
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int i = i0 + ty + 8 * q, j = j0 + tx;
+    if (i < nr && j < nc) dst[(long long)i * ldd + j] = tile[tx][ty + 8 * q];
+  }
+}
+
+// dst = a[ridx][:, cidx] in three shapes: whole rows of row-contiguous data (the vectorised
+// row gather), a column-contiguous source (the tiled transpose), and scattered columns of
+// row-contiguous data (`a[:, col_idx]` of a row-major a: one 8-byte element per index,
+// inherent to the layout).
 int launch_gather2d(const double* src, long long rs_, long long cs_, const int64_t* ridx, int nr,
                     const int64_t* cidx, int nc, double* dst, long long ldd, cudaStream_t st) {
   if (nr < 0 || nc < 0) return RS_ERR_ARG;
   if (nr == 0 || nc == 0) return RS_OK;
-  int threads = nc >= 256 ? 256 : ((nc + 31) / 32) * 32;
-  int grid = nr < 148 * 16 ? nr : 148 * 16;
-  gather2d_kernel<<<grid, threads, 0, st>>>(src, rs_, cs_, ridx, nr, cidx, nc, dst, ldd);
+  if (cs_ == 1 && cidx == nullptr) return launch_gather_rows(src, rs_, ridx, nr, nc, dst, ldd, st);
+  if (rs_ == 1 && nr > 1 && (nc + 31) / 32 <= 65535) {
+    gather2d_colmajor_kernel<<<dim3((nr + 31) / 32, (nc + 31) / 32), 256, 0, st>>>(src, cs_, ridx, nr, cidx, nc,
+                                                                                 dst, ldd);
+  } else {
+    int threads = nc >= 256 ? 256 : ((nc + 31) / 32) * 32;
+    int grid = nr < 148 * 16 ? nr : 148 * 16;
+    gather2d_kernel<<<grid, threads, 0, st>>>(src, rs_, cs_, ridx, nr, cidx, nc, dst, ldd);
+  }
   count_launch(1);
   return cudaGetLastError() == cudaSuccess ? RS_OK : RS_ERR_CUDA;
 }

@@ -319,3 +319,45 @@ def test_adaptive_rank_exhausted_full_width_block(b):
     assert np.array_equal(res.row_idx, ref["row_idx"])
     err = np.linalg.norm(a - res.w @ a[res.row_idx]) / np.linalg.norm(a)
     assert err <= 1e-12
+
+
+@pytest.mark.parametrize("ld_pad", [0, 1])
+def test_gather_kernels_match_numpy(rs, ld_pad):
+    """rs_gather_rows / rs_gather2d against numpy fancy indexing, for the vectorised path
+    (even leading dimensions) and the scalar path (odd), narrow and wide rows, both source
+    layouts, and idx < 0 = zero row (`skeleton.py:569,619,639-645`)."""
+    import torch
+    from paper_2310_09417_b200 import _lib, _device
+
+    g = np.random.default_rng(7)
+    st = _device.stream_handle()
+    for rows, cols in ((300, 64), (257, 5000), (40, 3)):
+        ld = cols + ld_pad
+        a = g.standard_normal((rows, ld))
+        dev = torch.from_numpy(a).cuda()
+        idx = g.integers(0, rows, size=rows + 17)
+        idx[5] = -1
+        out = torch.full((idx.size, cols), np.nan, dtype=torch.float64, device="cuda")
+        idx_d = torch.from_numpy(idx).cuda()
+        _lib.call("rs_gather_rows", dev.data_ptr(), ld, idx_d.data_ptr(), idx.size, cols, out.data_ptr(), cols, st)
+        ref = a[np.maximum(idx, 0), :cols].copy()
+        ref[5] = 0.0
+        assert np.array_equal(out.cpu().numpy(), ref)
+        # 2-D: rows and columns, row-major and column-major source
+        I = g.integers(0, rows, size=min(rows, 33))
+        J = g.integers(0, cols, size=min(cols, 70))
+        for colmajor in (False, True):
+            src = np.asfortranarray(a[:, :cols]) if colmajor else a
+            t = torch.from_numpy(src.T.copy() if colmajor else src).cuda()
+            rs_, cs_ = (1, rows) if colmajor else (ld, 1)
+            for ri, ci in ((I, None), (None, J), (I, J)):
+                nr = rows if ri is None else ri.size
+                nc = cols if ci is None else ci.size
+                o = torch.full((nr, nc), np.nan, dtype=torch.float64, device="cuda")
+                rid = torch.from_numpy(ri).cuda() if ri is not None else None  # kept alive for the call
+                cid = torch.from_numpy(ci).cuda() if ci is not None else None
+                _lib.call("rs_gather2d", t.data_ptr(), rs_, cs_, rid.data_ptr() if rid is not None else None, nr,
+                          cid.data_ptr() if cid is not None else None, nc, o.data_ptr(), nc, st)
+                want = a[:, :cols][ri if ri is not None else slice(None)]
+                want = want[:, ci] if ci is not None else want
+                assert np.array_equal(o.cpu().numpy(), want), (rows, cols, colmajor, ri is None, ci is None)
