@@ -208,6 +208,12 @@ int rs_sparse_sign_dense(int n, int ell, int zeta, const int64_t* idx, const dou
  * pivot j.  The Gram step of pinv_apply (dense.py:166-182). */
 int rs_cholesky(double* G, long long ldg, int n, int* status_dev, void* stream);
 
+/* x <- T^-1 x in place for a small triangular T (n <= 1024) stored by columns: T[i, j] at
+ * cols[j * ldc + i] (a row-major T^T).  lower = forward substitution, else backward; unit =
+ * implicit unit diagonal.  The solves of dgecon's dlacn2 iteration inside the 1-norm
+ * condition estimate (`_condition_estimate_1norm`, skeleton.py:592-603), one launch each. */
+int rs_trsv_cols(const double* cols, long long ldc, int n, int lower, int unit, double* x, void* stream);
+
 /* dst[i, j] = src[r(i)*rs + c(j)*cs], r/c via optional index vectors: the
  * skeleton gathers a[I], a[:, J], a[ix_(I, J)] (skeleton.py:619,639-645). */
 int rs_gather2d(const double* src, long long rs, long long cs, const int64_t* ridx, int nr,

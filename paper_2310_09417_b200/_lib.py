@@ -49,6 +49,7 @@ SIGNATURES = {
     "rs_pinv_scale": (_c_int, [_p, _c_ll, _c_int, _p, _c_ll, _c_int, _c_double, _p, _p]),
     "rs_norm1": (_c_int, [_p, _c_ll, _c_int, _c_int, _p, _p]),
     "rs_cholesky": (_c_int, [_p, _c_ll, _c_int, _p, _p]),
+    "rs_trsv_cols": (_c_int, [_p, _c_ll, _c_int, _c_int, _c_int, _p, _p]),
     "rs_what": (_c_int, [_p, _c_ll, _p, _c_int, _p, _c_int, _p, _c_ll, _p]),
     "rs_srtt_dense": (_c_int, [_c_int, _c_int, _p, _p, _p, _c_double, _p, _c_ll, _p]),
     "rs_sparse_sign_dense": (_c_int, [_c_int, _c_int, _c_int, _p, _p, _c_double, _p, _c_ll, _p]),

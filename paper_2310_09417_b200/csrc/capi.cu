@@ -228,6 +228,10 @@ int rs_cholesky(double* G, long long ldg, int n, int* status_dev, void* stream) 
   return rs::launch_cholesky(G, ldg, n, status_dev, S(stream));
 }
 
+int rs_trsv_cols(const double* cols, long long ldc, int n, int lower, int unit, double* x, void* stream) {
+  return rs::launch_trsv_cols(cols, ldc, n, lower, unit, x, S(stream));
+}
+
 int rs_norm1(const double* A, long long lda, int rows, int cols, double* out, void* stream) {
   return rs::launch_norm1(A, lda, rows, cols, out, S(stream));
 }

@@ -92,6 +92,7 @@ int launch_srtt_dense(int n, int ell, const int64_t* perm, const double* signs, 
 int launch_sparse_sign_dense(int n, int ell, int zeta, const int64_t* idx, const double* signs, double scale,
                              double* out, long long ldo, cudaStream_t st);
 int launch_cholesky(double* G, long long ldg, int n, int* status, cudaStream_t st);
+int launch_trsv_cols(const double* cols, long long ldc, int n, int lower, int unit, double* x, cudaStream_t st);
 int launch_norm1(const double* A, long long lda, int rows, int cols, double* out, cudaStream_t st);
 int launch_gather2d(const double* src, long long rs_, long long cs_, const int64_t* ridx, int nr,
                     const int64_t* cidx, int nc, double* dst, long long ldd, cudaStream_t st);

@@ -222,38 +222,80 @@ int launch_norm1(const double* A, long long lda, int rows, int cols, double* out
 // right-looking by columns (the Gram matrix of a well-conditioned
 // interpolation matrix in the pinv path, cur.py).  *status = 0, or j + 1 if
 // pivot j is not positive.
+// Right-looking Cholesky of a symmetric n x n (n <= 1024) matrix in place (upper factor R,
+// G = R^T R), one CTA.  Per column: the scaled row j is staged in shared memory, then the
+// 32 x 32 thread grid updates the trailing upper triangle row by row (no index division;
+// the matrix, <= 8 MB, stays in L2).
 __global__ void __launch_bounds__(1024) cholesky_kernel(double* __restrict__ G, long long ldg, int n,
                                                         int* __restrict__ status) {
-  __shared__ double s_d;
+  __shared__ double srow[1024];
   __shared__ int s_bad;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   if (threadIdx.x == 0) s_bad = 0;
   __syncthreads();
   for (int j = 0; j < n; ++j) {
-    if (threadIdx.x == 0) {
-      const double d = G[(long long)j * ldg + j];
-      if (!(d > 0.0)) s_bad = j + 1;
-      s_d = d > 0.0 ? sqrt(d) : 1.0;
+    double* gj = G + (long long)j * ldg;
+    const double djj = gj[j];
+    if (!(djj > 0.0)) {
+      if (threadIdx.x == 0) s_bad = j + 1;
+      break;  // uniform: every thread read the same diagonal
+    }
+    const double d = sqrt(djj);
+    for (int c = j + threadIdx.x; c < n; c += blockDim.x) {
+      const double v = c == j ? d : gj[c] / d;
+      srow[c] = v;
+      gj[c] = v;
     }
     __syncthreads();
-    if (s_bad) break;
-    const double d = s_d;
-    for (int c = j + threadIdx.x; c < n; c += blockDim.x)
-      G[(long long)j * ldg + c] = c == j ? d : G[(long long)j * ldg + c] / d;
-    __syncthreads();
-    // trailing update of the upper triangle: G[r][c] -= R[j][r] R[j][c], j < r <= c
-    const int m = n - j - 1;
-    for (long long e = threadIdx.x; e < (long long)m * m; e += blockDim.x) {
-      const int r = j + 1 + (int)(e / m), c = j + 1 + (int)(e % m);
-      if (c < r) continue;
-      G[(long long)r * ldg + c] -= G[(long long)j * ldg + r] * G[(long long)j * ldg + c];
+    // G[r][c] -= R[j][r] R[j][c] for j < r <= c
+    for (int r = j + 1 + ty; r < n; r += 32) {
+      const double rr = srow[r];
+      double* gr = G + (long long)r * ldg;
+      for (int c = r + tx; c < n; c += 32) gr[c] -= rr * srow[c];
     }
     __syncthreads();
   }
-  for (long long e = threadIdx.x; e < (long long)n * n; e += blockDim.x) {
-    const int r = (int)(e / n), c = (int)(e % n);
-    if (c < r) G[(long long)r * ldg + c] = 0.0;
-  }
+  __syncthreads();
+  for (int r = ty; r < n; r += 32)
+    for (int c = tx; c < r; c += 32) G[(long long)r * ldg + c] = 0.0;
   if (threadIdx.x == 0) *status = s_bad;
+}
+
+// x <- T^-1 x for a small triangular T (n <= 1024) given by columns (column j at
+// cols[j * ldc .. + n)), one CTA, one element of x per thread.  Column-oriented substitution
+// in LAPACK dtrsv's order: x_j /= T_jj, then x_i -= T_ij x_j for the rows still to solve.
+// One barrier per step (the pivot value alternates between two shared slots) and the next
+// column's entry is loaded before the barrier, so a step costs one barrier plus one
+// division on the diagonal thread.
+__global__ void __launch_bounds__(1024) trsv_cols_kernel(const double* __restrict__ cols, long long ldc, int n,
+                                                         int lower, int unit, double* __restrict__ x) {
+  __shared__ double s_xj[2];
+  const int i = threadIdx.x;
+  double xi = i < n ? x[i] : 0.0;
+  int j = lower ? 0 : n - 1;
+  double c = i < n ? cols[(long long)j * ldc + i] : 0.0;
+  for (int s = 0; s < n; ++s) {
+    const int jn = lower ? j + 1 : j - 1;
+    const double cn = (s + 1 < n && i < n) ? cols[(long long)jn * ldc + i] : 0.0;  // next column, early
+    if (i == j) {
+      if (!unit) xi = xi / c;
+      s_xj[s & 1] = xi;
+    }
+    __syncthreads();
+    const double xj = s_xj[s & 1];
+    if (i < n && (lower ? i > j : i < j)) xi = xi - c * xj;
+    j = jn;
+    c = cn;
+  }
+  if (i < n) x[i] = xi;
+}
+
+int launch_trsv_cols(const double* cols, long long ldc, int n, int lower, int unit, double* x, cudaStream_t st) {
+  if (n < 0 || n > 1024 || (n > 0 && ldc < n)) return RS_ERR_ARG;
+  if (n == 0) return RS_OK;
+  trsv_cols_kernel<<<1, ((n + 31) / 32) * 32, 0, st>>>(cols, ldc, n, lower, unit, x);
+  count_launch(1);
+  return cudaGetLastError() == cudaSuccess ? RS_OK : RS_ERR_CUDA;
 }
 
 int launch_cholesky(double* G, long long ldg, int n, int* status, cudaStream_t st) {

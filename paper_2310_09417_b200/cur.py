@@ -150,25 +150,23 @@ def _pinv_apply_compressed(A, B, b_planes=None):
     # from that (its 1-norm condition estimate < 1e10, so kappa_2 < sqrt(q) 1e10 <
     # 1e12), no value is truncated and M^+ = M^-1: solve by the device LU instead of
     # Jacobi sweeps.
-    if _cond1(Mm) < 1e10:
-        x = _lu_solve(Mm, H2)
-        if x is not None:
-            return x
+    lu = _lu_factors(Mm)                                 # one LU for the estimate and the solve
+    if lu is not None and _cond1(Mm, lu) < 1e10:
+        return _lu_solve(Mm, H2, lu)
     return _pinv_apply_jacobi(Mm, H2)
 
 
-def _lu_solve(M, B):
-    """X = M^-1 B for a square device Matrix M (LUPP + two blocked TRSMs)."""
-    q = M.rows
-    A = M.row_major().copy()
-    try:
-        perm, _ = dense._lupp_device(A, allow_partial=False)
-    except RankDeficientError:
-        return None
-    L, U = dense._split_lu(A, q)
+def _lu_solve(M, B, lu=None):
+    """X = M^-1 B for a square device Matrix M (LUPP + two blocked TRSMs); None when M is
+    exactly singular."""
+    if lu is None:
+        lu = _lu_factors(M)
+        if lu is None:
+            return None
+    perm, L, U = lu
     PB = _rows(B.row_major(), perm)                      # P B
-    y = dense._trsm_left(dense._mat(L.contiguous()), PB, lower=True, unit=True)
-    x = dense._trsm_left(dense._mat(U.contiguous()), y, lower=False, unit=False)
+    y = dense._trsm_left(dense._mat(L), PB, lower=True, unit=True)
+    x = dense._trsm_left(dense._mat(U), y, lower=False, unit=False)
     return x.tensor()
 
 
@@ -249,42 +247,67 @@ def _column_skeletons_from_rows(A, row_idx, k):
     return st.perm[:k].clone(), w   # x = w.T
 
 
-def _cond1(S):
+def _lu_factors(S):
+    """Device LUPP of the k x k Matrix S: (perm, L, U) as device tensors, or None when S is
+    exactly singular (dgetrf info > 0)."""
+    k = S.rows
+    A = S.row_major().copy()
+    try:
+        perm, _ = dense._lupp_device(A, allow_partial=False)
+    except RankDeficientError:
+        return None
+    L, U = dense._split_lu(A, k)
+    return perm, L.contiguous(), U.contiguous()
+
+
+def _cond1(S, lu=None):
     """LAPACK-style 1-norm condition estimate of the k x k device Matrix S
     (`_condition_estimate_1norm`, skeleton.py:592-603: dgetrf + dgecon).
 
-    The LU is the device LUPP (the same partial-pivoting rule as dgetrf);
-    ||S^-1||_1 is estimated by Hager/Higham's dlacn2 iteration (at most five
-    sign-vector steps plus the alternating-sign safeguard), every solve with
-    the LU factors on the device TRSM, so the flag follows the reference's
-    *estimate* rather than the exact condition number it bounds from below.
-    Returns 1/rcond (inf for an exactly singular S or a zero S)."""
+    The LU is the device LUPP (the same partial-pivoting rule as dgetrf; pass ``lu`` from
+    `_lu_factors` to reuse one); ||S^-1||_1 is estimated by Hager/Higham's dlacn2
+    iteration (at most five sign-vector steps plus the alternating-sign safeguard), every
+    solve with the LU factors on the device TRSM, so the flag follows the reference's
+    *estimate* rather than the exact condition number it bounds from below.  The host reads
+    one small vector per iteration step.  Returns 1/rcond (inf for an exactly singular S or
+    a zero S)."""
     k = S.rows
     dev = _device.device()
     out = torch.empty(1, dtype=torch.float64, device=dev)
     Sr = S.row_major()
     _lib.call("rs_norm1", Sr.ptr, Sr.ld, k, k, out.data_ptr(), _st())
+    if lu is None:
+        lu = _lu_factors(S)
     anorm = float(out.item())
-    if anorm == 0.0:
-        return np.inf
-    A = Sr.copy()
-    try:
-        dense._lupp_device(A, allow_partial=False)
-    except RankDeficientError:
-        return np.inf  # dgetrf info > 0
-    L, U = dense._split_lu(A, k)
-    Lm, Um = dense._mat(L.contiguous()), dense._mat(U.contiguous())
+    if anorm == 0.0 or lu is None:
+        return np.inf  # zero S, or dgetrf info > 0
+    _, L, U = lu
+    st = _st()
+    small = k <= 1024  # one-CTA column-oriented TRSV; larger k: the blocked device TRSM
+    if small:
+        Lt, Ut = L.t().contiguous(), U.t().contiguous()  # columns of L and U as rows
+    else:
+        Lm, Um = dense._mat(L), dense._mat(U)
 
     def solve(x, kase):
         """kase 1: x <- U^-1 L^-1 x ; kase 2: x <- L^-T U^-T x (dgecon's two dlatrs pairs)."""
-        X = dense._mat(x.reshape(k, 1).contiguous())
+        if not small:
+            X = dense._mat(x.reshape(k, 1).contiguous())
+            if kase == 1:
+                y = dense._trsm_left(Lm, X, lower=True, unit=True)
+                y = dense._trsm_left(Um, y, lower=False, unit=False)
+            else:
+                y = dense._trsm_left(Um.T, X, lower=True, unit=False)
+                y = dense._trsm_left(Lm.T, y, lower=False, unit=True)
+            return y.tensor().reshape(k)
+        y = x.contiguous().clone()
         if kase == 1:
-            y = dense._trsm_left(Lm, X, lower=True, unit=True)
-            y = dense._trsm_left(Um, y, lower=False, unit=False)
+            _lib.call("rs_trsv_cols", Lt.data_ptr(), k, k, 1, 1, y.data_ptr(), st)   # L (unit lower)
+            _lib.call("rs_trsv_cols", Ut.data_ptr(), k, k, 0, 0, y.data_ptr(), st)   # U (upper)
         else:
-            y = dense._trsm_left(Um.T, X, lower=True, unit=False)
-            y = dense._trsm_left(Lm.T, y, lower=False, unit=True)
-        return y.tensor().reshape(k)
+            _lib.call("rs_trsv_cols", U.data_ptr(), k, k, 1, 0, y.data_ptr(), st)    # U^T (lower)
+            _lib.call("rs_trsv_cols", L.data_ptr(), k, k, 0, 1, y.data_ptr(), st)    # L^T (unit upper)
+        return y
 
     def sgn(x):
         return torch.where(x >= 0, 1.0, -1.0).to(torch.float64)
@@ -303,14 +326,19 @@ def _cond1(S):
             e = torch.zeros(k, dtype=torch.float64, device=dev)
             e[j] = 1.0
             x = solve(e, 1)
-            estold, est = est, float(x.abs().sum())
             xs = sgn(x)
-            if bool(torch.equal(xs, isgn)) or est <= estold:
+            est_new, same = torch.stack([x.abs().sum(), (xs == isgn).all().to(torch.float64)]).tolist()
+            estold, est = est, est_new
+            if same != 0.0 or est <= estold:
                 break  # repeated sign vector / cycling
             isgn = xs
             x = solve(isgn, 2)
-            jlast, j = j, int(torch.argmax(x.abs()))
-            if float(x[jlast]) != float(x[j].abs()) and it < 5:
+            ax = x.abs()
+            jn = torch.argmax(ax)
+            jlast = j
+            jv, xl, xj = torch.stack([jn.to(torch.float64), x[jlast], ax[jn]]).tolist()
+            j = int(jv)
+            if xl != xj and it < 5:
                 it += 1
                 continue
             break
