@@ -121,24 +121,26 @@ def _lupp_device(A, allow_partial):
     dev = A.t.device
     perm = torch.arange(m, dtype=torch.int64, device=dev)
     sub = torch.empty(max(m, 1), dtype=torch.int64, device=dev)
-    nc_dev = torch.empty(1, dtype=torch.int32, device=dev)
+    npanel = (n + PANEL - 1) // PANEL
+    nc_dev = torch.empty(max(npanel, 1), dtype=torch.int32, device=dev)
     tmp = torch.empty(max(m * n, 1), dtype=torch.float64, device=dev)
     linv = torch.empty((PANEL, PANEL), dtype=torch.float64, device=dev)
-    for j0 in range(0, n, PANEL):
+    for bi, j0 in enumerate(range(0, n, PANEL)):
         w = min(PANEL, n - j0)
         R = m - j0
         blk = A.sub(j0, j0, R, w)
-        _lib.call("rs_panel_lupp", blk.ptr, A.ld, R, w, sub.data_ptr(), nc_dev.data_ptr(), _ws(), _st())
-        nc = int(nc_dev.item())
+        _lib.call("rs_panel_lupp", blk.ptr, A.ld, R, w, sub.data_ptr(), nc_dev[bi:].data_ptr(), _ws(), _st())
         # physical row order = position order (full rows, like the reference's swaps)
         rows = A.sub(j0, 0, R, n)
         _lib.call("rs_gather_rows", rows.ptr, A.ld, sub.data_ptr(), R, n, tmp.data_ptr(), n, _st())
         _lib.call("rs_gather_rows", tmp.data_ptr(), n, None, R, n, rows.ptr, A.ld, _st())
         perm[j0:] = perm[j0:][sub[:R]]
-        if nc < w:
-            if allow_partial:
+        if allow_partial:  # the caller wants the factored prefix: stop at the first short panel
+            nc = int(nc_dev[bi].item())
+            if nc < w:
                 return perm, j0 + nc
-            raise RankDeficientError(j0 + nc)
+        # (without allow_partial the panel counts are read once at the end: a short panel
+        # only leaves the rest unfactored, and the call raises)
         if j0 + w < n:
             # U12 = L11^{-1} A12
             L11 = A.sub(j0, j0, w, w)
@@ -151,6 +153,12 @@ def _lupp_device(A, allow_partial):
             if j0 + w < m:
                 A22 = A.sub(j0 + w, j0 + w, m - j0 - w, n - j0 - w)
                 _gemm(A22, A.sub(j0 + w, j0, m - j0 - w, w), A12, alpha=-1.0, beta=1.0, Cin=A22)
+    if not allow_partial and npanel:
+        ncs = nc_dev[:npanel].tolist()
+        for bi, nc in enumerate(ncs):
+            w = min(PANEL, n - bi * PANEL)
+            if nc < w:
+                raise RankDeficientError(bi * PANEL + nc)
     return perm, n
 
 
