@@ -224,7 +224,13 @@ __global__ void __launch_bounds__(PTHREADS, 1)
   int ncols = w;
   int late_j = -1;   // step whose columns late_j+2.. still need the rank-1 update
   int late_skip = -1;
+#if PANEL_DBG
+  unsigned long long tstep[PMAXW + 1];
+#endif
   for (int j = 0; j < w; ++j) {
+#if PANEL_DBG
+    tstep[j] = clock64();
+#endif
     const int par = j & 1;
     if (warp == 0) {
      if constexpr (CL > 1) {
@@ -498,6 +504,34 @@ __global__ void __launch_bounds__(PTHREADS, 1)
     PMARK(5);  // best row update
   }
 #if PANEL_DBG
+  tstep[ncols < w ? ncols : w] = clock64();
+  if (tid == 0 && (cta == 0 || cta == G / 2)) {
+    // per-column durations: the five slowest and the median
+    unsigned long long d[PMAXW];
+    const int nn = ncols < w ? ncols : w;
+    for (int q = 0; q < nn; ++q) d[q] = tstep[q + 1] - tstep[q];
+    unsigned long long srt[PMAXW];
+    for (int q = 0; q < nn; ++q) srt[q] = d[q];
+    for (int a = 1; a < nn; ++a) {
+      unsigned long long v = srt[a];
+      int b2 = a - 1;
+      while (b2 >= 0 && srt[b2] > v) { srt[b2 + 1] = srt[b2]; --b2; }
+      srt[b2 + 1] = v;
+    }
+    int top[5] = {-1, -1, -1, -1, -1};
+    for (int t = 0; t < 5 && t < nn; ++t) {
+      unsigned long long best = 0; int bj = -1;
+      for (int q = 0; q < nn; ++q) {
+        bool used = false;
+        for (int u = 0; u < t; ++u) used |= top[u] == q;
+        if (!used && d[q] >= best) { best = d[q]; bj = q; }
+      }
+      top[t] = bj;
+    }
+    printf("cta %d steps: median %llu min %llu max %llu cycles; slowest j=%d:%llu j=%d:%llu j=%d:%llu j=%d:%llu j=%d:%llu\n",
+           cta, srt[nn / 2], srt[0], srt[nn - 1], top[0], d[top[0]], top[1], d[top[1]], top[2], d[top[2]], top[3],
+           d[top[3]], top[4], d[top[4]]);
+  }
   if (PANEL_DBG && tid == 32 && (cta == 0 || cta == G / 2 || cta == 1)) tp_late_out[cta] = tlate;
   __syncthreads();
   unsigned long long gt1 = 0;
