@@ -61,13 +61,17 @@ constexpr int OZ_BM = 128, OZ_BN = 64, OZ_BK = 128;  // rows of A tile, rows of 
 constexpr int OZ_ATILE = OZ_BM * OZ_BK;               // 16 KB
 constexpr int OZ_BTILE = OZ_BN * OZ_BK;               // 8 KB
 constexpr int OZ_MAXS = 8;
-#ifndef OZ_NA_STAGES
-#define OZ_NA_STAGES 6
+#ifndef OZ_PPS  // A digit planes per pipeline stage (one bulk copy, one handshake); 2 measured equal
+#define OZ_PPS 1
 #endif
-constexpr int OZ_NA = OZ_NA_STAGES;                   // A plane stages
+#ifndef OZ_NA_STAGES
+#define OZ_NA_STAGES (6 / OZ_PPS)
+#endif
+constexpr int OZ_PPS_ = OZ_PPS;
+constexpr int OZ_NA = OZ_NA_STAGES;                   // A stages of OZ_PPS planes
 constexpr int OZ_NB = 2;                              // Omega k-block stages (SB planes each)
 constexpr int OZ_THREADS = 192;
-constexpr size_t OZ_SMEM = 1024 + (size_t)OZ_NA * OZ_ATILE + (size_t)OZ_NB * OZ_MAXS * OZ_BTILE + 512;
+constexpr size_t OZ_SMEM = 1024 + (size_t)OZ_NA * OZ_PPS_ * OZ_ATILE + (size_t)OZ_NB * OZ_MAXS * OZ_BTILE + 512;
 
 // ------------------------------------------------------------------ PTX ----
 RS_DEV uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -280,8 +284,8 @@ struct OzParams {
 __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(OzParams p) {
   extern __shared__ __align__(1024) uint8_t oz_smem[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_smem) + 1023) & ~uintptr_t(1023));
-  uint8_t* sa = sm;                                      // OZ_NA x 16 KB
-  uint8_t* sb = sm + OZ_NA * OZ_ATILE;                   // OZ_NB x SB x 8 KB
+  uint8_t* sa = sm;                                      // OZ_NA x OZ_PPS x 16 KB
+  uint8_t* sb = sm + OZ_NA * OZ_PPS_ * OZ_ATILE;         // OZ_NB x SB x 8 KB
   uint64_t* bars = reinterpret_cast<uint64_t*>(sb + OZ_NB * OZ_MAXS * OZ_BTILE);
   uint64_t* full_a = bars;
   uint64_t* empty_a = bars + OZ_NA;
@@ -330,13 +334,15 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(OzParams p) {
           }
           if (++bi == OZ_NB) { bi = 0; bph ^= 1; }
           const int8_t* asrc = p.adig + ((size_t)tm * p.KB + kb) * p.SA * OZ_ATILE;
-          for (int s = 0; s < p.SA; ++s) {
+          for (int s0 = 0; s0 < p.SA; s0 += OZ_PPS_) {
+            // planes s0.. of this k-block are consecutive 16 KB tiles in HBM: one copy
+            const uint32_t bytes = (uint32_t)(min(OZ_PPS_, p.SA - s0) * OZ_ATILE);
             mb_wait(empty_a + ai, aph ^ 1);
             if (OZ_DBG >= 3) {
               mb_arrive(full_a + ai);
             } else {
-              mb_expect_tx(full_a + ai, OZ_ATILE);
-              bulk_load(sa + (size_t)ai * OZ_ATILE, asrc + (size_t)s * OZ_ATILE, OZ_ATILE, full_a + ai);
+              mb_expect_tx(full_a + ai, bytes);
+              bulk_load(sa + (size_t)ai * OZ_PPS_ * OZ_ATILE, asrc + (size_t)s0 * OZ_ATILE, bytes, full_a + ai);
             }
             if (++ai == OZ_NA) { ai = 0; aph ^= 1; }
           }
@@ -374,15 +380,17 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(OzParams p) {
           OZ_T1(w_b);
           const uint8_t* bst = sb + (size_t)bi * OZ_MAXS * OZ_BTILE;
           for (int s = 0; s < p.SA; ++s) {
-            OZ_T0();
-            mb_wait(full_a + ai, aph);
-            OZ_T1(w_a);
-            tc_fence_after();
+            if (s % OZ_PPS_ == 0) {
+              OZ_T0();
+              mb_wait(full_a + ai, aph);
+              OZ_T1(w_a);
+              tc_fence_after();
+            }
             // A plane s times Omega planes t = 0..G-1-s in MMAs of up to 4 planes
             // (N <= 256): the planes are consecutive 64-row tiles in shared memory
             // and their accumulators g = s + t consecutive 64-column TMEM blocks, so
             // one MMA covers up to four (s, t) pairs and reads the A plane once.
-            const uint64_t da = smem_desc(sa + (size_t)ai * OZ_ATILE);
+            const uint64_t da = smem_desc(sa + ((size_t)ai * OZ_PPS_ + s % OZ_PPS_) * OZ_ATILE);
             const int nt = p.G - s;
             for (int t0 = 0; t0 < nt; t0 += 4) {
               const int ntile = min(4, nt - t0);
@@ -397,8 +405,10 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(OzParams p) {
                 if (OZ_DBG != 1) tc_mma_i8(d, da + 2 * kk, db + 2 * kk, idesc, acc);
               }
             }
-            tc_commit(empty_a + ai);  // the A stage is free once these MMAs have read it
-            if (++ai == OZ_NA) { ai = 0; aph ^= 1; }
+            if (s % OZ_PPS_ == OZ_PPS_ - 1 || s == p.SA - 1) {
+              tc_commit(empty_a + ai);  // the A stage is free once these MMAs have read it
+              if (++ai == OZ_NA) { ai = 0; aph ^= 1; }
+            }
           }
           tc_commit(empty_b + bi);
           if (++bi == OZ_NB) { bi = 0; bph ^= 1; }
