@@ -294,8 +294,11 @@ int rs_oz_gemm(int M, int N, int K, int kc, int mode, double alpha, const int8_t
                long long ldcin, double* C, long long ldc, void* workspace, void* stream) {
   rs::DGemmParams g = gemm_params(0, 0, 0, 0.0, nullptr, 0, nullptr, nullptr, 0, nullptr, 0.0, nullptr, 0, nullptr,
                                   nullptr, 0, RS_GEMM_PLAIN, workspace);
+  // tail split of the last wave: exact (H, L) partials in the chain-slot region (4 slots per
+  // tail unit), arrival counters in the last 128 ticket words (tile tickets use < 2048)
   return rs::launch_oz_gemm(M, N, K, kc, mode, alpha, a_digits, a_expo, SA, b_digits, b_expo, SB, beta, Cin, ldcin,
-                            C, ldc, g.slots, g.tickets, g.nslots, S(stream));
+                            C, ldc, g.slots, g.tickets, g.nslots, reinterpret_cast<long long*>(g.bslots),
+                            rs::GEMM_MAX_CTAS / 4, g.tickets + (rs::GEMM_SLOTS - rs::GEMM_MAX_CTAS / 4), S(stream));
 }
 
 int rs_uniform(unsigned long long seed, unsigned long long stream_id, long long n, double* out, void* stream) {

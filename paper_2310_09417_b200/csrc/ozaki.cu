@@ -279,7 +279,44 @@ struct OzParams {
   long long ldc;
   double* slots;
   int* tickets;
+  long long* hl;      // tail split: exact int64 (H, L) partials, 4 tiles of 128 x 64 per tail unit
+  int* tail_tickets;  // tail split: arrival counters per tail unit (zero between launches)
+  int split;          // 1: the last partial wave's units are halved over two CTAs each
 };
+
+// Work item i of this CTA.  Whole units u = blockIdx.x + i * gridDim.x; with the tail split,
+// the units after the last full wave are cut in two k-block halves, half (b & 1) of tail
+// unit (b >> 1) going to CTA b, so the last wave keeps every SM busy instead of half of
+// them.  The halves' int32 accumulators are summed exactly (as int64 Horner words), so a
+// split unit has the same bits as an unsplit one.
+RS_DEV bool oz_item(const OzParams& p, int i, int& u, int& kb0, int& kb1, int& half) {
+  const int G = gridDim.x, b = blockIdx.x;
+  const int rounds = p.units / G;
+  if (!p.split) {
+    u = b + i * G;
+    if (u >= p.units) return false;
+    half = -1;
+  } else if (i < rounds) {
+    u = b + i * G;
+    half = -1;
+  } else if (i == rounds && b < 2 * (p.units - rounds * G)) {
+    u = rounds * G + (b >> 1);
+    half = b & 1;
+  } else {
+    return false;
+  }
+  const int ch = u % p.nch;
+  const int k0 = ch * p.kbc, k1 = min(p.KB, k0 + p.kbc);
+  if (half < 0) {
+    kb0 = k0;
+    kb1 = k1;
+  } else {
+    const int mid = k0 + (k1 - k0 + 1) / 2;
+    kb0 = half ? mid : k0;
+    kb1 = half ? k1 : mid;
+  }
+  return true;
+}
 
 __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(OzParams p) {
   extern __shared__ __align__(1024) uint8_t oz_smem[];
@@ -319,10 +356,10 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(OzParams p) {
     if (lane == 0) {
       int ai = 0, bi = 0;
       uint32_t aph = 0, bph = 0;
-      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-        const int lt = u / p.nch, ch = u - lt * p.nch, tile = p.tile0 + lt;
+      int u, kb0, kb1, hf;
+      for (int item = 0; oz_item(p, item, u, kb0, kb1, hf); ++item) {
+        const int lt = u / p.nch, tile = p.tile0 + lt;
         const int tm = tile / p.tiles_n, tn = tile - tm * p.tiles_n;
-        const int kb0 = ch * p.kbc, kb1 = min(p.KB, kb0 + p.kbc);
         for (int kb = kb0; kb < kb1; ++kb) {
           mb_wait(empty_b + bi, bph ^ 1);
           if (OZ_DBG >= 3) {
@@ -366,9 +403,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(OzParams p) {
     // warp-wide wait + __syncwarp per stage made the k-block ~6 % slower in
     // tools/probe/tc_seq.cu, orders 7 vs 9).
     if (lane == 0) {
-      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-        const int lt = u / p.nch, ch = u - lt * p.nch;
-        const int kb0 = ch * p.kbc, kb1 = min(p.KB, kb0 + p.kbc);
+      int u, kb0, kb1, hf;
+      for (int item = 0; oz_item(p, item, u, kb0, kb1, hf); ++item) {
         OZ_T0();
         if (OZ_DBG != 5) mb_wait(tm_empty, tph ^ 1);  // the epilogue has drained the previous unit
         OZ_T1(w_tm);
@@ -428,7 +464,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(OzParams p) {
     const int r = q * 32 + lane;         // output row within the tile
     const int et = threadIdx.x - 64;     // 0..127
     uint32_t tph = 0;
-    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+    int u, kb0, kb1, hf;
+    for (int item = 0; oz_item(p, item, u, kb0, kb1, hf); ++item) {
       const int lt = u / p.nch, ch = u - lt * p.nch, tile = p.tile0 + lt;
       const int tm = tile / p.tiles_n, tn = tile - tm * p.tiles_n;
       const int row = tm * OZ_BM + r;
@@ -448,6 +485,21 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(OzParams p) {
         s_eb[et] = col < p.N ? p.bexp[(long long)col * p.nch + ch] : 0;
       }
       named_sync(1, 128);
+      // tail halves: this half's (H, L) words and the other half's, 128 x 64 int64 each
+      const int tt = hf >= 0 ? u - (p.units / gridDim.x) * gridDim.x : 0;
+      long long* hl_mine = p.hl + ((size_t)4 * tt + 2 * (hf > 0)) * (OZ_BM * OZ_BN) + r;
+      long long* hl_other = p.hl + ((size_t)4 * tt + 2 * (hf == 0)) * (OZ_BM * OZ_BN) + r;
+      for (int pass = 0; pass < (hf >= 0 ? 2 : 1); ++pass) {
+        if (pass == 1) {
+          // both halves of a split unit are in: the second to arrive finishes the unit
+          __threadfence();
+          named_sync(1, 128);
+          if (et == 0) *s_last = atomicAdd(p.tail_tickets + tt, 1) == 1;
+          named_sync(1, 128);
+          if (!*s_last) break;
+          __threadfence();
+          if (et == 0) p.tail_tickets[tt] = 0;
+        }
       for (int cb = 0; cb < OZ_BN / 16; ++cb) {
         // The G <= 8 exact int32 digit-sum accumulators of 16 columns, combined
         // exactly in two int64 words (H: g = 0..3, L: g = 4..7; 7-bit shifts,
@@ -456,7 +508,15 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(OzParams p) {
         long long H[16], L[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) { H[j] = 0; L[j] = 0; }
-        if (OZ_DBG != 2) {
+        if (pass == 1) {
+          // the exact sum of the two halves' words
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const size_t o = (size_t)(cb * 16 + j) * OZ_BM;
+            H[j] = __ldcg(hl_mine + o) + __ldcg(hl_other + o);
+            L[j] = __ldcg(hl_mine + (OZ_BM * OZ_BN) + o) + __ldcg(hl_other + (OZ_BM * OZ_BN) + o);
+          }
+        } else if (OZ_DBG != 2 && kb1 > kb0) {
           const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(cb * 16);
 #pragma unroll
           for (int half = 0; half < 2; ++half) {
@@ -477,6 +537,16 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(OzParams p) {
               }
             }
           }
+        }
+        if (hf >= 0 && pass == 0) {
+          // a tail half: publish this half's words; the unit is finished in pass 1
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const size_t o = (size_t)(cb * 16 + j) * OZ_BM;
+            __stcg(hl_mine + o, H[j]);
+            __stcg(hl_mine + (OZ_BM * OZ_BN) + o, L[j]);
+          }
+          continue;
         }
         // missing high accumulators (G < 8) still take their 7-bit shifts
         const int gl = p.G > 4 ? p.G - 4 : 0, gh = p.G < 4 ? p.G : 4;
@@ -505,8 +575,12 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(OzParams p) {
           for (int j = 0; j < 16; ++j) __stcg(slot + (size_t)(cb * 16 + j) * OZ_BM + r, v[j]);
         }
       }
-      tc_fence_before();
-      mb_arrive(tm_empty);  // TMEM may be overwritten by the next unit
+        if (pass == 0) {
+          tc_fence_before();
+          mb_arrive(tm_empty);  // TMEM may be overwritten by the next unit
+        }
+      }
+      if (hf >= 0 && !*s_last) continue;  // the first half to arrive: the other finishes
       if (p.nch == 1) continue;
       __threadfence();
       named_sync(1, 128);
@@ -618,7 +692,8 @@ int launch_oz_slice(const void* X, int fp32, long long ld, int colmajor, int row
 
 int launch_oz_gemm(int M, int N, int K, int kc, int mode, double alpha, const int8_t* adig, const int* aexp, int SA,
                    const int8_t* bdig, const int* bexp, int SB, double beta, const double* Cin, long long ldcin,
-                   double* C, long long ldc, double* slots, int* tickets, int nslots, cudaStream_t st) {
+                   double* C, long long ldc, double* slots, int* tickets, int nslots, long long* hl, int hl_units,
+                   int* tail_tickets, cudaStream_t st) {
   // G = SB accumulators and SA <= SB, so the s = 0 products touch every accumulator
   if (M < 0 || N < 0 || K < 0 || SA < 1 || SB < SA || SB > OZ_MAXS || kc % OZ_BK || kc <= 0 || kc > 16384)
     return RS_ERR_ARG;
@@ -649,7 +724,12 @@ int launch_oz_gemm(int M, int N, int K, int kc, int mode, double alpha, const in
     const long long t0 = tiles * gi / ngroups, t1 = tiles * (gi + 1) / ngroups;
     p.tile0 = (int)t0;
     p.units = (int)((t1 - t0) * p.nch);
-    oz_gemm_kernel<<<std::min(p.units, nsm), OZ_THREADS, OZ_SMEM, st>>>(p);
+    const int grid = std::min(p.units, nsm);
+    const int tail = p.units - (p.units / grid) * grid;
+    p.hl = hl;
+    p.tail_tickets = tail_tickets;
+    p.split = (hl != nullptr && tail > 0 && 2 * tail <= grid && tail <= hl_units) ? 1 : 0;
+    oz_gemm_kernel<<<grid, OZ_THREADS, OZ_SMEM, st>>>(p);
     count_launch(1);
   }
   return ok_or_cuda();

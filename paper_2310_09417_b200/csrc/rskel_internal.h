@@ -108,7 +108,7 @@ int launch_oz_slice(const void* X, int fp32, long long ld, int colmajor, int row
                     size_t mx_bytes, cudaStream_t st);
 int launch_oz_gemm(int M, int N, int K, int kc, int mode, double alpha, const int8_t* adig, const int* aexp, int SA,
                    const int8_t* bdig, const int* bexp, int SB, double beta, const double* Cin, long long ldcin,
-                   double* C, long long ldc, double* slots, int* tickets, int nslots, cudaStream_t st);
+                   double* C, long long ldc, double* slots, int* tickets, int nslots, long long* hl, int hl_units, int* tail_tickets, cudaStream_t st);
 // Input generators (gen.cu)
 int launch_uniform(uint64_t k0, uint64_t k1, long long n, double* out, cudaStream_t st);
 int launch_hadamard_init(double* x, long long ld, int n, double c, const double* rowscale, cudaStream_t st);

@@ -71,3 +71,26 @@ def test_fp32_input_sketched_from_fp32_planes(rs):
     r32 = rs.rand_lupp_adaptive(a, 16, 1e-3 * np.linalg.norm(a), spec, rs.RngStream(1))
     r64 = rs.rand_lupp_adaptive(a.astype(np.float64), 16, 1e-3 * np.linalg.norm(a), spec, rs.RngStream(1))
     assert r32.rank == r64.rank and np.array_equal(r32.row_idx, r64.row_idx)
+
+
+@pytest.mark.parametrize("fold", [False, True])
+def test_tensor_core_tail_split_is_bitwise(rs, fold):
+    """The sketch kernel halves the last partial wave's units over two CTAs and sums their
+    int32 accumulators exactly (csrc/ozaki.cu `oz_item`).  Rows of a launch that splits
+    (20480 x 4096: 640 units on 148 SMs, a 48-unit tail) must equal, bit for bit, the same
+    rows sliced and multiplied alone (2304 rows: 72 units, no split) -- the row-local
+    determinism contract of include/rskel.h."""
+    import os
+    import sys
+
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    from oz_check import oz
+
+    g = torch.Generator(device="cuda").manual_seed(11)
+    M, K, N = 20480, 4096 if not fold else 1000, 64
+    A = torch.randn(M, K, dtype=torch.float64, device="cuda", generator=g)
+    om = torch.randn(K, N, dtype=torch.float64, device="cuda", generator=g)
+    Y, _ = oz(A, False, om)
+    for r0 in (0, M - 2304):  # a leading block and the block whose tiles are the split tail
+        Ys, _ = oz(A[r0:r0 + 2304].contiguous(), False, om)
+        assert torch.equal(Y[r0:r0 + 2304], Ys)
