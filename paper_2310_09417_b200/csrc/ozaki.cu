@@ -70,7 +70,12 @@ constexpr int OZ_MAXS = 8;
 constexpr int OZ_PPS_ = OZ_PPS;
 constexpr int OZ_NA = OZ_NA_STAGES;                   // A stages of OZ_PPS planes
 constexpr int OZ_NB = 2;                              // Omega k-block stages (SB planes each)
-constexpr int OZ_THREADS = 192;
+#ifndef OZ_EPI_WARPS  // epilogue warps: 4 (one per TMEM lane quadrant) or 8 (two, splitting the columns)
+#define OZ_EPI_WARPS 8
+#endif
+constexpr int OZ_EPI = OZ_EPI_WARPS * 32;             // epilogue threads
+constexpr int OZ_CBS = OZ_EPI_WARPS / 4;              // column groups: each warp takes OZ_BN / OZ_CBS columns
+constexpr int OZ_THREADS = 64 + OZ_EPI;
 constexpr size_t OZ_SMEM = 1024 + (size_t)OZ_NA * OZ_PPS_ * OZ_ATILE + (size_t)OZ_NB * OZ_MAXS * OZ_BTILE + 512;
 
 // ------------------------------------------------------------------ PTX ----
@@ -339,7 +344,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(OzParams p) {
     for (int i = 0; i < OZ_NA; ++i) { mb_init(full_a + i, 1); mb_init(empty_a + i, 1); }
     for (int i = 0; i < OZ_NB; ++i) { mb_init(full_b + i, 1); mb_init(empty_b + i, 1); }
     mb_init(tm_full, 1);
-    mb_init(tm_empty, 128);
+    mb_init(tm_empty, OZ_EPI);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) {
@@ -462,7 +467,9 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(OzParams p) {
     // ------------------------------------------------------------ epilogue --
     const int q = warp & 3;              // TMEM lane quadrant this warp may read
     const int r = q * 32 + lane;         // output row within the tile
-    const int et = threadIdx.x - 64;     // 0..127
+    const int et = threadIdx.x - 64;     // 0..OZ_EPI-1
+    const int cgrp = (warp - 2) >> 2;    // column group of this warp
+    const int cb_lo = cgrp * (OZ_BN / 16 / OZ_CBS), cb_hi = cb_lo + OZ_BN / 16 / OZ_CBS;
     uint32_t tph = 0;
     int u, kb0, kb1, hf;
     for (int item = 0; oz_item(p, item, u, kb0, kb1, hf); ++item) {
@@ -479,12 +486,12 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(OzParams p) {
       }
       double* slot = p.slots + (size_t)u * (OZ_BM * OZ_BN);
       // this unit's column exponents, staged once in shared memory
-      named_sync(1, 128);
+      named_sync(1, OZ_EPI);
       if (et < OZ_BN) {
         const int col = tn * OZ_BN + et;
         s_eb[et] = col < p.N ? p.bexp[(long long)col * p.nch + ch] : 0;
       }
-      named_sync(1, 128);
+      named_sync(1, OZ_EPI);
       // tail halves: this half's (H, L) words and the other half's, 128 x 64 int64 each
       const int tt = hf >= 0 ? u - (p.units / gridDim.x) * gridDim.x : 0;
       long long* hl_mine = p.hl + ((size_t)4 * tt + 2 * (hf > 0)) * (OZ_BM * OZ_BN) + r;
@@ -493,14 +500,14 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(OzParams p) {
         if (pass == 1) {
           // both halves of a split unit are in: the second to arrive finishes the unit
           __threadfence();
-          named_sync(1, 128);
+          named_sync(1, OZ_EPI);
           if (et == 0) *s_last = atomicAdd(p.tail_tickets + tt, 1) == 1;
-          named_sync(1, 128);
+          named_sync(1, OZ_EPI);
           if (!*s_last) break;
           __threadfence();
           if (et == 0) p.tail_tickets[tt] = 0;
         }
-      for (int cb = 0; cb < OZ_BN / 16; ++cb) {
+      for (int cb = cb_lo; cb < cb_hi; ++cb) {
         // The G <= 8 exact int32 digit-sum accumulators of 16 columns, combined
         // exactly in two int64 words (H: g = 0..3, L: g = 4..7; 7-bit shifts,
         // |H|, |L| < 2^55), then two conversions and one fma:
@@ -583,14 +590,14 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(OzParams p) {
       if (hf >= 0 && !*s_last) continue;  // the first half to arrive: the other finishes
       if (p.nch == 1) continue;
       __threadfence();
-      named_sync(1, 128);
+      named_sync(1, OZ_EPI);
       if (et == 0) *s_last = atomicAdd(p.tickets + lt, 1) == p.nch - 1;
-      named_sync(1, 128);
+      named_sync(1, OZ_EPI);
       if (!*s_last) continue;
       __threadfence();
       // last chunk of the tile to arrive: fold the chunk partials in chunk order
       const double* base = p.slots + (size_t)lt * p.nch * (OZ_BM * OZ_BN) + r;
-      for (int cb = 0; cb < OZ_BN / 16; ++cb) {
+      for (int cb = cb_lo; cb < cb_hi; ++cb) {
         double acc[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) acc[j] = __ldcg(base + (size_t)(cb * 16 + j) * OZ_BM);
@@ -619,7 +626,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(OzParams p) {
           }
         }
       }
-      named_sync(1, 128);
+      named_sync(1, OZ_EPI);
       if (et == 0) p.tickets[lt] = 0;
     }
   }
