@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(OzParams p) {
         const int tm = tile / p.tiles_n, tn = tile - tm * p.tiles_n;
         for (int kb = kb0; kb < kb1; ++kb) {
           mb_wait(empty_b + bi, bph ^ 1);
-          if (OZ_DBG >= 3) {
+          if (OZ_DBG == 3 || OZ_DBG == 5 || OZ_DBG == 6) {  // no-load experiment modes
             mb_arrive(full_b + bi);
           } else {
             mb_expect_tx(full_b + bi, (uint32_t)(p.SB * OZ_BTILE));
@@ -380,7 +380,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(OzParams p) {
             // planes s0.. of this k-block are consecutive 16 KB tiles in HBM: one copy
             const uint32_t bytes = (uint32_t)(min(OZ_PPS_, p.SA - s0) * OZ_ATILE);
             mb_wait(empty_a + ai, aph ^ 1);
-            if (OZ_DBG >= 3) {
+            if (OZ_DBG == 3 || OZ_DBG == 5 || OZ_DBG == 6) {  // no-load experiment modes
               mb_arrive(full_a + ai);
             } else {
               mb_expect_tx(full_a + ai, bytes);
@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm_kernel(OzParams p) {
     // ---------------------------------------------------------- MMA issuer --
     int ai = 0, bi = 0;
     uint32_t aph = 0, bph = 0, tph = 0;
-#if OZ_DBG == 7  // where the MMA issuer waits (printf per 37th CTA)
+#if OZ_DBG == 7 || OZ_DBG == 8  // where the MMA issuer waits (7: printf per 37th CTA; 8: no printf)
     unsigned long long w_tm = 0, w_b = 0, w_a = 0, t_mark = 0;
     const unsigned long long t_start = clock64();
 #define OZ_T0() (t_mark = clock64())
