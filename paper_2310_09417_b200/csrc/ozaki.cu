@@ -731,7 +731,10 @@ int launch_oz_gemm(int M, int N, int K, int kc, int mode, double alpha, const in
     const long long t0 = tiles * gi / ngroups, t1 = tiles * (gi + 1) / ngroups;
     p.tile0 = (int)t0;
     p.units = (int)((t1 - t0) * p.nch);
-    const int grid = std::min(p.units, nsm);
+#ifndef OZ_MAX_CTAS  // experiment builds: leave SMs free for a concurrent kernel
+#define OZ_MAX_CTAS 100000
+#endif
+    const int grid = std::min(std::min(p.units, nsm), OZ_MAX_CTAS);
     const int tail = p.units - (p.units / grid) * grid;
     p.hl = hl;
     p.tail_tickets = tail_tickets;
