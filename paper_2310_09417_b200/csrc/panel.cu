@@ -50,6 +50,10 @@ __device__ unsigned long long tp_late_out[256];
 #endif
 constexpr int PWARPS = PTHREADS / 32;
 constexpr int PMAXW = 64;
+#ifndef RS_PANEL_EU_MAX  // rows per lane up to which warp 0 does the early update alone (0: never)
+#define RS_PANEL_EU_MAX 6
+#endif
+constexpr int EU_MAX = RS_PANEL_EU_MAX;
 constexpr int PMAXG = 256;  // >= CTAs of the cooperative grid (one per SM)
 
 // LL-style exchange: every 8-byte word carries the step flag next to 4 bytes
@@ -175,7 +179,7 @@ __global__ void __launch_bounds__(PTHREADS, 1)
   __shared__ double red_v[PWARPS];
   __shared__ int red_p[PWARPS], red_r[PWARPS];
   __shared__ double s_val;
-  __shared__ int s_pos, s_row;
+  __shared__ int s_pos, s_row, s_skip;
   // Cluster exchange (CL > 1), by step parity: the leader gathers the CL candidates (record +
   // row) in crec/crow (cbar counts their bytes); every CTA receives the step's winner record in
   // brec and its U row straight into Urow2 (bbar counts those bytes).
@@ -222,6 +226,9 @@ __global__ void __launch_bounds__(PTHREADS, 1)
   if (PANEL_DBG) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
 #define PMARK(k) if (PANEL_DBG && tid == 0) { tm1 = clock64(); tp[k] += tm1 - tm0; tm0 = tm1; }
   int ncols = w;
+  // few rows per CTA: warp 0 does the early update and argmax alone (every CTA of the grid
+  // decides for itself; the decision only changes which threads do the same arithmetic)
+  const bool warp_early = nloc <= 32 * EU_MAX;
   int late_j = -1;   // step whose columns late_j+2.. still need the rank-1 update
   int late_skip = -1;
 #if PANEL_DBG
@@ -427,6 +434,11 @@ __global__ void __launch_bounds__(PTHREADS, 1)
       // Rank-1 update of columns jl+2.. of every live row; each lane owns at
       // most two columns (u0, u1 in registers) and walks 4 rows per trip so
       // the smem load -> dmul -> dsub -> store chains overlap.
+      if (warp_early) {
+        // warp 0 did step late_j's early update alone: wait for its scaled column
+        asm volatile("bar.sync 2, %0;\n" ::"r"(PTHREADS) : "memory");
+        late_skip = s_skip;
+      }
       const int jl = late_j;
       const unsigned long long tl0 = PANEL_DBG ? clock64() : 0;
       const int c0 = jl + 2 + lane, c1 = c0 + 32;
@@ -473,6 +485,60 @@ __global__ void __launch_bounds__(PTHREADS, 1)
     const double upiv = Urow2[par][j];
     const double unext = (j + 1 < w) ? Urow2[par][j + 1] : 0.0;
     bv = -1.0; bp = 0x7fffffff; br = -1;
+    if (warp_early) {
+      // Few rows per CTA: warp 0 alone scales column j and updates column j + 1 of up to
+      // EU_MAX rows per lane (independent rows, so the divisions overlap), then a warp
+      // argmax -- no block-wide barrier on the critical path.  Warps 1-7 wait for it on a
+      // named barrier before the late update of this column.
+      if (warp == 0) {
+#pragma unroll
+        for (int q = 0; q < EU_MAX; ++q) {
+          const int i = lane + 32 * q;
+          if (i < nloc) {
+            int pi = pos[i];
+            if (pi >= j) {
+              if (r0 + i == prow) {
+                pos[i] = j;
+              } else {
+                if (pi == j) { pi = ppos; pos[i] = pi; }
+                const double l = __ddiv_rn(at(i, j), upiv);
+                at(i, j) = l;
+                if (j + 1 < w) {
+                  double& a = at(i, j + 1);
+                  const double v = __dsub_rn(a, __dmul_rn(l, unext));
+                  a = v;
+                  const double av = fabs(v);
+                  if (br < 0 || key_better(av, pi, bv, bp)) { bv = av; bp = pi; br = i; }
+                }
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
+          const int op = __shfl_xor_sync(0xffffffffu, bp, off);
+          const int orr = __shfl_xor_sync(0xffffffffu, br, off);
+          if (orr >= 0 && (br < 0 || key_better(ov, op, bv, bp))) { bv = ov; bp = op; br = orr; }
+        }
+        PMARK(4);  // early update + warp argmax
+        if (br >= 0) {
+          const double l = at(br, j);
+          for (int c = j + 2 + lane; c < w; c += 32) {
+            double& a = at(br, c);
+            a = __dsub_rn(a, __dmul_rn(l, Urow2[par][c]));
+          }
+        }
+        if (lane == 0) s_skip = br;
+        __syncwarp();
+        // the last column has no late update: no arrival, so the barrier stays balanced
+        if (j + 1 < w) asm volatile("bar.arrive 2, %0;\n" ::"r"(PTHREADS) : "memory");
+      }
+      late_j = j;
+      late_skip = br;  // (warps 1-7 read s_skip after the named barrier)
+      PMARK(5);  // best row update
+      continue;
+    }
     for (int i = tid; i < nloc; i += PTHREADS) {
       int pi = pos[i];
       if (pi < j) continue;
