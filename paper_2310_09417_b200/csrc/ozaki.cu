@@ -125,14 +125,6 @@ RS_DEV void tc_ld16_async(uint32_t taddr, int* v) {
       : "r"(taddr));
 }
 RS_DEV void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
-RS_DEV void tc_ld16(uint32_t taddr, int (&v)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-}
 // 2^e exactly (normal range; the digit exponents of finite fp64 data stay far inside it)
 RS_DEV double pow2(int e) {
   return e >= -1022 && e <= 1023 ? __longlong_as_double((long long)(e + 1023) << 52) : ldexp(1.0, e);
