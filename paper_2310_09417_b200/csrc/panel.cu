@@ -571,6 +571,11 @@ __global__ void __launch_bounds__(PTHREADS, 1)
   }
 #if PANEL_DBG
   tstep[ncols < w ? ncols : w] = clock64();
+  if (tid == 0) {
+    unsigned sm_all;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_all));
+    printf("CTASM %d %u %d\n", cta, sm_all, G);
+  }
   if (tid == 0 && (cta == 0 || cta == G / 2)) {
     // per-column durations: the five slowest and the median
     unsigned long long d[PMAXW];
@@ -594,6 +599,9 @@ __global__ void __launch_bounds__(PTHREADS, 1)
       }
       top[t] = bj;
     }
+    unsigned smid_;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid_));
+    printf("smid %u ", smid_);
     printf("cta %d steps: median %llu min %llu max %llu cycles; slowest j=%d:%llu j=%d:%llu j=%d:%llu j=%d:%llu j=%d:%llu\n",
            cta, srt[nn / 2], srt[0], srt[nn - 1], top[0], d[top[0]], top[1], d[top[1]], top[2], d[top[2]], top[3],
            d[top[3]], top[4], d[top[4]]);
