@@ -335,3 +335,24 @@ def test_cond1_is_dgecon_estimate_not_exact():
     # the kappa * eps level (measured 1.5e-5 relative)
     assert abs(est - float(g["est"])) <= 1e-3 * float(g["est"])
     assert est < cur.COND_LIMIT < float(g["exact"])
+
+
+@pytest.mark.parametrize("k", [1, 5, 300, 1100])
+def test_cond1_matches_lapack_dgecon(k):
+    """The device estimate against LAPACK's own dgetrf + dgecon (the reference's
+    `_condition_estimate_1norm`, skeleton.py:592-603) on graded random matrices: the
+    one-launch TRSV path (k <= 1024) and the blocked-TRSM path (k > 1024)."""
+    import torch
+    from scipy.linalg import lapack
+
+    from paper_2310_09417_b200 import cur, dense
+
+    g = np.random.default_rng(k)
+    s = g.standard_normal((k, k)) * np.logspace(0, -6, k)[None, :]
+    lu, piv, info = lapack.dgetrf(s)
+    assert info == 0
+    rcond, info = lapack.dgecon(lu, np.abs(s).sum(axis=0).max(), norm="1")
+    want = 1.0 / rcond
+    est = cur._cond1(dense._mat(torch.from_numpy(s).cuda().contiguous()))
+    # same algorithm (dlacn2 on an LUPP with the same pivots), different rounding
+    assert abs(est - want) <= 1e-6 * want
