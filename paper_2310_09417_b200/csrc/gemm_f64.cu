@@ -52,6 +52,8 @@ using CfgRow = GemmCfg<128, 64, 16, 4, 2, 3, 2>;  // row-major A: 8 warps of 32x
 using CfgRow = GemmCfg<128, 64, 32, 4, 2, 2, 2>;
 #elif RS_ROW_VARIANT == 2
 using CfgRow = GemmCfg<128, 64, 16, 2, 2, 4, 2>;
+#elif RS_ROW_VARIANT == 4
+using CfgRow = GemmCfg<128, 64, 16, 2, 2, 3, 2>;  // 4 warps of 64x32, 3 stages: two CTAs fit an SM
 #else
 using CfgRow = GemmCfg<128, 64, 32, 2, 2, 2, 2>;
 #endif
