@@ -44,3 +44,65 @@ def test_adaptive_equals_one_shot_prefix(rs):
     blocks = [_draw_block(A, spec, rs.RngStream(32).child(t), 10).cpu().numpy() for t in range(res.rank // 10)]
     one = rs.lupp(np.hstack(blocks))
     assert np.array_equal(res.row_idx, one.perm[: res.rank])
+
+
+def _gaussian_spec(rs, n, ell=None):
+    return rs.SketchSpec("gaussian", n=n, ell=ell or min(n, 32))  # the reference helper (test_skeleton.py:8-9)
+
+
+def _exact_rank_matrix(m, n, r, seed):
+    g = np.random.default_rng(seed)
+    return g.standard_normal((m, r)) @ g.standard_normal((r, n))
+
+
+def test_adaptive_init_shapes_and_determinism(rs):
+    """Reference `test_skeleton.py:77-86`."""
+    a, _ = rs.gen_fast_decay(60, 40, 1e-10, rs.RngStream(10))
+    spec = _gaussian_spec(rs, 40)
+    s1 = rs.adaptive_init(a, 8, spec, rs.RngStream(11))
+    s2 = rs.adaptive_init(a, 8, spec, rs.RngStream(11))
+    assert s1.L1.shape == (8, 8)
+    assert np.array_equal(np.diagonal(s1.L1), np.ones(8))
+    assert np.abs(np.tril(s1.L1, -1)).max() <= 1 + 1e-14
+    assert np.array_equal(s1.perm, s2.perm)
+    assert np.array_equal(s1.ysofar, s2.ysofar)
+
+
+def test_adaptive_init_full_width_boundary(rs):
+    """Reference `test_skeleton.py:89-96`: the first block spans the factorable width."""
+    a, _ = rs.gen_fast_decay(30, 20, 1e-8, rs.RngStream(12))
+    res = rs.rand_lupp_adaptive(a, b=20, tau=1e-14, spec=_gaussian_spec(rs, 20), rng=rs.RngStream(13))
+    assert res.rank == 20
+    assert len(res.trace) == 1
+
+
+def test_adaptive_step_exact_rank_small_estimate(rs):
+    """Reference `test_skeleton.py:99-105`."""
+    a = _exact_rank_matrix(80, 60, 10, 14)
+    spec = _gaussian_spec(rs, 60)
+    state = rs.adaptive_init(a, 12, spec, rs.RngStream(15))
+    e, state2 = rs.adaptive_step(state, a, spec)
+    assert e <= 1e-10 * np.linalg.norm(a)
+    assert state2.rank == 24
+
+
+def test_adaptive_rank_detection_scaled(rs):
+    """Reference `test_skeleton.py:176-183`."""
+    a, _ = rs.gen_fast_decay(200, 200, 1e-16, rs.RngStream(24))
+    na = np.linalg.norm(a)
+    res = rs.rand_lupp_adaptive(a, b=20, tau=1e-4 * na, spec=_gaussian_spec(rs, 200), rng=rs.RngStream(25))
+    assert res.status == rs.STATUS_OK
+    assert 40 <= res.rank <= 80
+    assert rs.row_id_error(a, res) <= 3 * 1e-4 * na
+
+
+def test_adaptive_trace_monotone_on_decaying_spectra(rs):
+    """Reference `test_skeleton.py:186-195`: >= 95 % of seeded runs have a monotone trace."""
+    a, _ = rs.gen_fast_decay(150, 150, 1e-16, rs.RngStream(26))
+    spec = _gaussian_spec(rs, 150)
+    monotone = 0
+    for seed in range(20):
+        res = rs.rand_lupp_adaptive(a, b=15, tau=1e-13 * np.linalg.norm(a), spec=spec, rng=rs.RngStream(seed))
+        vals = [rec.e_schur for rec in res.trace]
+        monotone += all(b <= a_ for a_, b in zip(vals, vals[1:]))
+    assert monotone >= 19
