@@ -106,3 +106,59 @@ def test_adaptive_trace_monotone_on_decaying_spectra(rs):
         vals = [rec.e_schur for rec in res.trace]
         monotone += all(b <= a_ for a_, b in zip(vals, vals[1:]))
     assert monotone >= 19
+
+
+# --------------------------------------------------- reference test_dense.py on the device ---
+def test_lupp_matches_lapack_pivots(rs):
+    """Reference `test_dense.py:154-167`: LAPACK getrf picks the same first-maximum pivots."""
+    import scipy.linalg
+
+    for seed in range(8):
+        a = np.random.default_rng(seed).standard_normal((40, 25))
+        f = rs.lupp(a)
+        lu, piv = scipy.linalg.lu_factor(a)
+        perm = np.arange(40)
+        for i, p in enumerate(piv):
+            perm[[i, p]] = perm[[p, i]]
+        assert np.array_equal(f.perm, perm)
+        assert np.abs(f.L - (np.tril(lu[:, :25], -1) + np.eye(40, 25))).max() <= 1e-13
+        assert np.abs(f.U - np.triu(lu[:25, :25])).max() <= 1e-13
+
+
+def test_lupp_bitwise_deterministic(rs):
+    """Reference `test_dense.py:170-176`."""
+    a = np.random.default_rng(77).standard_normal((60, 30))
+    f1, f2 = rs.lupp(a), rs.lupp(a)
+    assert np.array_equal(f1.L, f2.L) and np.array_equal(f1.U, f2.U) and np.array_equal(f1.perm, f2.perm)
+
+
+@pytest.mark.parametrize("m,k,seed", [(20, 10, 0), (100, 60, 1), (300, 100, 2), (2, 1, 3), (24, 24, 4)])
+def test_lupp_reconstruction(rs, m, k, seed):
+    """Reference `test_dense.py:186-205` (shapes and the property test's bounds)."""
+    eps = np.finfo(float).eps
+    a = np.random.default_rng(seed).standard_normal((m, k))
+    f = rs.lupp(a)
+    assert np.linalg.norm(a[f.perm] - f.L @ f.U) <= 1e-12 * np.linalg.norm(a) * m
+    assert np.abs(np.tril(f.L, -1)).max(initial=0.0) <= 1 + 16 * eps
+
+
+@pytest.mark.parametrize("n", [2, 5, 10, 20, 30])
+def test_chan_growth_factor_tight(rs, n):
+    """Reference `test_dense.py:446-451`: growth exactly 2^(n-1), ties keep the first row."""
+    eps = np.finfo(float).eps
+    a = rs.gen_chan(n)
+    f = rs.lupp(a)
+    growth = np.abs(f.U).max() / np.abs(a).max()
+    assert abs(growth - 2.0 ** (n - 1)) <= 4 * eps * 2.0 ** (n - 1)
+    assert np.array_equal(f.perm, np.arange(n))
+
+
+def test_pinv_apply_reference_cases(rs):
+    """Reference `test_dense.py:422-433`: the null direction is truncated; normal equations hold."""
+    x = rs.pinv_apply(np.diag([2.0, 0.0]), [[2.0], [2.0]])
+    assert np.abs(np.asarray(x) - np.array([[1.0], [0.0]])).max() <= 1e-12
+    g = np.random.default_rng(17)
+    a = g.standard_normal((10, 4))
+    b = g.standard_normal((10, 2))
+    x = np.asarray(rs.pinv_apply(a, b))
+    assert np.abs(a.T @ (a @ x - b)).max() <= 1e-12
