@@ -162,3 +162,79 @@ def test_pinv_apply_reference_cases(rs):
     b = g.standard_normal((10, 2))
     x = np.asarray(rs.pinv_apply(a, b))
     assert np.abs(a.T @ (a @ x - b)).max() <= 1e-12
+
+
+# --------------------------------------------- reference test_acceptance.py on the device ---
+def test_criterion_01_lu_factorization_correctness(rs):
+    """Reference `test_acceptance.py:36-58`, the LU half (CPQR is the reference's
+    comparator, not on the hot path): 100 factorizations, scaled residual <= 1e-12."""
+    eps = np.finfo(float).eps
+    shapes = [(20, 10), (100, 60), (300, 100)]
+    worst_lu, worst_l = 0.0, 0.0
+    for i in range(100):
+        m, k = shapes[i % 3]
+        a = np.random.default_rng(i).standard_normal((m, k))
+        f = rs.lupp(a)
+        worst_lu = max(worst_lu, np.linalg.norm(a[f.perm] - f.L @ f.U) / (np.linalg.norm(a) * m))
+        worst_l = max(worst_l, np.abs(np.tril(f.L, -1)).max())
+    assert worst_lu <= 1e-12 and worst_l <= 1 + 16 * eps
+
+
+def test_criterion_06_growth_factor_bound(rs):
+    """Reference `test_acceptance.py:185-214`: svd tail / ||U_r||_F estimate <=
+    (4 log k / k) sqrt(m - k) at every rank of 20 seeded adaptive runs."""
+    a, sigma = rs.gen_fast_decay(500, 500, 1e-16, rs.RngStream(888))
+    m, p = 500, 10
+    violations, points = 0, set()
+    for seed in range(20):
+        rng = rs.RngStream(seed)
+        spec = rs.SketchSpec("gaussian", n=500, ell=45)
+        state = rs.adaptive_init(a, 45, spec, rng)
+        y_r = rs.draw_residual_sample(a, p, spec, rng)
+        while True:
+            k = state.rank
+            est = rs.residual_ur_estimates(state, a, p, spec, rng, sample_r=y_r)
+            tail = float(np.sqrt(np.sum(np.asarray(sigma)[k:] ** 2)))  # svd_tail_norm (dense.py:499)
+            points.add(k)
+            if tail / est.norm_ur > (4 * np.log(k) / k) * np.sqrt(m - k):
+                violations += 1
+            if k + 45 > 450:
+                break
+            _, state = rs.adaptive_step(state, a, spec)
+    assert violations == 0 and len(points) == 10
+
+
+def test_criterion_08_sketch_isometry(rs):
+    """Reference `test_acceptance.py:235-256`: 10^4 draws per kind."""
+    x = np.random.default_rng(31337).standard_normal((8, 64))
+    nx2 = np.linalg.norm(x) ** 2
+    for kind in ("gaussian", "srtt", "sparsesign"):
+        spec = rs.SketchSpec(kind, n=64, ell=16, zeta=8)
+        base = rs.RngStream(hash(kind) & 0xFFFF)
+        total = 0.0
+        for i in range(10_000):
+            op = rs.make_sketch(spec, base.child(i))
+            total += np.linalg.norm(np.asarray(rs.apply_sketch(x, op))) ** 2
+        assert 0.95 <= total / 10_000 / nx2 <= 1.05, kind
+
+
+def test_criterion_10_exact_rank_recovery(rs):
+    """Reference `test_acceptance.py:279-313` for the five hot-path methods (CPQR aside)."""
+    for r, seed in ((10, 1), (40, 2)):
+        g = np.random.default_rng(seed)
+        a = g.standard_normal((150, r)) @ g.standard_normal((r, 120))
+        na = np.linalg.norm(a)
+        spec = rs.SketchSpec("gaussian", n=120, ell=r)
+        rng = rs.RngStream(seed)
+        rl = rs.rand_lupp(a, r, spec, rng.child(1))
+        errs = [np.linalg.norm(a - rl.w @ a[rl.row_idx])]
+        ra = rs.rand_lupp_adaptive(a, b=r // 2, tau=1e-9 * na, spec=spec, rng=rng.child(3))
+        assert ra.rank == r
+        errs.append(np.linalg.norm(a - ra.w @ a[ra.row_idx]))
+        rc = rs.column_id(a, r, spec, rng.child(4))
+        errs.append(np.linalg.norm(a - a[:, rc.col_idx] @ rc.x))
+        rt = rs.two_sided_id(a, r, spec, rng.child(5))
+        errs.append(np.linalg.norm(a - rt.w @ a[np.ix_(rt.row_idx, rt.col_idx)] @ rt.x))
+        cur = rs.cur_decompose(a, r, spec, rng.child(6))
+        errs.append(np.linalg.norm(a - a[:, cur.col_idx] @ cur.u_mid @ a[cur.row_idx]))
+        assert max(errs) <= 1e-8 * na, (r, errs)
