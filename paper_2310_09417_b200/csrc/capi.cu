@@ -15,10 +15,16 @@ void count_launch(int n) { g_launch_count.fetch_add((unsigned long long)n, std::
 namespace {
 
 constexpr int kMaxB = 64;
+#ifndef RS_SCHUR_STAGE_B  // experiment builds: 0 = the GEMM gathers Y[perm[:k]] per stage
+#define RS_SCHUR_STAGE_B 1
+#endif
 
 struct WorkspaceLayout {
-  size_t panel_off, sumsq_off, gemm_off, total;
+  size_t panel_off, sumsq_off, gemm_off, ytop_off, total;
 };
+
+// Y[perm[:k]] staged contiguously for the Schur GEMM's B operand (k <= kYtopRows)
+constexpr long long kYtopRows = 65536;
 
 // Fixed layout (device independent); the GEMM ticket counters at the end of
 // the GEMM region must be zero when the workspace is first used.
@@ -28,7 +34,8 @@ WorkspaceLayout layout() {
   L.panel_off = 0;
   L.sumsq_off = up(rs::panel_workspace_bytes());
   L.gemm_off = L.sumsq_off + up(rs::sumsq_workspace_bytes());
-  L.total = L.gemm_off + up(rs::gemm_workspace_bytes());
+  L.ytop_off = L.gemm_off + up(rs::gemm_workspace_bytes());
+  L.total = L.ytop_off + up(sizeof(double) * (size_t)kYtopRows * kMaxB);
   return L;
 }
 
@@ -118,6 +125,15 @@ int rs_schur_block(int m, int k, int b, const double* Y, long long ldy, const in
   int rc;
   if (k == 0) {
     rc = rs::launch_gather_rows(Y, ldy, perm, R, b, S_, lds, S(stream));
+  } else if (k <= kYtopRows && RS_SCHUR_STAGE_B) {
+    // B = Y[perm[:k]] gathered once into a contiguous k x b block (16-byte loads), so the
+    // GEMM's B tiles need no per-stage row-index loads
+    double* ytop = reinterpret_cast<double*>(W(workspace, layout().ytop_off));
+    rc = rs::launch_gather_rows(Y, ldy, perm, k, b, ytop, b, S(stream));
+    if (rc != RS_OK) return rc;
+    rs::DGemmParams p = gemm_params(R, b, k, -1.0, T, ldt, nullptr, ytop, b, nullptr, 1.0, Y, ldy, perm + k, S_, lds,
+                                    RS_GEMM_PLAIN, workspace);
+    rc = rs::launch_dgemm(p, false, 0, S(stream));
   } else {
     rs::DGemmParams p = gemm_params(R, b, k, -1.0, T, ldt, nullptr, Y, ldy, perm, 1.0, Y, ldy, perm + k, S_, lds,
                                     RS_GEMM_PLAIN, workspace);
