@@ -162,6 +162,22 @@ int main(int argc, char** argv) {
   unsigned base = 0;
   int nsm;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  if (which == 9) {  // many launches at G = 32: per-launch step time (bimodality check)
+    for (int rep = 0; rep < 40; ++rep) {
+      int G = 32, busy = 0;
+      const int st2 = 200;
+      void* args[] = {&rec, (void*)&st2, &base, &out, &busy};
+      base += 1 << 16;
+      cudaEvent_t e0, e1;
+      cudaEventCreate(&e0); cudaEventCreate(&e1);
+      cudaEventRecord(e0);
+      cudaLaunchCooperativeKernel((void*)flat, G, 256, args, 0, 0);
+      cudaEventRecord(e1);
+      cudaDeviceSynchronize();
+      float ms; cudaEventElapsedTime(&ms, e0, e1);
+      printf("launch %d: %.3f us/step\n", rep, ms * 1e3 / st2);
+    }
+  }
   if (which == 0 || which == 1) for (int G : {32, 64, 96, 128, nsm}) {
     int busy = which;
     void* args[] = {&rec, (void*)&steps, &base, &out, &busy};
