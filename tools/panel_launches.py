@@ -9,6 +9,10 @@ REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, REPO)
 from paper_2310_09417_b200 import _device, _lib  # noqa: E402
 
+if os.environ.get("PANEL_LIB"):  # an experiment build instead of the library
+    _lib._lib = None
+    _lib.load(os.environ["PANEL_LIB"])
+
 ws, st = _device.workspace().data_ptr(), _device.stream_handle()
 for R in [int(x) for x in (sys.argv[1:] or ["2000", "4096", "16000"])]:
     S0 = torch.randn(R, 64, dtype=torch.float64, device="cuda")
@@ -24,4 +28,4 @@ for R in [int(x) for x in (sys.argv[1:] or ["2000", "4096", "16000"])]:
         ev[i + 1].record()
     torch.cuda.synchronize()
     t = [1e3 * ev[i].elapsed_time(ev[i + 1]) for i in range(30)]
-    print(f"R={R}: " + " ".join(f"{x:.0f}" for x in t) + f"  (us per launch; median {sorted(t)[15]:.0f})", flush=True)
+    print(f"{os.path.basename(os.environ.get('PANEL_LIB', 'librskel.so'))} R={R}: " + " ".join(f"{x:.0f}" for x in t) + f"  (us per launch; median {sorted(t)[15]:.0f})", flush=True)
