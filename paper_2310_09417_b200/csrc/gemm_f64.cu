@@ -54,6 +54,10 @@ using CfgRow = GemmCfg<128, 64, 32, 4, 2, 2, 2>;
 using CfgRow = GemmCfg<128, 64, 16, 2, 2, 4, 2>;
 #elif RS_ROW_VARIANT == 4
 using CfgRow = GemmCfg<128, 64, 16, 2, 2, 3, 2>;  // 4 warps of 64x32, 3 stages: two CTAs fit an SM
+#elif RS_ROW_VARIANT == 5
+using CfgRow = GemmCfg<128, 64, 16, 4, 2, 4, 2>;  // the library config with 4 stages
+#elif RS_ROW_VARIANT == 6
+using CfgRow = GemmCfg<128, 64, 8, 4, 2, 6, 2>;   // BK 8, 6 stages
 #else
 using CfgRow = GemmCfg<128, 64, 32, 2, 2, 2, 2>;
 #endif
