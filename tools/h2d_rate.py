@@ -42,3 +42,19 @@ for rep in range(3):
     print(f"rep {rep}: rc {rc} register {1e3*(t1-t0):.1f} ms, H2D {1e3*(t2-t1):.1f} ms, unregister {1e3*(t3-t2):.1f} ms | "
           f"fresh out: register {1e3*(t5-t4):.1f} ms, D2H {1e3*(t6-t5):.1f} ms, unregister {1e3*(t7-t6):.1f} ms", flush=True)
     del o
+
+# host-side copy alone: pageable -> reused pinned 32 MB buffers with the thread pool (no DMA)
+from paper_2310_09417_b200 import _omega  # noqa: E402
+
+pool = _omega._pool()
+bufs = [torch.empty(32 << 20, dtype=torch.uint8, pin_memory=True).numpy() for _ in range(4)]
+src = h.reshape(-1).view(np.uint8)
+for nthr in (8, 16):
+    t0 = time.perf_counter()
+    for i, c0 in enumerate(range(0, src.size, 32 << 20)):
+        c1 = min(src.size, c0 + (32 << 20))
+        buf = bufs[i % 4]
+        part = -(-(c1 - c0) // nthr)
+        list(pool.map(lambda q: np.copyto(buf[q:q + part][: max(0, min(part, c1 - c0 - q))], src[c0 + q:c0 + q + part][: max(0, min(part, c1 - c0 - q))]), range(0, c1 - c0, part)))
+    t1 = time.perf_counter()
+    print(f"host copy pageable->pinned, {nthr} threads: {gb / (t1 - t0):.1f} GB/s", flush=True)
