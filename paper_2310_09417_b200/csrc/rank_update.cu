@@ -372,7 +372,13 @@ int launch_rank_update(int M, int N, int K, const double* A, long long lda, cons
                     ldcin % 2 == 0 && ldc % 2 == 0;
   RankUpdateParams p{M, N, K, A, lda, B, ldb, bidx, Cin, ldcin, cidx, C, ldc, 0, 0};
   if (vec2 && K > 0 && K % 2 == 0 && N % 2 == 0) {
+#if !defined(RS_RU_VARIANT) || RS_RU_VARIANT == 0  // (experiment builds: tools/build_ru_cfg.sh)
     launch_stream<128, 1, 2>(p, nsm, st);
+#elif RS_RU_VARIANT == 1
+    launch_stream<64, 2, 3>(p, nsm, st);
+#else
+    launch_stream<64, 2, 2>(p, nsm, st);
+#endif
   } else {
     p.tiles_n = (N + UBN - 1) / UBN;
     p.tiles = p.tiles_n * ((M + UBM - 1) / UBM);

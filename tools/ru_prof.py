@@ -8,6 +8,10 @@ REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, REPO)
 from paper_2310_09417_b200 import _device, _lib  # noqa: E402
 
+if os.environ.get("RU_LIB"):  # an experiment build instead of the library
+    _lib._lib = None
+    _lib.load(os.environ["RU_LIB"])
+
 m, b, k = 20000, 64, int(os.environ.get("RU_K", 8000))
 R = m - k - b
 st = _device.stream_handle()
@@ -26,4 +30,4 @@ for _ in range(10):
 e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 10
-print(f"rank update R={R} k={k}: {ms:.3f} ms, {2 * R * k * b / ms / 1e9:.1f} TF/s, {16 * R * k / ms / 1e6:.0f} GB/s")
+print(f"{os.path.basename(os.environ.get('RU_LIB', 'librskel.so'))} rank update R={R} k={k}: {ms:.3f} ms, {2 * R * k * b / ms / 1e9:.1f} TF/s, {16 * R * k / ms / 1e6:.0f} GB/s")
