@@ -28,18 +28,22 @@
 // contiguous 16 KB bulk copy (cp.async.bulk, the TMA engine's linear mode)
 // and no tensor map is needed.  At SA = 8 the planes take 8 bytes per entry,
 // the same HBM traffic as the fp64 matrix, while the int8 tensor pipe does
-// the 36 plane products (4.5 POP/s dense) -- the sketch becomes HBM-bound
-// instead of bound by the 37 TF/s DMMA pipe.
+// the 36 plane products (4.5 POP/s dense) -- the sketch is no longer bound by
+// the 37 TF/s DMMA pipe (measured bound: the MMA issue through the stage
+// handshake).
 //
-// Kernel (one CTA per SM, persistent over (tile, chunk) units):
+// Kernel (one CTA per SM, persistent over (tile, chunk) units; the units after
+// the last full wave are halved over two CTAs, see oz_item):
 //   warp 0  producer: bulk copies of the Omega planes of a k-block (one copy
 //           of SB x 8 KB) and of the A planes (one 16 KB stage each);
-//   warp 1  TMEM owner + MMA issuer (one elected lane): for every A plane s
-//           and Omega plane t with s + t < G, 4 x tcgen05.mma m128n64k32
-//           into accumulator g = s + t; tcgen05.commit releases the stages;
-//   warps 2-5 epilogue: tcgen05.ld of the G int32 accumulators (one TMEM
-//           lane = one output row per thread), fp64 combination, chunk slot
-//           or direct store, last-arriving unit folds the chunk slots.
+//   warp 1  TMEM owner + MMA issuer (one thread): for every A plane s and
+//           Omega plane t with s + t < G, tcgen05.mma m128 n64..256 k32 into
+//           accumulator g = s + t; tcgen05.commit releases the stages;
+//   warps 2-9 epilogue, two warps per TMEM lane quadrant splitting the
+//           columns: tcgen05.ld of the G int32 accumulators (one TMEM lane =
+//           one output row per thread), exact int64 combination, fp64
+//           conversion, chunk slot or direct store; the last-arriving unit of
+//           a tile folds the chunk slots.
 #include <algorithm>
 #include <cstdio>
 #include <cstdint>
