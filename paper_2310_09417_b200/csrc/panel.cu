@@ -12,11 +12,13 @@
 // (|v|, pos, row, the row's values) with a release-store of a per-step
 // sequence number; warp 0 of every CTA polls the G sequence numbers (this is
 // the grid barrier and the data exchange in one round trip), reduces the G
-// candidates identically (deterministic), loads the pivot row, and all
-// threads scale column j and update column j+1 of their rows ("early"
-// update, one row per thread) to find the next candidate.  The rest of the
-// rank-1 update (columns j+2..w-1, "late" update) runs while warp 0 publishes
-// and waits for the next column, so it is off the critical path.
+// candidates identically (deterministic), loads the pivot row, and column j
+// is scaled and column j+1 updated for every local row ("early" update) to
+// find the next candidate -- by warp 0 alone with a warp argmax when a CTA
+// holds at most 192 rows, else by all threads with a block argmax.  The rest
+// of the rank-1 update (columns j+2..w-1, "late" update, warps 1-7) runs
+// while warp 0 publishes and waits for the next column, so it is off the
+// critical path.
 //
 // Arithmetic follows numpy's rounding exactly: l = s / pivot (IEEE division),
 // s' = s - (l * u) with the product rounded before the subtraction (np.outer
