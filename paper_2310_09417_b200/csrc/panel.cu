@@ -61,11 +61,18 @@ constexpr int PMAXG = 256;  // >= CTAs of the cooperative grid (one per SM)
 // LL-style exchange: every 8-byte word carries the step flag next to 4 bytes
 // of payload, so a reader that sees the flag in a word also sees its payload
 // (8-byte single-copy atomicity) -- no fences, no separate barrier.
+// Each CTA writes its record to NREP replicas in different lines; CTA c polls replica c % NREP,
+// so a hot record line has G / NREP pollers instead of G.
+#ifndef RS_PANEL_NREP
+#define RS_PANEL_NREP 8
+#endif
+constexpr int NREP = RS_PANEL_NREP;
+
 struct PanelScratch {
   // One 128-byte line per CTA for its record and for its copy of the winner
   // broadcast: no line is shared by two writers or polled by many readers
   // (a hot line serialises in its L2 slice and made each hop ~1.3 us).
-  uint4 rec[2][PMAXG][8];           // [0] = {val.lo, f, val.hi, f}, [1] = {pos, f, row + 1, f}
+  uint4 rec[2][NREP][PMAXG][8];     // [0] = {val.lo, f, val.hi, f}, [1] = {pos, f, row + 1, f}
   uint4 rowdata[2][PMAXG][PMAXW];   // candidate row: {x.lo, f, x.hi, f} per column
 };
 
@@ -297,16 +304,16 @@ __global__ void __launch_bounds__(PTHREADS, 1)
         }
         if (lane == 0) {
           const unsigned long long x = (unsigned long long)__double_as_longlong(cr >= 0 ? cv : -1.0);
-          st_v4(&ws->rec[par][rec_id][0], (unsigned)x, f, (unsigned)(x >> 32), f);
-          st_v4(&ws->rec[par][rec_id][1], (unsigned)cp, f, (unsigned)(cr + 1), f);
+          st_v4(&ws->rec[par][0][rec_id][0], (unsigned)x, f, (unsigned)(x >> 32), f);
+          st_v4(&ws->rec[par][0][rec_id][1], (unsigned)cp, f, (unsigned)(cr + 1), f);
         }
         PMARK(7);  // cluster reduce + global publish
         double v = -1.0;
         int pp = 0x7fffffff, rr = -1, cc = -1;
         if (lane < nrec) {
           for (;;) {
-            const uint4 qa = ld_v4(&ws->rec[par][lane][0]);
-            const uint4 qb = ld_v4(&ws->rec[par][lane][1]);
+            const uint4 qa = ld_v4(&ws->rec[par][0][lane][0]);
+            const uint4 qb = ld_v4(&ws->rec[par][0][lane][1]);
             if (qa.y != f || qa.w != f || qb.y != f || qb.w != f) continue;
             if ((int)qb.z - 1 >= 0) { v = join(qa.x, qa.z); pp = (int)qb.x; rr = (int)qb.z - 1; cc = lane; }
             break;
@@ -362,12 +369,12 @@ __global__ void __launch_bounds__(PTHREADS, 1)
       // ---- publish this CTA's candidate for column j (no fence needed).
       // The record goes first: it is what every CTA polls; the row values are
       // read only by the winner's readers, one exchange hop later. ----
-      if (lane == 0) {
+      if (lane < NREP) {  // (bv, bp, br are uniform across the warp)
         const double v = br >= 0 ? bv : -1.0;
         const unsigned long long x = (unsigned long long)__double_as_longlong(v);
         const unsigned growp1 = br >= 0 ? (unsigned)(r0 + br + 1) : 0u;
-        st_v4(&ws->rec[par][cta][0], (unsigned)x, f, (unsigned)(x >> 32), f);
-        st_v4(&ws->rec[par][cta][1], (unsigned)bp, f, growp1, f);
+        st_v4(&ws->rec[par][lane][cta][0], (unsigned)x, f, (unsigned)(x >> 32), f);
+        st_v4(&ws->rec[par][lane][cta][1], (unsigned)bp, f, growp1, f);
       }
       if (br >= 0) {
         for (int c = lane; c < w; c += 32) {
@@ -390,8 +397,8 @@ __global__ void __launch_bounds__(PTHREADS, 1)
 #pragma unroll
           for (int i = 0; i < QMAX; ++i) {
             if ((pending >> i) & 1u) {
-              a[i] = ld_v4(&ws->rec[par][lane + 32 * i][0]);
-              b[i] = ld_v4(&ws->rec[par][lane + 32 * i][1]);
+              a[i] = ld_v4(&ws->rec[par][cta % NREP][lane + 32 * i][0]);
+              b[i] = ld_v4(&ws->rec[par][cta % NREP][lane + 32 * i][1]);
             }
           }
 #pragma unroll
