@@ -67,13 +67,17 @@ constexpr int PMAXG = 256;  // >= CTAs of the cooperative grid (one per SM)
 #define RS_PANEL_NREP 8
 #endif
 constexpr int NREP = RS_PANEL_NREP;
+#ifndef RS_PANEL_RD_NREP  // replicas of the published candidate rows (pivot-row hop)
+#define RS_PANEL_RD_NREP 1
+#endif
+constexpr int RD_NREP = RS_PANEL_RD_NREP;
 
 struct PanelScratch {
   // One 128-byte line per CTA for its record and for its copy of the winner
   // broadcast: no line is shared by two writers or polled by many readers
   // (a hot line serialises in its L2 slice and made each hop ~1.3 us).
   uint4 rec[2][NREP][PMAXG][8];     // [0] = {val.lo, f, val.hi, f}, [1] = {pos, f, row + 1, f}
-  uint4 rowdata[2][PMAXG][PMAXW];   // candidate row: {x.lo, f, x.hi, f} per column
+  uint4 rowdata[2][RD_NREP][PMAXG][PMAXW];  // candidate row: {x.lo, f, x.hi, f} per column
 };
 
 RS_DEV void st_v4(uint4* p, unsigned a, unsigned b, unsigned c, unsigned d) {
@@ -299,7 +303,7 @@ __global__ void __launch_bounds__(PTHREADS, 1)
         if (cr >= 0) {
           for (int c = lane; c < w; c += 32) {
             const unsigned long long x = (unsigned long long)__double_as_longlong(crow[par][cm][c]);
-            st_v4(&ws->rowdata[par][rec_id][c], (unsigned)x, f, (unsigned)(x >> 32), f);
+            st_v4(&ws->rowdata[par][0][rec_id][c], (unsigned)x, f, (unsigned)(x >> 32), f);
           }
         }
         if (lane == 0) {
@@ -334,8 +338,8 @@ __global__ void __launch_bounds__(PTHREADS, 1)
           bool need0 = c0 < w, need1 = c1 < w;
           while (need0 || need1) {
             uint4 x0 = make_uint4(0, 0, 0, 0), x1 = make_uint4(0, 0, 0, 0);
-            if (need0) x0 = ld_v4(&ws->rowdata[par][cc][c0]);
-            if (need1) x1 = ld_v4(&ws->rowdata[par][cc][c1]);
+            if (need0) x0 = ld_v4(&ws->rowdata[par][0][cc][c0]);
+            if (need1) x1 = ld_v4(&ws->rowdata[par][0][cc][c1]);
             if (need0 && x0.y == f && x0.w == f) { u0 = join(x0.x, x0.z); need0 = false; }
             if (need1 && x1.y == f && x1.w == f) { u1 = join(x1.x, x1.z); need1 = false; }
           }
@@ -379,7 +383,9 @@ __global__ void __launch_bounds__(PTHREADS, 1)
       if (br >= 0) {
         for (int c = lane; c < w; c += 32) {
           const unsigned long long x = (unsigned long long)__double_as_longlong(at(br, c));
-          st_v4(&ws->rowdata[par][cta][c], (unsigned)x, f, (unsigned)(x >> 32), f);
+#pragma unroll
+          for (int rp = 0; rp < RD_NREP; ++rp)
+            st_v4(&ws->rowdata[par][rp][cta][c], (unsigned)x, f, (unsigned)(x >> 32), f);
         }
       }
       PMARK(0);  // publish
@@ -431,8 +437,8 @@ __global__ void __launch_bounds__(PTHREADS, 1)
         bool need0 = c0 < w, need1 = c1 < w;
         while (need0 || need1) {  // both words in flight at once
           uint4 x0 = make_uint4(0, 0, 0, 0), x1 = make_uint4(0, 0, 0, 0);
-          if (need0) x0 = ld_v4(&ws->rowdata[par][cc][c0]);
-          if (need1) x1 = ld_v4(&ws->rowdata[par][cc][c1]);
+          if (need0) x0 = ld_v4(&ws->rowdata[par][cta % RD_NREP][cc][c0]);
+          if (need1) x1 = ld_v4(&ws->rowdata[par][cta % RD_NREP][cc][c1]);
           if (need0 && x0.y == f && x0.w == f) { Urow2[par][c0] = join(x0.x, x0.z); need0 = false; }
           if (need1 && x1.y == f && x1.w == f) { Urow2[par][c1] = join(x1.x, x1.z); need1 = false; }
         }
