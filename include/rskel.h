@@ -203,6 +203,23 @@ int rs_srtt_dense(int n, int ell, const int64_t* perm, const double* signs, cons
 int rs_sparse_sign_dense(int n, int ell, int zeta, const int64_t* idx, const double* signs, double scale,
                          double* out, long long ldo, void* stream);
 
+/* Scratch bytes of rs_sparse_sign_apply's plan: two bitmaps (rows holding the
+ * column, negative signs) per operator column per 32 operator rows. */
+long long rs_sparse_sign_plan_bytes(int n, int ell);
+
+/* y = a @ Omega for the sparse-sign embedding without forming Omega: the
+ * reference's `(csr.T @ a.T).T` (`SparseSignSketch.apply`, sketching.py:176-185).
+ * a: m x n, row-major (a[i*lda + j]) or column-major (a[j*lda + i]); y: m x ell
+ * row-major.  Each y[i, c] is summed over the operator rows j holding c in
+ * ascending j with a separate multiply and add, scipy's csc_matvecs order, so
+ * the result is bitwise the reference's.  idx/signs: n x zeta (int64, +-1.0);
+ * plan: rs_sparse_sign_plan_bytes of device scratch; bad: a caller-zeroed device
+ * int, set to 1 (index outside [0, ell) or a sign other than +-1) or 2 (an index
+ * repeated within a row) -- y is then not meaningful. */
+int rs_sparse_sign_apply(long long m, int n, int ell, int zeta, const double* a, long long lda, int a_colmajor,
+                         const int64_t* idx, const double* signs, double scale, double* y, long long ldy, void* plan,
+                         int* bad, void* stream);
+
 /* Cholesky G = R^T R of a small SPD matrix (n <= 1024) in place (upper R,
  * strict lower part zeroed); *status_dev = 0 or j + 1 for a non-positive
  * pivot j.  The Gram step of pinv_apply (dense.py:166-182). */

@@ -74,15 +74,36 @@ def srtt_dense(seed, stream, n, ell):
     return np.sqrt(n / ell) * c[:, cols]
 
 
-def sparse_sign_dense(seed, stream, n, ell, zeta):
-    """`sketching.py:160-187,219-235`: dense sparse-sign embedding (n x ell)."""
+def sparse_sign_operator(seed, stream, n, ell, zeta):
+    """`sketching.py:219-235`: (idx, signs, scale) of the sparse-sign embedding."""
     g = np.random.Generator(np.random.Philox(key=[seed & _M64, stream & _M64]))
     u = g.random((n, ell))
     idx = np.argsort(u, axis=1)[:, :zeta]
     signs = g.integers(0, 2, size=(n, zeta)) * 2.0 - 1.0
+    return idx, signs, 1.0 / np.sqrt(zeta)
+
+
+def sparse_sign_dense(seed, stream, n, ell, zeta):
+    """`sketching.py:160-187,219-235`: dense sparse-sign embedding (n x ell)."""
+    idx, signs, scale = sparse_sign_operator(seed, stream, n, ell, zeta)
     om = np.zeros((n, ell))
     np.put_along_axis(om, idx, signs / np.sqrt(zeta), axis=1)
     return om
+
+
+def sparse_sign_apply(a, idx, signs, scale, ell):
+    """`SparseSignSketch.apply` (`sketching.py:176-185`): ``(csr.T @ a.T).T`` in
+    the order scipy's csc_matvecs evaluates it -- operator rows j ascending,
+    ``y[:, c] += v * a[:, j]`` with ``v = signs * scale`` (a multiply, then an
+    add), each y starting from zero."""
+    a = np.asarray(a, dtype=np.float64)
+    v = np.asarray(signs, dtype=np.float64) * scale
+    y = np.zeros((a.shape[0], ell))
+    for j in range(idx.shape[0]):
+        for z in range(idx.shape[1]):
+            c = idx[j, z]
+            y[:, c] += v[j, z] * a[:, j]
+    return y
 
 
 # ------------------------------------------------------------------- LUPP --

@@ -480,16 +480,37 @@ def sketch_omega(a, spec, rng):
     ``rng``: the device draw by default, the host draw under RSKEL_HOST_RNG=1.
     Same Omega bit for bit either way."""
     n, ell = spec.n, spec.ell
-    if spec.kind != "gaussian":  # SRTT / sparse sign: reference operator, dense on the device
+    if spec.kind != "gaussian":  # SRTT: dense on the device; sparse sign: SpMM
         from .sketching import make_sketch
 
-        return sketch_dev(a, make_sketch(spec, rng).device_dense())
+        op = make_sketch(spec, rng)
+        if spec.kind == "sparsesign":
+            return sparse_sign_apply(a, op.idx, op.signs, op.ell, op.scale)
+        return sketch_dev(a, op.device_dense())
     unit = spec.scale != "inv_sqrt_ell"
     if host_rng():
         om = torch.as_tensor(host_gaussian(rng, n, ell, unit)).to(device())
     else:
         om = gaussian(rng, n, ell, unit=unit)
     return sketch_dev(a, om)
+
+
+def sparse_sign_apply(a, idx, signs, ell, scale, out=None):
+    """Y = a @ Omega for a sparse-sign Omega given by its (n x zeta) index and
+    sign arrays, without forming Omega (`rs_sparse_sign_apply`; bitwise the
+    reference's scipy SpMM).  ``out``: an (m x ell) row-major fp64 device tensor."""
+    m, n = a.shape
+    dev = device()
+    idx_d = torch.as_tensor(np.ascontiguousarray(idx, dtype=np.int64)).to(dev)
+    sg_d = torch.as_tensor(np.ascontiguousarray(signs, dtype=np.float64)).to(dev)
+    zeta = idx_d.shape[1]
+    plan = torch.empty(max(1, int(_lib.load().rs_sparse_sign_plan_bytes(n, ell))), dtype=torch.uint8, device=dev)
+    bad = torch.zeros(1, dtype=torch.int32, device=dev)
+    y = out if out is not None else torch.empty((m, ell), dtype=torch.float64, device=dev)
+    _lib.call("rs_sparse_sign_apply", m, n, ell, zeta, a.ptr, a.ld, int(a.colmajor), idx_d.data_ptr(),
+              sg_d.data_ptr(), float(scale), y.data_ptr(), y.stride(0), plan.data_ptr(), bad.data_ptr(),
+              stream_handle())
+    return y
 
 
 def sketch_dev(a, om):

@@ -53,6 +53,9 @@ SIGNATURES = {
     "rs_what": (_c_int, [_p, _c_ll, _p, _c_int, _p, _c_int, _p, _c_ll, _p]),
     "rs_srtt_dense": (_c_int, [_c_int, _c_int, _p, _p, _p, _c_double, _p, _c_ll, _p]),
     "rs_sparse_sign_dense": (_c_int, [_c_int, _c_int, _c_int, _p, _p, _c_double, _p, _c_ll, _p]),
+    "rs_sparse_sign_plan_bytes": (_c_ll, [_c_int, _c_int]),
+    "rs_sparse_sign_apply": (_c_int, [_c_ll, _c_int, _c_int, _c_int, _p, _c_ll, _c_int, _p, _p, _c_double, _p, _c_ll,
+                                      _p, _p, _p]),
     "rs_jacobi_sweep": (_c_int, [_p, _c_ll, _c_int, _p, _c_ll, _c_int, _p, _c_int, _c_int, _c_double, _p, _p, _p]),
     "rs_gather2d": (_c_int, [_p, _c_ll, _c_ll, _p, _c_int, _p, _c_int, _p, _c_ll, _p]),
     "rs_gaussian_workspace_bytes": (ctypes.c_size_t, [_c_ll]),

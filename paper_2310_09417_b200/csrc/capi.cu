@@ -240,6 +240,18 @@ int rs_sparse_sign_dense(int n, int ell, int zeta, const int64_t* idx, const dou
   return rs::launch_sparse_sign_dense(n, ell, zeta, idx, signs, scale, out, ldo, S(stream));
 }
 
+long long rs_sparse_sign_plan_bytes(int n, int ell) {
+  if (n < 1 || ell < 1) return 0;
+  return rs::sparse_sign_plan_words(n, ell) * (long long)sizeof(unsigned);
+}
+
+int rs_sparse_sign_apply(long long m, int n, int ell, int zeta, const double* a, long long lda, int a_colmajor,
+                         const int64_t* idx, const double* signs, double scale, double* y, long long ldy, void* plan,
+                         int* bad, void* stream) {
+  return rs::launch_sparse_sign_apply(m, n, ell, zeta, a, lda, a_colmajor, idx, signs, scale, y, ldy,
+                                      static_cast<unsigned*>(plan), bad, S(stream));
+}
+
 int rs_cholesky(double* G, long long ldg, int n, int* status_dev, void* stream) {
   return rs::launch_cholesky(G, ldg, n, status_dev, S(stream));
 }

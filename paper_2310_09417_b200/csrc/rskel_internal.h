@@ -91,6 +91,10 @@ int launch_srtt_dense(int n, int ell, const int64_t* perm, const double* signs, 
                       double* out, long long ldo, cudaStream_t st);
 int launch_sparse_sign_dense(int n, int ell, int zeta, const int64_t* idx, const double* signs, double scale,
                              double* out, long long ldo, cudaStream_t st);
+long long sparse_sign_plan_words(int n, int ell);
+int launch_sparse_sign_apply(long long m, int n, int ell, int zeta, const double* a, long long lda, int colmajor,
+                             const int64_t* idx, const double* signs, double scale, double* y, long long ldy,
+                             unsigned* plan, int* bad, cudaStream_t st);
 int launch_cholesky(double* G, long long ldg, int n, int* status, cudaStream_t st);
 int launch_trsv_cols(const double* cols, long long ldc, int n, int lower, int unit, double* x, cudaStream_t st);
 int launch_norm1(const double* A, long long lda, int rows, int cols, double* out, cudaStream_t st);

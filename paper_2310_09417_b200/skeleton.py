@@ -412,7 +412,7 @@ class _AdaptiveDriver:
         # rank can reach b even when max_rank < b (`skeleton.py:435-441`)
         self.st = _engine.TFormState(m, max(max_rank, b), min(b, _engine.MAX_BLOCK))
         # tensor-core sketch: A's digit planes once, Omega_t's per block
-        self.ozaki = _ozaki.sketch_engine() == "ozaki" and self.yb is None
+        self.ozaki = _ozaki.sketch_engine() == "ozaki" and self.yb is None and self.kind != "sparsesign"
         if self.ozaki:
             tok = self.prof.start("a_slice")
             self.ap = planes if planes is not None else _ozaki.Planes.of_matrix(a)
@@ -427,7 +427,7 @@ class _AdaptiveDriver:
 
     # -- Omega pipeline --------------------------------------------------------
     def _issue_copy(self, t):
-        if t in self._issued:
+        if t in self._issued or self.kind == "sparsesign":
             return
         self._issued.add(t)
         slot = t % 2
@@ -465,6 +465,17 @@ class _AdaptiveDriver:
         if t < self.nb_pre:
             return
         slot = t % 2
+        if self.kind == "sparsesign":
+            # the reference's per-block operator (`skeleton.py:286-295`) applied
+            # as an SpMM on the compute stream: Y_t bitwise the reference's
+            from .lu_state import _block_spec
+
+            op = make_sketch(_block_spec(self.spec, self.n, self.b), self.rng.child(t))
+            tok = self.prof.start("sketch_gemm")
+            _device.sparse_sign_apply(self.a, op.idx, op.signs, op.ell, op.scale, out=self.y[slot])
+            self.prof.stop(tok)
+            self.y_ready[slot] = None
+            return
         self._issue_copy(t)
         if ahead and self.ozaki:
             ss = self.sketch_stream

@@ -191,10 +191,23 @@ class SparseSignSketch:
 
     def __init__(self, idx, signs, ell, scale):
         self.idx, self.signs, self.ell, self.scale = idx, signs, ell, scale
+        self._exact = None
 
     @property
     def shape(self):
         return (self.idx.shape[0], self.ell)
+
+    def spmm_exact(self):
+        """True when the operator is one the SpMM reproduces bitwise: signs of
+        +-1 and no index repeated within a row (every `make_sparse_sign` draw).
+        Hand-built operators outside that use the dense device form."""
+        if self._exact is None:
+            idx = np.asarray(self.idx)
+            srt = np.sort(idx, axis=1)
+            self._exact = bool(np.all(np.abs(np.asarray(self.signs)) == 1.0)
+                               and np.all(srt[:, 1:] != srt[:, :-1])
+                               and idx.min(initial=0) >= 0 and idx.max(initial=0) < self.ell)
+        return self._exact
 
     def device_dense(self):
         import torch
@@ -211,7 +224,14 @@ class SparseSignSketch:
         return out
 
     def apply(self, a):
-        return _apply_dense(self, a)
+        """``a @ Omega`` as an SpMM over the (index, sign) pairs, bitwise the
+        reference's `(csr.T @ a.T).T` (`sketching.py:176-185`)."""
+        if not self.spmm_exact():
+            return _apply_dense(self, a)
+        A = _device.as_matrix(a)
+        if A.cols != self.shape[0]:
+            raise DimensionError(f"operator ambient dimension {self.shape[0]} does not match {A.shape}")
+        return _device.to_output(_device.sparse_sign_apply(A, self.idx, self.signs, self.ell, self.scale), A)
 
     def to_dense(self):
         return self.device_dense().cpu().numpy()
@@ -261,6 +281,8 @@ def apply_sketch(a, op, side="right"):
     if isinstance(op, (SrttSketch, SparseSignSketch)):
         if target.cols != op.shape[0]:
             raise DimensionError(f"operator ambient dimension {op.shape[0]} does not match {target.shape}")
+        if isinstance(op, SparseSignSketch) and op.spmm_exact():
+            return _device.to_output(_device.sparse_sign_apply(target, op.idx, op.signs, op.ell, op.scale), a)
         return _device.to_output(_device.sketch_dev(target, op.device_dense()), a)
     omega = op if isinstance(op, np.ndarray) else getattr(op, "omega", None)
     if omega is None:

@@ -208,6 +208,18 @@ def test_oracle_structured_embeddings(kind):
     np.testing.assert_allclose(a @ om, g["y"], rtol=0, atol=1e-12)
 
 
+def test_oracle_sparse_sign_spmm_order_is_the_references():
+    """The oracle's SpMM restatement (csc_matvecs order: rows ascending, multiply
+    then add) reproduces the reference's `SparseSignSketch.apply` bit for bit,
+    on both application sides (golden `y`, `yt`)."""
+    g = golden("sketch_sparsesign")
+    a = np.random.default_rng(80).standard_normal((90, 70))
+    idx, signs, scale = orc.sparse_sign_operator(81, 0, 70, 16, 4)
+    assert np.array_equal(orc.sparse_sign_apply(a, idx, signs, scale, 16), g["y"])
+    idx, signs, scale = orc.sparse_sign_operator(82, 0, 90, 16, 4)
+    assert np.array_equal(orc.sparse_sign_apply(a.T, idx, signs, scale, 16), g["yt"])
+
+
 def test_cond1_estimate_straddles_limit():
     """The oracle's cond_1 is dgecon's estimate (skeleton.py:592-603), not the exact
     1-norm condition number: on this matrix they fall on opposite sides of 1e14."""
