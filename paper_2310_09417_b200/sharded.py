@@ -139,12 +139,13 @@ class DeviceShardOps:
     def scatter_rows(self, src, lds, idx, n, cols, dst, ldd):
         _lib.call("rs_scatter_rows", src.data_ptr(), lds, idx.data_ptr(), n, cols, dst.data_ptr(), ldd, self.st)
 
-    def schur(self, r, k, b, Tg, Ytop, Y, loc, out):
-        """out (r x b) = Y[loc] - Tg (r x k) @ Ytop (k x b)."""
+    def schur(self, r, k, b, Tg, Ytop, Y, loc, out, ldy=None):
+        """out (r x b) = Y[loc] - Tg (r x k) @ Ytop (k x b); Y rows ldy apart (default b)."""
+        ldy = b if ldy is None else ldy
         if k == 0:
-            return self.gather_rows(Y, b, loc, r, b, out, b)
+            return self.gather_rows(Y, ldy, loc, r, b, out, b)
         _lib.call("rs_dgemm", r, b, k, -1.0, Tg.data_ptr(), k, 0, None, Ytop.data_ptr(), b, None, 1.0,
-                  Y.data_ptr(), b, loc.data_ptr(), out.data_ptr(), b, self.ws.data_ptr(), self.st)
+                  Y.data_ptr(), ldy, loc.data_ptr(), out.data_ptr(), b, self.ws.data_ptr(), self.st)
 
     def sumsq(self, X, R, w, out):
         _lib.call("rs_sumsq", X.data_ptr(), w, R, w, out.data_ptr(), self.ws.data_ptr(), self.st)
@@ -217,7 +218,8 @@ def rand_lupp_adaptive_sharded(a_local, b, tau, spec, rng, max_rank=None, group=
     the candidate rows (rank order = row order).  Same stopping rule, trace
     and statuses; returns a SkeletonResult whose ``row_idx``/``rank``/
     ``trace``/``status`` are global (identical on every rank) and whose ``w``
-    holds this rank's rows of W.  Block width b <= 64 (one panel per block).
+    holds this rank's rows of W.  Any block width: b <= 64 is one panel per block
+    (pipelined), b > 64 is factored as 64-column panels (`_run_wide`).
     """
     if ops is None:
         a_local = _device.as_matrix(a_local)
@@ -238,8 +240,6 @@ def rand_lupp_adaptive_sharded(a_local, b, tau, spec, rng, max_rank=None, group=
         raise ValueError(f"tau must be positive, got {tau}")
     if not 1 <= b <= min(m, n):
         raise DimensionError(f"block size must be in [1, {min(m, n)}], got {b}")
-    if b > MAX_BLOCK:
-        raise NotImplementedError("the sharded loop factors one panel per block: b <= 64")
     if spec.kind != "gaussian":
         raise NotImplementedError(f"sketch kind {spec.kind!r} is outside the B200 hot path (Gaussian only)")
     if max_rank is None:
@@ -310,32 +310,40 @@ class _ShardedLoop:
         self.k = 0
         self.r = mg  # upper bound of the local row count (exact after each readback)
 
-    def _schur(self, Y):
+    def _schur(self, Y, j0=0, w=None):
+        """Schur block of columns [j0, j0 + w) of the block sketch Y (rows b
+        apart) into S (R x w, position order) and its squared norm into e2."""
         o, b, k = self.ops, self.b, self.k
+        w = b if w is None else w
+        Yj = Y[j0:] if j0 else Y
         Tg = self.T[self.cur]
         if k > 0:
-            o.gather_rows(Y, b, self.ytop_src, k, b, self.Ytop, b)
-            _allreduce(self.Ytop[: k * b], self.group)
-        o.schur(self.r, k, b, Tg, self.Ytop, Y, self.loc, self.Sg)
+            o.gather_rows(Yj, b, self.ytop_src, k, w, self.Ytop, w)
+            _allreduce(self.Ytop[: k * w], self.group)
+        if w == b:
+            o.schur(self.r, k, w, Tg, self.Ytop, Yj, self.loc, self.Sg)
+        else:
+            o.schur(self.r, k, w, Tg, self.Ytop, Yj, self.loc, self.Sg, ldy=b)
         R = self.m - k
-        S = self.S[self.scur][: R * b]
+        S = self.S[self.scur][: R * w]
         if self.world == 1:
-            o.scatter_rows(self.Sg, b, self.spos, self.r, b, S, b)
+            o.scatter_rows(self.Sg, w, self.spos, self.r, w, S, w)
         else:
             # the one exchange of pivot candidates: every rank's Schur rows and their
             # positions (padded to P rows, padding at position -1) all-gathered, then
-            # scattered into position order -- R (b + 1) words per rank received
+            # scattered into position order -- R (w + 1) words per rank received
             P = self.pmax
-            recv, rpos = self.recv[: self.world * P * b], self.recv_pos[: self.world * P]
-            dist.all_gather_into_tensor(recv, self.Sg[: P * b], group=self.group)
+            recv, rpos = self.recv[: self.world * P * w], self.recv_pos[: self.world * P]
+            dist.all_gather_into_tensor(recv, self.Sg[: P * w], group=self.group)
             dist.all_gather_into_tensor(rpos, self.spos[:P], group=self.group)
-            o.scatter_rows(recv, b, rpos, self.world * P, b, S, b)
-        o.sumsq(S, R, b, self.e2)
+            o.scatter_rows(recv, w, rpos, self.world * P, w, S, w)
+        o.sumsq(S, R, w, self.e2)
 
-    def _absorb(self, nc):
-        """Fold nc factored columns of the current S into (T, perm); launches
-        sized by the row-count bound self.r."""
-        o, b, m = self.ops, self.b, self.m
+    def _absorb(self, nc, w=None):
+        """Fold nc factored columns of the current S (R x w, default w = b) into
+        (T, perm); launches sized by the row-count bound self.r."""
+        o, m = self.ops, self.m
+        b = self.b if w is None else w
         k_old, cur, S = self.k, self.cur, self.S[self.scur]
         k_new = k_old + nc
         nxt = 1 - cur
@@ -357,11 +365,64 @@ class _ShardedLoop:
         self._prev = (cur, k_old)
         self.cur, self.k = nxt, k_new
 
+    def _run_wide(self):
+        """b > 64 (the paper's b = 128): each block is factored as 64-column
+        panels, the single-GPU wide path (`_absorb_block`, the blocked
+        `_lupp_partial` of `skeleton.py:318-351`): e_schur sums the sub-blocks'
+        squared norms against the state before the block; then each sub-block's
+        Schur rows are formed against the state that already holds the earlier
+        sub-blocks, exchanged, factored and absorbed.  Synchronous per panel."""
+        o, b, m, tau = self.ops, self.b, self.m, self.tau
+        trace = ErrorTrace()
+        status = STATUS_NOT_CONVERGED
+        t = 0
+        while True:
+            Y = self.Ys[t % 2]
+            o.sketch(o.omega(self.rng, t, b), b, Y)
+            e2 = 0.0
+            for j0 in range(0, b, MAX_BLOCK):
+                self._schur(Y, j0, min(MAX_BLOCK, b - j0))
+                e2 += float(o.read(self.e2)[0])
+            if t > 0:
+                e_schur = math.sqrt(e2) if e2 >= 0 else float("nan")
+                trace.append(TraceRecord(k=self.k, e_schur=e_schur))
+                if e_schur <= tau:
+                    status = STATUS_OK
+                    break
+                if self.k + b > self.max_rank:
+                    break
+            if not math.isfinite(e2):
+                raise ValueError("matrix contains non-finite entries")
+            done = 0
+            for j0 in range(0, b, MAX_BLOCK):
+                w = min(MAX_BLOCK, b - j0)
+                self._schur(Y, j0, w)
+                o.panel(self.S[self.scur], m - self.k, w, self.sub, self.meta[0:1])
+                (nc,) = o.read(self.meta[0:1])
+                self._absorb(nc, w)
+                if self.world > 1:
+                    self.r, self.pmax = o.read(self.meta[1:2], self.meta[2:3])
+                else:
+                    (self.r,) = o.read(self.meta[1:2])
+                done += nc
+                if nc < w:
+                    break
+            if done < b:
+                if t == 0:
+                    raise RankDeficientError(done)
+                status = STATUS_RANK_EXHAUSTED
+                break
+            t += 1
+        return trace, status
+
     def run(self):
         o, b, m, tau = self.ops, self.b, self.m, self.tau
         o.iota(self.perm[0], m)
         o.maps(self.perm[0], m, 0, self.lo, self.hi, None, None, 0, 0, self.lrow[0], self.loc, self.spos, None,
                None, None, self.ytop_src, self.meta[1:2], self.pmax if self.world > 1 else 0)
+        if b > MAX_BLOCK:
+            trace, status = self._run_wide()
+            return self._result(trace, status)
         trace = ErrorTrace()
         status = STATUS_NOT_CONVERGED
         from . import skeleton
@@ -440,6 +501,10 @@ class _ShardedLoop:
             self.scur = 1 - self.scur  # the next Schur block goes to the other buffer
             pending = True
             t += 1
+        return self._result(trace, status)
+
+    def _result(self, trace, status):
+        o = self.ops
         k = self.k
         mg = self.hi - self.lo
         W = o.f64(mg * k)

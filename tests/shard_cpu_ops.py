@@ -59,8 +59,10 @@ class CpuShardOps:
             if r >= 0:
                 d[r * ldd: r * ldd + cols] = s[i * lds: i * lds + cols]
 
-    def schur(self, r, k, b, Tg, Ytop, Y, loc, out):
-        y = _np(Y)[: self.a.shape[0] * b].reshape(-1, b)[_np(loc)[:r]]
+    def schur(self, r, k, b, Tg, Ytop, Y, loc, out, ldy=None):
+        ldy = b if ldy is None else ldy
+        rows = _np(loc)[:r].astype(np.int64)
+        y = _np(Y)[rows[:, None] * ldy + np.arange(b)[None, :]]
         if k > 0:
             y = y - _np(Tg)[: r * k].reshape(r, k) @ _np(Ytop)[: k * b].reshape(k, b)
         _np(out)[: r * b] = y.ravel()

@@ -42,7 +42,10 @@ def _single(a, b, tau, seed):
     return rs.rand_lupp_adaptive(a, b, tau, spec, rs.RngStream(seed))
 
 
-def test_sharded_world1_bitwise_equals_single():
+@pytest.mark.parametrize("b", [64, 128, 96])
+def test_sharded_world1_bitwise_equals_single(b):
+    """b = 64 (one panel per block) and b > 64 (64-column panels per block, the
+    paper's b = 128)."""
     import torch.distributed as dist
 
     import paper_2310_09417_b200 as rs
@@ -50,12 +53,12 @@ def test_sharded_world1_bitwise_equals_single():
 
     a = _matrix(700, 500, 2)
     tau = 1e-9 * np.linalg.norm(a)
-    ref = _single(a, 64, tau, 4)
+    ref = _single(a, b, tau, 4)
     store = dist.HashStore()
     dist.init_process_group("gloo", store=store, rank=0, world_size=1)
     try:
-        spec = rs.SketchSpec("gaussian", 500, 64)
-        got = rand_lupp_adaptive_sharded(a, 64, tau, spec, rs.RngStream(4))
+        spec = rs.SketchSpec("gaussian", 500, b)
+        got = rand_lupp_adaptive_sharded(a, b, tau, spec, rs.RngStream(4))
     finally:
         dist.destroy_process_group()
     assert got.rank == ref.rank and got.status == ref.status
@@ -95,7 +98,9 @@ def _worker(rank, world, port, case, q):
 @pytest.mark.parametrize("case", [
     (900, 600, 64, 1e-9, 3, [400, 500]),
     (1000, 700, 32, 1e-11, 5, [300, 350, 350]),
-], ids=["w2-b64", "w3-b32"])
+    (900, 700, 128, 1e-9, 7, [450, 450]),
+    (1000, 800, 96, 1e-11, 8, [200, 500, 300]),
+], ids=["w2-b64", "w3-b32", "w2-b128", "w3-b96"])
 def test_sharded_multi_rank_one_gpu(case):
     import torch.multiprocessing as mp
 

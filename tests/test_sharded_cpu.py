@@ -74,10 +74,15 @@ CASES = [
     ("decay", 240, 160, 8, 1e-6, 3, [60, 120, 60], None),     # 3 ranks, uneven
     ("zero_rows", 60, 40, 8, 1e-30, 5, [25, 35], None),       # rank_exhausted at 12
     ("decay", 200, 150, 16, 1e-14, 1, [10, 190], 96),          # not_converged at max_rank
+    # b > 64: each block factored as 64-column panels (the paper's b = 128)
+    ("decay", 400, 300, 96, 1e-6, 3, [150, 250], None),       # panels 64 + 32, converges
+    ("decay", 420, 380, 128, 1e-14, 1, [420], 256),           # one rank, not_converged at max_rank
+    ("decay", 420, 380, 128, 1e-14, 1, [100, 200, 120], 256),  # three ranks, same case
 ]
 
 
-@pytest.mark.parametrize("case", CASES, ids=["ok-2", "ok-3-uneven", "exhausted-2", "maxrank-2"])
+@pytest.mark.parametrize("case", CASES, ids=["ok-2", "ok-3-uneven", "exhausted-2", "maxrank-2", "wide96-2",
+                                             "wide128-1", "wide128-3"])
 def test_sharded_matches_oracle(case):
     import torch.multiprocessing as mp
 
