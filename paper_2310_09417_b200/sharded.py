@@ -109,6 +109,20 @@ class DeviceShardOps:
         _lib.call("rs_sketch_gemm", m, n, b, self.a.ptr, self.a.ld, int(self.a.colmajor), om.data_ptr(), b,
                   out.data_ptr(), b, ws.data_ptr(), st)
 
+    def sketch_structured(self, spec, rng, t, b, out):
+        """Block t of an SRTT / sparse-sign embedding on the local rows: the
+        reference's operator from rng.child(t); sparse sign as the SpMM (bitwise
+        the reference's rows), SRTT dense through the sketch engine."""
+        from .lu_state import _block_spec
+        from .sketching import make_sketch
+
+        m, n = self.a.shape
+        op = make_sketch(_block_spec(spec, n, b), rng.child(t))
+        if spec.kind == "sparsesign":
+            _device.sparse_sign_apply(self.a, op.idx, op.signs, op.ell, op.scale, out=out[: m * b].view(m, b))
+        else:
+            self.sketch(op.device_dense(), b, out)
+
     def sketch_async(self, rng, t, b, out, prof=None):
         """Omega_t draw + sketch on a side stream (own workspace), so they
         overlap the current block's exchanges and panel; `wait_sketch` joins."""
@@ -240,12 +254,10 @@ def rand_lupp_adaptive_sharded(a_local, b, tau, spec, rng, max_rank=None, group=
         raise ValueError(f"tau must be positive, got {tau}")
     if not 1 <= b <= min(m, n):
         raise DimensionError(f"block size must be in [1, {min(m, n)}], got {b}")
-    if spec.kind != "gaussian":
-        raise NotImplementedError(f"sketch kind {spec.kind!r} is outside the B200 hot path (Gaussian only)")
     if max_rank is None:
         max_rank = max(b, min(m, n) - b)
     max_rank = min(max_rank, min(m, n))
-    res = _ShardedLoop(ops, group, m, n, lo, hi, b, tau, rng, max_rank, counts).run()
+    res = _ShardedLoop(ops, group, m, n, lo, hi, b, tau, rng, max_rank, counts, spec).run()
     ok = torch.tensor([1 if (not hasattr(ops, "rng_ok") or ops.rng_ok()) else 0], dtype=torch.int32,
                       device=ops.dev)
     if _world(group)[0] > 1:
@@ -253,7 +265,7 @@ def rand_lupp_adaptive_sharded(a_local, b, tau, spec, rng, max_rank=None, group=
     if int(ok.item()) == 0:  # a draw the device resolver could not place (never observed): host draws
         if hasattr(ops, "host_rng"):
             ops.host_rng = True
-        res = _ShardedLoop(ops, group, m, n, lo, hi, b, tau, rng, max_rank, counts).run()
+        res = _ShardedLoop(ops, group, m, n, lo, hi, b, tau, rng, max_rank, counts, spec).run()
     return res
 
 
@@ -266,8 +278,11 @@ class _ShardedLoop:
     short block (an exactly zero pivot) is re-absorbed from its own factored
     Schur block, kept in the other S buffer."""
 
-    def __init__(self, ops, group, m, n, lo, hi, b, tau, rng, max_rank, counts=None):
+    def __init__(self, ops, group, m, n, lo, hi, b, tau, rng, max_rank, counts=None, spec=None):
         self.ops, self.group = ops, group
+        # SRTT / sparse sign: the reference's per-block operator (`skeleton.py:286-295`),
+        # the same on every rank (drawn from rng.child(t)), applied to the local rows
+        self.spec = spec if spec is not None and spec.kind != "gaussian" else None
         self.m, self.n, self.lo, self.hi = m, n, lo, hi
         self.b, self.tau, self.rng, self.max_rank = b, tau, rng, max_rank
         mg = hi - lo
@@ -365,6 +380,13 @@ class _ShardedLoop:
         self._prev = (cur, k_old)
         self.cur, self.k = nxt, k_new
 
+    def _sketch_block(self, t, out):
+        o, b = self.ops, self.b
+        if self.spec is not None:
+            o.sketch_structured(self.spec, self.rng, t, b, out)
+        else:
+            o.sketch(o.omega(self.rng, t, b), b, out)
+
     def _run_wide(self):
         """b > 64 (the paper's b = 128): each block is factored as 64-column
         panels, the single-GPU wide path (`_absorb_block`, the blocked
@@ -378,7 +400,7 @@ class _ShardedLoop:
         t = 0
         while True:
             Y = self.Ys[t % 2]
-            o.sketch(o.omega(self.rng, t, b), b, Y)
+            self._sketch_block(t, Y)
             e2 = 0.0
             for j0 in range(0, b, MAX_BLOCK):
                 self._schur(Y, j0, min(MAX_BLOCK, b - j0))
@@ -431,7 +453,7 @@ class _ShardedLoop:
         pending = False  # speculative full-width absorb awaiting its ncols
         sketched = set()
 
-        ahead_ok = hasattr(o, "sketch_async")
+        ahead_ok = hasattr(o, "sketch_async") and self.spec is None
 
         def sketch(tt, ahead=False):
             if tt in sketched:
@@ -444,9 +466,8 @@ class _ShardedLoop:
                 # this block's exchanges, panel and absorb
                 o.sketch_async(self.rng, tt, b, self.Ys[tt % 2], prof=prof)
                 return
-            om = o.omega(self.rng, tt, b)
             tok = prof.start("sketch_gemm")
-            o.sketch(om, b, self.Ys[tt % 2])
+            self._sketch_block(tt, self.Ys[tt % 2])
             prof.stop(tok)
 
         t = 0

@@ -43,6 +43,16 @@ class CpuShardOps:
         m, n = self.a.shape
         _np(out)[: m * b] = (self.a @ om).ravel()
 
+    def sketch_structured(self, spec, rng, t, b, out):
+        m, n = self.a.shape
+        st = orc.child_stream(self.stream, t)
+        if spec.kind == "sparsesign":
+            idx, sg, sc = orc.sparse_sign_operator(self.seed, st, n, b, min(spec.zeta, b))
+            y = orc.sparse_sign_apply(self.a, idx, sg, sc, b)
+        else:
+            y = self.a @ orc.srtt_dense(self.seed, st, n, b)
+        _np(out)[: m * b] = y.ravel()
+
     def iota(self, p, n):
         _np(p)[:n] = np.arange(n)
 

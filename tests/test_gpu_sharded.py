@@ -67,6 +67,31 @@ def test_sharded_world1_bitwise_equals_single(b):
     assert np.array_equal(got.w, ref.w)
 
 
+@pytest.mark.parametrize("sk", ["sparsesign", "srtt"])
+def test_sharded_structured_world1_bitwise_equals_single(sk):
+    """SRTT / sparse-sign blocks: the sharded loop applies the reference's per-block
+    operator to its rows (sparse sign through the SpMM) exactly as the single-GPU loop."""
+    import torch.distributed as dist
+
+    import paper_2310_09417_b200 as rs
+    from paper_2310_09417_b200.sharded import rand_lupp_adaptive_sharded
+
+    a = _matrix(600, 450, 3)
+    tau = 1e-9 * np.linalg.norm(a)
+    kw = {"zeta": 6} if sk == "sparsesign" else {}
+    ref = rs.rand_lupp_adaptive(a, 48, tau, rs.SketchSpec(sk, 450, 48, **kw), rs.RngStream(9))
+    store = dist.HashStore()
+    dist.init_process_group("gloo", store=store, rank=0, world_size=1)
+    try:
+        got = rand_lupp_adaptive_sharded(a, 48, tau, rs.SketchSpec(sk, 450, 48, **kw), rs.RngStream(9))
+    finally:
+        dist.destroy_process_group()
+    assert got.rank == ref.rank and got.status == ref.status and got.rank > 48
+    assert np.array_equal(got.row_idx, ref.row_idx)
+    assert [(r.k, r.e_schur) for r in got.trace] == [(r.k, r.e_schur) for r in ref.trace]
+    assert np.array_equal(got.w, ref.w)
+
+
 def _worker(rank, world, port, case, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     sys.path[:0] = [REPO, HERE]

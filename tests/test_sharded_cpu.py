@@ -52,12 +52,13 @@ def _worker(rank, world, port, case, q):
 
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        kind, m, n, b, tau, seed, counts, max_rank = case
+        kind, m, n, b, tau, seed, counts, max_rank = case[:8]
+        sk = case[8] if len(case) > 8 else "gaussian"
         a = _matrix(kind, m, n, seed)
         lo = sum(counts[:rank])
         hi = lo + counts[rank]
         ops = CpuShardOps(a[lo:hi], seed)
-        spec = rs.SketchSpec("gaussian", n, b)
+        spec = rs.SketchSpec(sk, n, b, **({"zeta": 4} if sk == "sparsesign" else {}))
         res = rand_lupp_adaptive_sharded(a[lo:hi], b, tau, spec, rs.RngStream(seed), max_rank=max_rank, ops=ops)
         q.put((rank, res.rank, np.asarray(res.row_idx), res.status,
                [(r.k, r.e_schur) for r in res.trace], np.asarray(res.w)))
@@ -79,6 +80,47 @@ CASES = [
     ("decay", 420, 380, 128, 1e-14, 1, [420], 256),           # one rank, not_converged at max_rank
     ("decay", 420, 380, 128, 1e-14, 1, [100, 200, 120], 256),  # three ranks, same case
 ]
+
+
+def _run_world(case):
+    import torch.multiprocessing as mp
+
+    world = len(case[6])
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = {}
+    try:
+        for _ in range(world):
+            item = q.get(timeout=240)
+            assert item[1] != "error", item
+            outs[item[0]] = item
+    finally:
+        for p in procs:
+            p.join(timeout=60)
+            if p.is_alive():
+                p.kill()
+    return outs
+
+
+@pytest.mark.parametrize("sk", ["sparsesign", "srtt"])
+def test_sharded_structured_sketch_world_invariant(sk):
+    """SRTT / sparse-sign blocks in the sharded loop: every rank applies the same
+    per-block operator to its rows, so 1 and 3 ranks give the same skeleton,
+    trace bits and W."""
+    base = ("decay", 300, 200, 16, 1e-8, 6)
+    one = _run_world(base + ([300], None, sk))
+    three = _run_world(base + ([90, 110, 100], None, sk))
+    _, k1, r1, s1, t1, w1 = one[0]
+    assert k1 > 16 and len(t1) >= 2
+    for r in range(3):
+        _, k, ri, st, tr, _ = three[r]
+        assert (k, st, tr) == (k1, s1, t1)
+        assert np.array_equal(ri, r1)
+    assert np.array_equal(np.vstack([three[r][5] for r in range(3)]), w1)
 
 
 @pytest.mark.parametrize("case", CASES, ids=["ok-2", "ok-3-uneven", "exhausted-2", "maxrank-2", "wide96-2",
