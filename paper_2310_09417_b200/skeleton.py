@@ -421,6 +421,10 @@ class _AdaptiveDriver:
             self.sketch_stream = torch.cuda.Stream(device=dev)
             self.ws_ahead = _device.workspace(slot=1)
         self.y_ready = [None, None]
+        # a large numpy W: its pages are faulted in while the loop runs (host idle)
+        self.w_host = None
+        if a.kind == "numpy" and 8 * m * max(max_rank, b) >= (256 << 20):
+            self.w_host = _device.HostPrefault(8 * m * max(max_rank, b))
         self.stream = _device.stream_handle()
         self.ws = _device.workspace()
         self._issued = set()
@@ -611,6 +615,8 @@ class _AdaptiveDriver:
                     break
                 if not math.isfinite(e2):
                     raise ValueError("matrix contains non-finite entries")
+                if self.w_host is not None:
+                    self.w_host.advance(8 * self.m * (st.k + 2 * b))
                 if not wide:
                     tok = self.prof.start("panel")
                     st.panel(b, self.nc)
@@ -633,6 +639,10 @@ class _AdaptiveDriver:
                 if nc < b:
                     status = STATUS_RANK_EXHAUSTED
                     break
+        except BaseException:
+            if self.w_host is not None:
+                self.w_host.close()
+            raise
         finally:
             if self.src is not None:
                 self.src.close()
@@ -644,6 +654,8 @@ class _AdaptiveDriver:
             # a block the parallel ziggurat resolver could not place (never
             # observed): redo the whole loop with the host draw, same bits
             self.dev_rng = False
+            if self.w_host is not None:
+                self.w_host.close()
             self.__init__(self.a, self.b, self.tau, self.rng, self.max_rank, host=True, spec=self.spec)
             # (the presketched blocks are dropped: every block is redrawn on the host)
             return self.run()
@@ -653,4 +665,4 @@ class _AdaptiveDriver:
         self.prof.stop(tok)
         kind = self.a.kind
         return SkeletonResult(rank=k, row_idx=_device.to_host_index(st.perm[:k].clone(), kind),
-                              w=_device.to_output(w, kind), trace=trace, status=status)
+                              w=_device.to_output(w, kind, host_out=self.w_host), trace=trace, status=status)

@@ -121,3 +121,21 @@ def test_zoo_generators_match_reference_construction():
         rs.gen_fast_decay(3, 5, 0.5, rs.RngStream(0))
     with pytest.raises(ValueError):
         rs.gen_kahan(4, 1.5)
+
+
+def test_host_prefault_result_buffer():
+    """HostPrefault: pages populated in the background up to advance(), the result a
+    contiguous writeable zero-filled array over the mapping; close is idempotent."""
+    from paper_2310_09417_b200._device import HostPrefault
+
+    hp = HostPrefault(64 << 20)
+    hp.advance(10 << 20)
+    hp.advance(5 << 20)  # never moves back
+    a = hp.array((1000, 1000), np.float64)
+    assert a.flags.c_contiguous and a.flags.writeable and a.shape == (1000, 1000)
+    assert not a.any()
+    a[:] = 3.0
+    assert a.sum() == 3.0e6
+    hp.close()
+    big = HostPrefault(1 << 20).array((1000, 1000), np.float64)  # larger than the mapping
+    assert big.shape == (1000, 1000)
