@@ -238,14 +238,9 @@ static int ss_launch(long long m, int n, int ell, const double* a, long long lda
   const size_t stage = (size_t)(cm ? SC * RB : RB * (SC + 1)) + (2 * KQ * CG + 1) / 2;
   const size_t smem = SS_STAGES * stage * sizeof(double);
   auto k = cm ? sparse_sign_apply_kernel<RPL, CPW, KQ, true> : sparse_sign_apply_kernel<RPL, CPW, KQ, false>;
-  static int configured[64] = {0};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 64 && !(configured[dev] & (cm ? 2 : 1))) {
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-      return RS_ERR_CUDA;
-    configured[dev] |= cm ? 2 : 1;
-  }
+  // set on every launch (cheap), so every device of the process has it
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return RS_ERR_CUDA;
   const dim3 grid((unsigned)((m + RB - 1) / RB), (unsigned)((ell + CG - 1) / CG));
   k<<<grid, SS_WARPS * 32, smem, st>>>(m, n, ell, a, lda, nq, nzm, sgm, scale, y, ldy);
   count_launch(1);
