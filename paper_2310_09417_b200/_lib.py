@@ -12,7 +12,9 @@ import os
 from .errors import DeviceError
 
 _PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG_DIR, "librskel.so")
+_DEFAULT_LIB = os.path.join(_PKG_DIR, "librskel.so")
+# experiment builds (tools/build_*_variants.sh) can be loaded in place of the library
+LIB_PATH = os.environ.get("RSKEL_LIB_PATH") or _DEFAULT_LIB
 
 _c_int = ctypes.c_int
 _c_ll = ctypes.c_longlong

@@ -666,8 +666,12 @@ int launch_panel(double* S, long long lds, int R, int w, int64_t* perm_out, int*
 #endif
   constexpr int CL = RS_PANEL_CLUSTER;
   constexpr int FLAT_MAX = 64;  // the flat exchange's hop is ~1 us up to 64 records, ~3 us at 148
+#ifndef RS_PANEL_MAXG  // experiment cap on the grid (fewer, fuller CTAs: a cheaper exchange)
+#define RS_PANEL_MAXG 1024
+#endif
   int G = (R + RS_PANEL_ROWS - 1) / RS_PANEL_ROWS;
   if (G > nsm) G = nsm;
+  if (G > RS_PANEL_MAXG) G = RS_PANEL_MAXG;
   if (G > PMAXG) G = PMAXG;
   if (G < 1) G = 1;
   size_t static_smem = 2048;  // >= the kernel's static shared memory (12 KB with the cluster slots)
