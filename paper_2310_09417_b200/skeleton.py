@@ -328,6 +328,39 @@ def _presketch(a, b, rng, max_rank, spec):
     return A, yb, nb
 
 
+class _BlockOperators:
+    """SRTT / sparse-sign block operators (the reference's per-block draw,
+    `skeleton.py:286-295`) drawn ahead on the host thread pool: numpy releases
+    the GIL in the uniform fill and the argsort, so the draws of the next
+    blocks (~30 ms each for a 20000 x 64 sparse sign) overlap each other and
+    the device work of the current block.  Same operators, same order."""
+
+    def __init__(self, spec, n, b, rng, nblocks, depth=None):
+        import os
+
+        from . import _omega
+        from .lu_state import _block_spec
+
+        if depth is None:  # blocks drawn ahead (RSKEL_OPS_AHEAD=1: the current block only)
+            depth = int(os.environ.get("RSKEL_OPS_AHEAD", "8"))
+
+        self.sp, self.rng, self.nblocks, self.depth = _block_spec(spec, n, b), rng, nblocks, depth
+        self.pool = _omega._pool()
+        self.fut = {}
+
+    def get(self, t):
+        for u in range(t, min(self.nblocks, t + self.depth)):
+            if u not in self.fut:
+                self.fut[u] = self.pool.submit(make_sketch, self.sp, self.rng.child(u))
+        f = self.fut.pop(t, None)
+        return f.result() if f is not None else make_sketch(self.sp, self.rng.child(t))
+
+    def close(self):
+        for f in self.fut.values():
+            f.cancel()
+        self.fut.clear()
+
+
 class PhaseTimer:
     """Optional CUDA-event instrumentation of the adaptive loop phases
     (sketch / schur / panel / absorb / interp), used by bench.py for the
@@ -395,6 +428,8 @@ class _AdaptiveDriver:
         self.dev_rng = not (host or _device.host_rng())
         self.src = None if (self.dev_rng or self.kind != "gaussian") else _omega.BlockOmegaSource(n, b, rng)
         self.rng_status = torch.zeros(max(max_rank, b) // b + 4, dtype=torch.int32, device=dev)
+        self.ops_ahead = (None if self.kind == "gaussian" else
+                          _BlockOperators(spec, n, b, rng, self.rng_status.numel()))
         self.om = [torch.empty((n, b), dtype=torch.float64, device=dev) for _ in range(2)]
         self.y = [torch.empty((m, b), dtype=torch.float64, device=dev) for _ in range(2)]
         self.om_ready = [torch.cuda.Event() for _ in range(2)]
@@ -442,12 +477,8 @@ class _AdaptiveDriver:
             if self.om_free[slot] is not None:
                 self.copy_stream.wait_event(self.om_free[slot])
             if self.kind != "gaussian":
-                # SRTT / sparse sign: the reference's per-block operator
-                # (`skeleton.py:286-295`), dense on the device
-                from .lu_state import _block_spec
-
-                op = make_sketch(_block_spec(self.spec, self.n, self.b), self.rng.child(t))
-                self.om[slot].copy_(op.device_dense())
+                # SRTT: the reference's per-block operator (`skeleton.py:286-295`), dense on the device
+                self.om[slot].copy_(self.ops_ahead.get(t).device_dense())
             elif h is None:
                 _device.gaussian(self.rng.child(t), self.n, self.b, out=self.om[slot],
                                  status=self.rng_status[t:t + 1])
@@ -472,9 +503,7 @@ class _AdaptiveDriver:
         if self.kind == "sparsesign":
             # the reference's per-block operator (`skeleton.py:286-295`) applied
             # as an SpMM on the compute stream: Y_t bitwise the reference's
-            from .lu_state import _block_spec
-
-            op = make_sketch(_block_spec(self.spec, self.n, self.b), self.rng.child(t))
+            op = self.ops_ahead.get(t)
             tok = self.prof.start("sketch_gemm")
             _device.sparse_sign_apply(self.a, op.idx, op.signs, op.ell, op.scale, out=self.y[slot])
             self.prof.stop(tok)
@@ -646,6 +675,8 @@ class _AdaptiveDriver:
         finally:
             if self.src is not None:
                 self.src.close()
+            if self.ops_ahead is not None:
+                self.ops_ahead.close()
             # speculative draws / sketches may still be in flight on the side streams
             self.compute.wait_stream(self.copy_stream)
             if self.ozaki:
