@@ -203,41 +203,70 @@ def cpu_sample(a_host, b, tau, seed, blocks):
     return dt, out["rank"], algo_flops(m, n, out["rank"], b), cores
 
 
+def workload_config(args, world, sharded=None):
+    """The workload both arms name in `config` (same dict for --impl reference):
+    cfg2 at N = 1, cfg5 column-sharded at N > 1.  Run outputs go to `result`."""
+    cfg5 = world > 1
+    n = args.n or (65536 if cfg5 else 20000)
+    b, tau = args.b, args.tau
+    sharded = (world > 1 or args.sharded) if sharded is None else sharded
+    return {
+        "workload": (f"cfg5: rand_lupp_adaptive_sharded(A[:, J_g].T, b={b}, tau={tau:g} abs) on a {n}x{n} "
+                     f"fp64 fast-decay matrix (beta=1e-16, randomized-Hadamard bases), column-sharded"
+                     if cfg5 else
+                     f"cfg2: rand_lupp_adaptive(A.T, b={b}, tau={tau:g} abs) on a {n}x{n} "
+                     f"fp64 fast-decay matrix (beta=1e-16, Haar bases), seed {args.seed}"),
+        "n": n, "b": b, "tau": tau, "seed": args.seed,
+        "parallelism": (f"A column-sharded over {world} GPUs (all-reduce of Y_top, S, T_P per block)"
+                        if sharded else "1 GPU"),
+        "l2": "inputs (A: %.1f GB) larger than L2 between steps" % (n * n * 8 / 1e9),
+    }
+
+
 def reference_arm(args, rank):
     if rank != 0:
         return
     import torch
 
     dev = torch.device("cuda", 0) if torch.cuda.is_available() else None
-    n = args.n or 20000
-    if dev is not None:
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    config = workload_config(args, world)
+    n = config["n"]
+    if world > 1 and dev is not None:  # cfg5: the same device generator as the GPU arm
+        import paper_2310_09417_b200 as rs
+
+        a = rs.gen_fast_decay_hadamard(n, 1e-16, rs.RngStream(args.seed).child(1 << 41))[0].cpu().numpy()
+        torch.cuda.empty_cache()
+    elif dev is not None:
         a = gen_fast_decay_device(n, 1e-16, args.seed, dev).cpu().numpy()
     else:  # no GPU: generate on the host (slow for large n)
         sys.path.insert(0, os.path.join(REPO, "oracle"))
         import randskel_oracle as orc
         a, _ = orc.gen_fast_decay(n, n, 1e-16, args.seed)
     at = a.T
+    # cfg5 (65536^2): a block costs ~16x a cfg2 block on the host; 2 blocks keep a step ~10 s
+    blocks = max(1, args.cpu_blocks // 4) if world > 1 else args.cpu_blocks
     for _ in range(max(0, min(args.warmup, 1))):
-        cpu_sample(at, args.b, args.tau, args.seed, args.cpu_blocks)
+        cpu_sample(at, args.b, args.tau, args.seed, blocks)
     times, flops = [], []
     for _ in range(args.steps):
-        dt, k, f, cores = cpu_sample(at, args.b, args.tau, args.seed, args.cpu_blocks)
+        dt, k, f, cores = cpu_sample(at, args.b, args.tau, args.seed, blocks)
         times.append(dt)
         flops.append(f)
     ms = 1e3 * float(np.median(times))
     val = flops[0] / (ms * 1e-3) / 1e12
-    sample = (f"BOUNDED SAMPLE: the first {args.cpu_blocks} blocks (rank 0 -> {k}) of the adaptive loop on "
-              f"the same {n}x{n} fast-decay matrix (the GPU arm runs all ~227 blocks); numpy/OpenBLAS "
-              f"oracle port, median of {args.steps}.  The whole loop on 16 host cores of this pool took "
-              f"235 s = 0.066 TF/s (profiles/r01_cfg2_full_parity.json), i.e. the sample overstates the "
-              f"CPU's whole-loop throughput ~3x")
+    sample = (f"BOUNDED SAMPLE: the first {blocks} blocks (rank 0 -> {k}) of the adaptive loop on "
+              f"the same {n}x{n} fast-decay matrix (the GPU arm runs the whole loop); numpy/OpenBLAS "
+              f"oracle port on {cores} host cores of rank 0, single process, median of {args.steps}.  "
+              f"The whole cfg2 loop on 16 host cores of this pool took 235 s = 0.066 TF/s "
+              f"(profiles/r01_cfg2_full_parity.json), i.e. the sample overstates the CPU's whole-loop "
+              f"throughput ~3x")
     line = {
         "impl": "reference", "metric": "adaptive column-ID throughput (algorithmic TFLOP/s)",
         "value": val, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"cfg2 adaptive column ID {n}x{n} fp64 fast-decay, b={args.b}, "
-                               f"tau={args.tau:g} (abs), bounded CPU sample", "n": n, "b": args.b},
+        "config": config,
         "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": cores, "kind": "port",
                          "sample": sample},
         "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -430,19 +459,9 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {
-                "workload": (f"cfg5: rand_lupp_adaptive_sharded(A[:, J_g].T, b={b}, tau={tau:g} abs) on a {n}x{n} "
-                             f"fp64 fast-decay matrix (beta=1e-16, randomized-Hadamard bases), column-sharded"
-                             if cfg5 else
-                             f"cfg2: rand_lupp_adaptive(A.T, b={b}, tau={tau:g} abs) on a {n}x{n} "
-                             f"fp64 fast-decay matrix (beta=1e-16, Haar bases), seed {args.seed}"),
-                "sketch_engine": rs.sketch_engine(),
-                "n": n, "b": b, "tau": tau, "rank": k, "status": res.status,
-                "row_id_error_rel": resid,
-                "blocks": len(res.trace) + 1, "parallelism": (f"A column-sharded over {world} GPUs ({backend} all-reduce of Y_top, S, T_P per block)"
-                                if sharded else "1 GPU"),
-                "l2": "inputs (A: %.1f GB) larger than L2 between steps" % (n * n * 8 / 1e9),
-            },
+            "config": workload_config(args, world, sharded),
+            "result": {"rank": k, "status": res.status, "row_id_error_rel": resid, "blocks": len(res.trace) + 1,
+                       "sketch_engine": rs.sketch_engine(), "collective_backend": backend if sharded else None},
             "seconds_per_step": ms_max / 1e3,
             "phase_ms_per_step": phase_ms,
             "roofline": roofline,

@@ -29,6 +29,8 @@ def test_reference_arm_contract():
     assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
     assert line["value"] > 0 and line["higher_is_better"] is True
+    assert {"workload", "n", "b", "tau", "seed", "parallelism", "l2"} <= set(line["config"])
+    assert line["config"]["n"] == 400 and line["config"]["workload"].startswith("cfg2:")
 
 
 @pytest.mark.gpu
@@ -41,4 +43,7 @@ def test_b200_arm_contract():
     assert line["e2e"]["h2d_bytes_per_step"] > 0 and line["e2e"]["value"] > 0
     assert line["gpu_launches"] > 0
     assert line["cpu_baseline"]["kind"] == "port"
-    assert line["config"]["status"] in ("ok", "not_converged", "rank_exhausted")
+    assert line["result"]["status"] in ("ok", "not_converged", "rank_exhausted")
+    # the reference arm names the same workload (the driver compares the two lines' config)
+    ref = _run(["--impl", "reference", "--size", "1500", "--steps", "1", "--warmup", "1", "--cpu-blocks", "2"])
+    assert ref["config"] == line["config"]
