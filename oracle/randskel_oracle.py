@@ -195,9 +195,13 @@ class LUState:
         return self.U1.shape[0]
 
 
-def block(a, seed, stream, t, b):
+def block(a, seed, stream, t, b, zeta=None):
     """Sketch block t: a @ Omega_t, Omega_t ~ N(0, 1/b) from child(t)
-    (`skeleton.py:286-295`)."""
+    (`skeleton.py:286-295`); with ``zeta`` the sparse-sign block of the same
+    stream (`_block_spec`: zeta capped at b), applied in scipy's SpMM order."""
+    if zeta is not None:
+        idx, sg, sc = sparse_sign_operator(seed, child_stream(stream, t), a.shape[1], b, min(zeta, b))
+        return sparse_sign_apply(a, idx, sg, sc, b)
     return a @ gaussian(seed, child_stream(stream, t), a.shape[1], b)
 
 
@@ -223,9 +227,9 @@ def extend(state, y, u2, L, U, sperm, nc):
     return LUState(L1, L2, U1, perm, np.hstack([state.ysofar, y[:, :nc]]))
 
 
-def adaptive_init(a, b, seed, stream=0):
+def adaptive_init(a, b, seed, stream=0, zeta=None):
     """`skeleton.py:298-314`."""
-    y = block(a, seed, stream, 0, b)
+    y = block(a, seed, stream, 0, b, zeta)
     L, U, perm, _ = lupp(y)
     return LUState(L[:b].copy(), L[b:].copy(), U, perm, y)
 
@@ -262,20 +266,21 @@ def residual_ur_estimates(state, a, p, seed, stream=0):
     return dict(norm_ur=norm_ur, max_ur=max_ur, est_norm=factor * norm_ur, est_max=factor * max_ur)
 
 
-def rand_lupp_adaptive(a, b, tau, seed, stream=0, max_rank=None, want_w=True, max_blocks=None):
+def rand_lupp_adaptive(a, b, tau, seed, stream=0, max_rank=None, want_w=True, max_blocks=None, zeta=None):
     """`skeleton.py:391-460`: returns dict(rank, row_idx, w, trace, status).
 
     ``max_blocks`` (not in the reference) stops after that many sketch blocks
-    -- the bounded CPU-baseline sample of bench.py."""
+    -- the bounded CPU-baseline sample of bench.py.  ``zeta``: sparse-sign
+    blocks with that many nonzeros per row instead of Gaussian ones."""
     a = np.asarray(a, dtype=np.float64)
     m, n = a.shape
     if max_rank is None:
         max_rank = max(b, min(m, n) - b)
     max_rank = min(max_rank, min(m, n))
-    state = adaptive_init(a, b, seed, stream)
+    state = adaptive_init(a, b, seed, stream, zeta)
     trace, status, t = [], "not_converged", 1
     while max_blocks is None or t < max_blocks:
-        y = block(a, seed, stream, t, b)
+        y = block(a, seed, stream, t, b, zeta)
         u2, s = schur(state, y)
         e = float(np.linalg.norm(s))
         trace.append((state.rank, e))

@@ -120,3 +120,19 @@ def test_adaptive_loop_sparse_sign_sketches_are_the_references():
     tr = np.array([[r.k, r.e_schur] for r in res.trace])
     # the last entry is at rounding level (exact-rank input): absolute floor 1e-12 x the first
     np.testing.assert_allclose(tr, ga["trace"], rtol=1e-9, atol=1e-12 * ga["trace"][0, 1])
+
+
+@pytest.mark.parametrize("b,zeta", [(32, 8), (64, 4)])
+def test_adaptive_sparse_sign_vs_oracle(b, zeta):
+    """The sparse-sign adaptive loop at 1500 x 1200 against the oracle's (pinned to the
+    reference's golden sparse-sign case): with Y_t bitwise the reference's, rank, status and
+    pivots match exactly; the trace to 1e-9 relative."""
+    rs = _rs()
+    a, _ = orc.gen_fast_decay(1500, 1200, 1e-12, 3, 77)
+    tau = 1e-8 * np.linalg.norm(a)
+    ref = orc.rand_lupp_adaptive(a, b, tau, 11, zeta=zeta)
+    got = rs.rand_lupp_adaptive(a, b, tau, rs.SketchSpec("sparsesign", 1200, b, zeta=zeta), rs.RngStream(11))
+    assert got.rank == ref["rank"] and got.status == ref["status"] and got.rank > 2 * b
+    assert np.array_equal(got.row_idx, ref["row_idx"])
+    tr = np.array([[r.k, r.e_schur] for r in got.trace])
+    np.testing.assert_allclose(tr, np.array(ref["trace"]), rtol=1e-9, atol=1e-12 * np.linalg.norm(a))

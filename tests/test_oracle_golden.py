@@ -220,6 +220,18 @@ def test_oracle_sparse_sign_spmm_order_is_the_references():
     assert np.array_equal(orc.sparse_sign_apply(a.T, idx, signs, scale, 16), g["yt"])
 
 
+def test_oracle_sparse_sign_adaptive_matches_reference():
+    """The oracle's adaptive loop with sparse-sign blocks reproduces the reference's
+    golden case (rank, status, pivots, trace)."""
+    ga = golden("adapt_sparsesign")
+    gg = np.random.default_rng(84)
+    b_exact = gg.standard_normal((120, 25)) @ gg.standard_normal((25, 90))
+    r = orc.rand_lupp_adaptive(b_exact, 8, 1e-9, 85, zeta=4)
+    assert r["rank"] == int(ga["rank"]) and r["status"] == str(ga["status"])
+    assert np.array_equal(r["row_idx"], ga["row_idx"])
+    np.testing.assert_allclose(np.array(r["trace"]), ga["trace"], rtol=1e-12, atol=1e-12 * ga["trace"][0, 1])
+
+
 def test_cond1_estimate_straddles_limit():
     """The oracle's cond_1 is dgecon's estimate (skeleton.py:592-603), not the exact
     1-norm condition number: on this matrix they fall on opposite sides of 1e14."""
