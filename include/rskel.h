@@ -203,6 +203,21 @@ int rs_srtt_dense(int n, int ell, const int64_t* perm, const double* signs, cons
 int rs_sparse_sign_dense(int n, int ell, int zeta, const int64_t* idx, const double* signs, double scale,
                          double* out, long long ldo, void* stream);
 
+/* Device scratch for rs_srtt_apply to transform m rows of length n in one batch
+ * (fewer bytes are accepted: the rows then go in batches). */
+long long rs_srtt_workspace_bytes(long long m, int n);
+
+/* y = a @ Omega for the SRTT embedding as a fast transform, the reference's
+ * `SrttSketch.apply` (sketching.py:147-155): per row, the DCT-II (ortho) of
+ * a[i, perm] through one length-n real FFT (Makhoul's reordering; cuFFT D2Z),
+ * times signs[k], at the sampled frequencies k = cols[j], times scale.
+ * O(m n log n); agrees with the reference to floating-point rounding (pocketfft's
+ * order cannot be reproduced).  a: m x n row- or column-major; y: m x ell row-major;
+ * ws: >= rs_srtt_workspace_bytes(1, n) bytes. */
+int rs_srtt_apply(long long m, int n, int ell, const double* a, long long lda, int a_colmajor, const int64_t* perm,
+                  const double* signs, const int64_t* cols, double scale, double* y, long long ldy, void* ws,
+                  long long ws_bytes, void* stream);
+
 /* Scratch bytes of rs_sparse_sign_apply's plan: two bitmaps (rows holding the
  * column, negative signs) per operator column per 32 operator rows. */
 long long rs_sparse_sign_plan_bytes(int n, int ell);

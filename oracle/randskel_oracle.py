@@ -74,6 +74,24 @@ def srtt_dense(seed, stream, n, ell):
     return np.sqrt(n / ell) * c[:, cols]
 
 
+def srtt_operator(seed, stream, n, ell):
+    """`sketching.py:207-216`: (perm, signs, cols, scale) of the SRTT embedding."""
+    g = np.random.Generator(np.random.Philox(key=[seed & _M64, stream & _M64]))
+    perm = g.permutation(n)
+    signs = g.integers(0, 2, size=n) * 2.0 - 1.0
+    cols = g.choice(n, size=ell, replace=False)
+    return perm, signs, cols, np.sqrt(n / ell)
+
+
+def srtt_apply(a, perm, signs, cols, scale):
+    """`SrttSketch.apply` (`sketching.py:147-155`): scale * (DCT-II_ortho(a[:, perm]) * signs)[:, cols]."""
+    import scipy.fft
+
+    c = scipy.fft.dct(np.asarray(a, dtype=np.float64)[:, perm], type=2, axis=1, norm="ortho")
+    c *= signs
+    return scale * c[:, cols]
+
+
 def sparse_sign_operator(seed, stream, n, ell, zeta):
     """`sketching.py:219-235`: (idx, signs, scale) of the sparse-sign embedding."""
     g = np.random.Generator(np.random.Philox(key=[seed & _M64, stream & _M64]))

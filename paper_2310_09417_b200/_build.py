@@ -75,7 +75,7 @@ def build(force=False, verbose=False):
                 raise RuntimeError("nvcc failed building librskel.so")
             if verbose:
                 sys.stderr.write(res.stderr)
-        link = subprocess.run([nvcc, *ARCH_FLAGS, "-shared", "-o", LIB_PATH + ".tmp", *objs],
+        link = subprocess.run([nvcc, *ARCH_FLAGS, "-shared", "-o", LIB_PATH + ".tmp", *objs, "-lcufft"],
                               capture_output=True, text=True)
         if link.returncode != 0:
             sys.stderr.write(link.stdout + link.stderr)

@@ -582,6 +582,24 @@ def sketch_omega(a, spec, rng):
     return sketch_dev(a, om)
 
 
+def srtt_apply(a, perm, signs, cols, scale, out=None):
+    """Y = a @ Omega for an SRTT Omega given by (perm, signs, cols, scale) as a fast
+    transform (`rs_srtt_apply`: per-row DCT-II through one real FFT, O(m n log n))."""
+    m, n = a.shape
+    dev = device()
+    ell = len(cols)
+    perm_d = torch.as_tensor(np.ascontiguousarray(perm, dtype=np.int64)).to(dev)
+    sg_d = torch.as_tensor(np.ascontiguousarray(signs, dtype=np.float64)).to(dev)
+    cols_d = torch.as_tensor(np.ascontiguousarray(cols, dtype=np.int64)).to(dev)
+    lib = _lib.load()
+    nbytes = min(int(lib.rs_srtt_workspace_bytes(m, n)), max(256 << 20, int(lib.rs_srtt_workspace_bytes(1, n))))
+    ws = torch.empty(max(1, nbytes), dtype=torch.uint8, device=dev)
+    y = out if out is not None else torch.empty((m, ell), dtype=torch.float64, device=dev)
+    _lib.call("rs_srtt_apply", m, n, ell, a.ptr, a.ld, int(a.colmajor), perm_d.data_ptr(), sg_d.data_ptr(),
+              cols_d.data_ptr(), float(scale), y.data_ptr(), y.stride(0), ws.data_ptr(), nbytes, stream_handle())
+    return y
+
+
 def sparse_sign_apply(a, idx, signs, ell, scale, out=None):
     """Y = a @ Omega for a sparse-sign Omega given by its (n x zeta) index and
     sign arrays, without forming Omega (`rs_sparse_sign_apply`; bitwise the

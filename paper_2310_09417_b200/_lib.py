@@ -55,6 +55,9 @@ SIGNATURES = {
     "rs_what": (_c_int, [_p, _c_ll, _p, _c_int, _p, _c_int, _p, _c_ll, _p]),
     "rs_srtt_dense": (_c_int, [_c_int, _c_int, _p, _p, _p, _c_double, _p, _c_ll, _p]),
     "rs_sparse_sign_dense": (_c_int, [_c_int, _c_int, _c_int, _p, _p, _c_double, _p, _c_ll, _p]),
+    "rs_srtt_workspace_bytes": (_c_ll, [_c_ll, _c_int]),
+    "rs_srtt_apply": (_c_int, [_c_ll, _c_int, _c_int, _p, _c_ll, _c_int, _p, _p, _p, _c_double, _p, _c_ll, _p, _c_ll,
+                               _p]),
     "rs_sparse_sign_plan_bytes": (_c_ll, [_c_int, _c_int]),
     "rs_sparse_sign_apply": (_c_int, [_c_ll, _c_int, _c_int, _c_int, _p, _c_ll, _c_int, _p, _p, _c_double, _p, _c_ll,
                                       _p, _p, _p]),

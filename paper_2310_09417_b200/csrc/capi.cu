@@ -240,6 +240,18 @@ int rs_sparse_sign_dense(int n, int ell, int zeta, const int64_t* idx, const dou
   return rs::launch_sparse_sign_dense(n, ell, zeta, idx, signs, scale, out, ldo, S(stream));
 }
 
+long long rs_srtt_workspace_bytes(long long m, int n) {
+  if (m < 0 || n < 1) return 0;
+  return rs::srtt_workspace_bytes(m, n);
+}
+
+int rs_srtt_apply(long long m, int n, int ell, const double* a, long long lda, int a_colmajor, const int64_t* perm,
+                  const double* signs, const int64_t* cols, double scale, double* y, long long ldy, void* ws,
+                  long long ws_bytes, void* stream) {
+  return rs::launch_srtt_apply(m, n, ell, a, lda, a_colmajor, perm, signs, cols, scale, y, ldy, ws, ws_bytes,
+                               S(stream));
+}
+
 long long rs_sparse_sign_plan_bytes(int n, int ell) {
   if (n < 1 || ell < 1) return 0;
   return rs::sparse_sign_plan_words(n, ell) * (long long)sizeof(unsigned);

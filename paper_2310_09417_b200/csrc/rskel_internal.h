@@ -91,6 +91,10 @@ int launch_srtt_dense(int n, int ell, const int64_t* perm, const double* signs, 
                       double* out, long long ldo, cudaStream_t st);
 int launch_sparse_sign_dense(int n, int ell, int zeta, const int64_t* idx, const double* signs, double scale,
                              double* out, long long ldo, cudaStream_t st);
+long long srtt_workspace_bytes(long long m, int n);
+int launch_srtt_apply(long long m, int n, int ell, const double* a, long long lda, int colmajor,
+                      const int64_t* perm, const double* signs, const int64_t* cols, double scale, double* y,
+                      long long ldy, void* ws, long long ws_bytes, cudaStream_t st);
 long long sparse_sign_plan_words(int n, int ell);
 int launch_sparse_sign_apply(long long m, int n, int ell, int zeta, const double* a, long long lda, int colmajor,
                              const int64_t* idx, const double* signs, double scale, double* y, long long ldy,

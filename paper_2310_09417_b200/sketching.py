@@ -152,6 +152,9 @@ def _apply_dense(op, a):
     return _device.to_output(_device.sketch_dev(A, op.device_dense()), A)
 
 
+SRTT_FFT_MIN_ELL = 512  # sampled columns from which the FFT form beats the dense product (~450 at 20000^2)
+
+
 class SrttSketch:
     """Subsampled randomized trigonometric transform (reference
     `sketching.py:134-157`): ``y = scale * (DCT-II(x[perm]) * signs)[cols]``."""
@@ -179,7 +182,15 @@ class SrttSketch:
         return out
 
     def apply(self, a):
-        return _apply_dense(self, a)
+        """``a @ Omega``: for ell >= SRTT_FFT_MIN_ELL as the reference computes it, a
+        length-n DCT per row (`rs_srtt_apply`, O(m n log n)); below that the dense
+        embedding on the sketch engine is the cheaper pass over A."""
+        A = _device.as_matrix(a)
+        if A.cols != self.shape[0]:
+            raise DimensionError(f"operator ambient dimension {self.shape[0]} does not match {A.shape}")
+        if self.shape[1] >= SRTT_FFT_MIN_ELL:
+            return _device.to_output(_device.srtt_apply(A, self.perm, self.signs, self.cols, self.scale), A)
+        return _apply_dense(self, A)
 
     def to_dense(self):
         return self.device_dense().cpu().numpy()
@@ -283,6 +294,8 @@ def apply_sketch(a, op, side="right"):
             raise DimensionError(f"operator ambient dimension {op.shape[0]} does not match {target.shape}")
         if isinstance(op, SparseSignSketch) and op.spmm_exact():
             return _device.to_output(_device.sparse_sign_apply(target, op.idx, op.signs, op.ell, op.scale), a)
+        if isinstance(op, SrttSketch) and op.shape[1] >= SRTT_FFT_MIN_ELL:
+            return _device.to_output(_device.srtt_apply(target, op.perm, op.signs, op.cols, op.scale), a)
         return _device.to_output(_device.sketch_dev(target, op.device_dense()), a)
     omega = op if isinstance(op, np.ndarray) else getattr(op, "omega", None)
     if omega is None:

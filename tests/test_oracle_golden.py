@@ -220,6 +220,14 @@ def test_oracle_sparse_sign_spmm_order_is_the_references():
     assert np.array_equal(orc.sparse_sign_apply(a.T, idx, signs, scale, 16), g["yt"])
 
 
+def test_oracle_srtt_apply_is_the_references():
+    """The oracle's SRTT application (per-row DCT) reproduces the reference's golden y / yt."""
+    g = golden("sketch_srtt")
+    a = np.random.default_rng(80).standard_normal((90, 70))
+    assert np.array_equal(orc.srtt_apply(a, *orc.srtt_operator(81, 0, 70, 16)), g["y"])
+    assert np.array_equal(orc.srtt_apply(a.T, *orc.srtt_operator(82, 0, 90, 16)), g["yt"])
+
+
 def test_oracle_sparse_sign_adaptive_matches_reference():
     """The oracle's adaptive loop with sparse-sign blocks reproduces the reference's
     golden case (rank, status, pivots, trace)."""

@@ -11,5 +11,5 @@ T=$(mktemp -d)
 F="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr -Xcompiler -fPIC -I ../../include"
 for f in *.cu; do [ "$f" = "$SRC" ] || nvcc $F -c $f -o $T/$f.o & done
 for v in "$@"; do tag=${v%%:*}; fl=${v#*:}; nvcc $F $fl -c $SRC -o $T/v_$tag.o & done; wait
-for v in "$@"; do tag=${v%%:*}; nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../../tools/librskel_${STEM}_$tag.so $(ls $T/*.cu.o) $T/v_$tag.o; done
+for v in "$@"; do tag=${v%%:*}; nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../../tools/librskel_${STEM}_$tag.so $(ls $T/*.cu.o) $T/v_$tag.o -lcufft; done
 rm -rf $T

@@ -6,5 +6,5 @@ cd "$(dirname "$0")/../paper_2310_09417_b200/csrc"
 T=$(mktemp -d)
 F="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr -Xcompiler -fPIC -I ../../include"
 for f in *.cu; do [ "$f" = ozaki.cu ] || nvcc $F -c $f -o $T/$f.o & done; wait
-for d in "$@"; do nvcc $F $OZ_EXTRA -DOZ_NA_STAGES=$d -c ozaki.cu -o $T/oz$d.o; nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../../tools/librskel_ozna$d.so $(ls $T/*.cu.o) $T/oz$d.o; done
+for d in "$@"; do nvcc $F $OZ_EXTRA -DOZ_NA_STAGES=$d -c ozaki.cu -o $T/oz$d.o; nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../../tools/librskel_ozna$d.so $(ls $T/*.cu.o) $T/oz$d.o -lcufft; done
 rm -rf $T

@@ -7,5 +7,5 @@ T=$(mktemp -d)
 F="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr -Xcompiler -fPIC -I ../../include"
 for f in *.cu; do [ "$f" = panel.cu ] || nvcc $F -c $f -o $T/$f.o & done
 nvcc $F -DPANEL_DBG=1 $PANEL_EXTRA -c panel.cu -o $T/pdbg.o & wait
-nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../../tools/librskel_paneldbg${PANEL_TAG}.so $(ls $T/*.cu.o) $T/pdbg.o
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../../tools/librskel_paneldbg${PANEL_TAG}.so $(ls $T/*.cu.o) $T/pdbg.o -lcufft
 rm -rf $T

@@ -8,5 +8,5 @@ T=$(mktemp -d)
 F="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr -Xcompiler -fPIC -I ../../include"
 for f in *.cu; do [ "$f" = panel.cu ] || nvcc $F -c $f -o $T/$f.o & done
 for v in "$@"; do tag=${v%%:*}; fl=${v#*:}; nvcc $F $fl -c panel.cu -o $T/p_$tag.o & done; wait
-for v in "$@"; do tag=${v%%:*}; nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../../tools/librskel_panel_$tag.so $(ls $T/*.cu.o) $T/p_$tag.o; done
+for v in "$@"; do tag=${v%%:*}; nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../../tools/librskel_panel_$tag.so $(ls $T/*.cu.o) $T/p_$tag.o -lcufft; done
 rm -rf $T

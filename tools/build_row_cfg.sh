@@ -7,5 +7,5 @@ T=$(mktemp -d)
 F="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr -Xcompiler -fPIC -I ../../include"
 for f in *.cu; do [ "$f" = gemm_f64.cu ] || nvcc $F -c $f -o $T/$f.o & done; wait
 for i in ${ROW_VARIANTS:-1 2 3}; do nvcc $F -DRS_ROW_VARIANT=$i -c gemm_f64.cu -o $T/g$i.o & done; wait
-for i in ${ROW_VARIANTS:-1 2 3}; do nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../../tools/librskel_row$i.so $(ls $T/*.cu.o) $T/g$i.o; done
+for i in ${ROW_VARIANTS:-1 2 3}; do nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ../../tools/librskel_row$i.so $(ls $T/*.cu.o) $T/g$i.o -lcufft; done
 rm -rf $T
