@@ -328,6 +328,13 @@ def _presketch(a, b, rng, max_rank, spec):
     return A, yb, nb
 
 
+# experiment switch: RSKEL_LOOKAHEAD=0 sketches block t + 1 on the compute stream
+# instead of beside block t's panel and absorb
+import os as _os  # noqa: E402
+
+_LOOKAHEAD = _os.environ.get("RSKEL_LOOKAHEAD", "1") != "0"
+
+
 class _BlockOperators:
     """SRTT / sparse-sign block operators (the reference's per-block draw,
     `skeleton.py:286-295`) drawn ahead on the host thread pool: numpy releases
@@ -510,7 +517,7 @@ class _AdaptiveDriver:
             self.y_ready[slot] = None
             return
         self._issue_copy(t)
-        if ahead and self.ozaki:
+        if ahead and self.ozaki and _LOOKAHEAD:
             ss = self.sketch_stream
             ss.wait_stream(self.compute)        # the slot's previous readers are enqueued on compute
             ss.wait_event(self.om_ready[slot])
