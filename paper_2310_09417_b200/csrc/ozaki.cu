@@ -229,30 +229,35 @@ __global__ void oz_slice_kernel(const T* __restrict__ X, long long ld, int rows,
   }
   const int k = k0 + q * 16;
   if (i >= rows_pad || k >= k1_pad) return;
-  double y[16];
+  // The S digits d_s = trunc(128 y_s), y_{s+1} = 128 y_s - d_s of y = x 2^-e (|y| < 1) are the
+  // base-128 digits of trunc(|y| 2^56) with y's sign: one exact conversion per entry instead
+  // of S truncations and conversions.
+  long long t[16];
   const int e = (i < rows && k < K) ? expo[(long long)i * nch + k / kc] : 0;
+  const bool pw = e >= -1023;  // 2^-e representable: x * 2^-e rounds exactly as ldexp(x, -e)
+  const double p2 = pw ? ldexp(1.0, -e) : 0.0;
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
     const int kk = k + j;
     const double x = (i < rows && kk < K) ? ld_elem(X, ld, COLMAJOR, i, kk) : 0.0;
-    y[j] = ldexp(x, -e);  // |y| < 1, exact
+    const double y = pw ? x * p2 : ldexp(x, -e);
+    t[j] = __double2ll_rz(y * 72057594037927936.0);  // y 2^56: exact, |.| < 2^56
   }
   const int tile = i / tile_rows, r = i % tile_rows, kb = k / OZ_BK, c16 = (k % OZ_BK) / 16;
   const size_t tile_bytes = (size_t)tile_rows * OZ_BK;
   int8_t* base = dig + ((size_t)tile * KB + kb) * S * tile_bytes + (size_t)(r >> 3) * 1024 + (r & 7) * 128 +
                  ((c16 ^ (r & 7)) * 16);
   for (int s = 0; s < S; ++s) {
+    const int sh = 7 * (7 - s);
     uint32_t w[4];
 #pragma unroll
     for (int j4 = 0; j4 < 4; ++j4) {
       uint32_t packed = 0;
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
-        const int j = j4 * 4 + b;
-        const double z = y[j] * 128.0;  // exact
-        const double d = trunc(z);      // |d| <= 127
-        y[j] = z - d;                   // exact
-        packed |= (uint32_t)(uint8_t)(int8_t)(int)d << (8 * b);
+        const long long tj = t[j4 * 4 + b];
+        const int mag = (int)(((unsigned long long)(tj < 0 ? -tj : tj) >> sh) & 127u);
+        packed |= (uint32_t)(uint8_t)(int8_t)(tj < 0 ? -mag : mag) << (8 * b);
       }
       w[j4] = packed;
     }
