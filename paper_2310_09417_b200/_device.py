@@ -588,6 +588,13 @@ def srtt_apply(a, perm, signs, cols, scale, out=None):
     m, n = a.shape
     dev = device()
     ell = len(cols)
+    perm, cols = np.asarray(perm), np.asarray(cols)
+    for name, ix in (("perm", perm), ("cols", cols)):  # numpy's fancy indexing would raise the same
+        if ix.size and (ix.min() < -n or ix.max() >= n):
+            raise IndexError(f"SRTT {name} index out of bounds for size {n}")
+    perm, cols = np.where(perm < 0, perm + n, perm), np.where(cols < 0, cols + n, cols)
+    if len(perm) != n or len(np.asarray(signs)) != n:
+        raise DimensionError(f"SRTT operator of size {len(perm)} does not match {n} columns")
     perm_d = torch.as_tensor(np.ascontiguousarray(perm, dtype=np.int64)).to(dev)
     sg_d = torch.as_tensor(np.ascontiguousarray(signs, dtype=np.float64)).to(dev)
     cols_d = torch.as_tensor(np.ascontiguousarray(cols, dtype=np.int64)).to(dev)

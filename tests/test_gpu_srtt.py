@@ -86,3 +86,22 @@ def test_fft_and_dense_forms_agree():
     fft = _device.srtt_apply(A, op.perm, op.signs, op.cols, op.scale).cpu().numpy()
     dense = _device.sketch_dev(A, op.device_dense()).cpu().numpy()
     _check(fft, dense, a)
+
+
+def test_invalid_operator_indices_raise():
+    """Out-of-range permutation / sampled-column indices raise IndexError as numpy's
+    indexing does in the reference; negative indices wrap as in numpy."""
+    from paper_2310_09417_b200 import _device, sketching
+
+    n, ell = 600, 520
+    perm, signs, cols, scale = orc.srtt_operator(3, 0, n, ell)
+    a = np.random.default_rng(2).standard_normal((10, n))
+    bad = cols.copy()
+    bad[3] = n
+    with pytest.raises(IndexError):
+        sketching.SrttSketch(perm, signs, bad, scale).apply(a)
+    neg = cols.copy()
+    neg[4] = neg[4] - n
+    want = orc.srtt_apply(a, perm, signs, cols, scale)
+    got = _device.srtt_apply(_device.as_matrix(a), perm, signs, neg, scale).cpu().numpy()
+    _check(got, want, a)
