@@ -455,6 +455,8 @@ class _AdaptiveDriver:
         self.st = _engine.TFormState(m, max(max_rank, b), min(b, _engine.MAX_BLOCK))
         # tensor-core sketch: A's digit planes once, Omega_t's per block
         self.ozaki = _ozaki.sketch_engine() == "ozaki" and self.yb is None and self.kind != "sparsesign"
+        if self.kind == "sparsesign":  # the look-ahead SpMM's stream
+            self.sketch_stream = torch.cuda.Stream(device=dev)
         if self.ozaki:
             tok = self.prof.start("a_slice")
             self.ap = planes if planes is not None else _ozaki.Planes.of_matrix(a)
@@ -508,9 +510,19 @@ class _AdaptiveDriver:
             return
         slot = t % 2
         if self.kind == "sparsesign":
-            # the reference's per-block operator (`skeleton.py:286-295`) applied
-            # as an SpMM on the compute stream: Y_t bitwise the reference's
+            # the reference's per-block operator (`skeleton.py:286-295`) applied as an
+            # SpMM (Y_t bitwise the reference's); the look-ahead block on its own stream,
+            # where its small CTAs can share the SMs with the cooperative panel
             op = self.ops_ahead.get(t)
+            if ahead and _LOOKAHEAD:
+                ss = self.sketch_stream
+                ss.wait_stream(self.compute)  # the slot's previous readers
+                with torch.cuda.stream(ss):
+                    _device.sparse_sign_apply(self.a, op.idx, op.signs, op.ell, op.scale, out=self.y[slot])
+                    ev = torch.cuda.Event()
+                    ev.record(ss)
+                self.y_ready[slot] = ev
+                return
             tok = self.prof.start("sketch_gemm")
             _device.sparse_sign_apply(self.a, op.idx, op.signs, op.ell, op.scale, out=self.y[slot])
             self.prof.stop(tok)
@@ -686,7 +698,7 @@ class _AdaptiveDriver:
                 self.ops_ahead.close()
             # speculative draws / sketches may still be in flight on the side streams
             self.compute.wait_stream(self.copy_stream)
-            if self.ozaki:
+            if self.ozaki or self.kind == "sparsesign":
                 self.compute.wait_stream(self.sketch_stream)
         if self.dev_rng and bool(self.rng_status.any()):
             # a block the parallel ziggurat resolver could not place (never
