@@ -120,10 +120,26 @@ __global__ void sumsq_stage1(const double* __restrict__ X, long long ldx, int R,
   int r0 = blockIdx.x * rows_per, r1 = min(R, r0 + rows_per);
   double acc = 0.0;
   long long n = (long long)(r1 > r0 ? r1 - r0 : 0) * w;
-  for (long long e = threadIdx.x; e < n; e += SS_THREADS) {
-    int i = (int)(e / w), c = (int)(e - (long long)i * w);
-    double v = X[(long long)(r0 + i) * ldx + c];
-    acc = fma(v, v, acc);
+  // thread t takes elements t, t + 256, ... of the CTA's rows (row-major order), in that order
+  if (ldx == w) {  // contiguous rows: the element index is the offset
+    const double* base = X + (long long)r0 * ldx;
+    for (long long e = threadIdx.x; e < n; e += SS_THREADS) {
+      const double v = base[e];
+      acc = fma(v, v, acc);
+    }
+  } else {  // (row, column) advanced by 256 elements per step without a division
+    const int q = SS_THREADS / w, rq = SS_THREADS % w;
+    int i = threadIdx.x / w, c = threadIdx.x % w;
+    for (long long e = threadIdx.x; e < n; e += SS_THREADS) {
+      const double v = X[(long long)(r0 + i) * ldx + c];
+      acc = fma(v, v, acc);
+      i += q;
+      c += rq;
+      if (c >= w) {
+        c -= w;
+        ++i;
+      }
+    }
   }
   red[threadIdx.x] = acc;
   __syncthreads();
