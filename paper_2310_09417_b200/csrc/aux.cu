@@ -265,7 +265,12 @@ int launch_trinv(const double* T, long long rs_, long long cs_, const int64_t* r
 // x_j -= y_a L1[a][j] for all j < a -- 63 independent FMAs per step), L1 as
 // shared-memory broadcasts.  Replaces the trinv + GEMM pair of the absorb.
 constexpr int WH_T = 128;
+constexpr int WH_G = 4;  // lanes per row: lane g of a group owns x[j], j = g mod 4
 
+// Four lanes per row (four times the warps of one row per thread, which left ~4 warps per
+// SM at R = 20000): step a takes y_a = x[a] from its owner lane by shuffle, then every lane
+// folds it into its own x[j], j < a.  Each x[j] sees the same fma sequence in the same order
+// as a one-row-per-thread substitution, so the bits are unchanged.
 __global__ void __launch_bounds__(WH_T) what_kernel(const double* __restrict__ S, long long lds,
                                                     const int64_t* __restrict__ sub, int nc,
                                                     const int64_t* __restrict__ ridx, int R,
@@ -276,29 +281,41 @@ __global__ void __launch_bounds__(WH_T) what_kernel(const double* __restrict__ S
     L1[a][b] = (a < nc && b < a) ? S[sub[a] * lds + b] : 0.0;
   }
   __syncthreads();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= R) return;
-  const double* src = S + ridx[i] * lds;
-  double x[TI_MAX];
+  constexpr int NJ = TI_MAX / WH_G;
+  const int lane = threadIdx.x & 31, g = lane & (WH_G - 1);
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) / WH_G;
+  const bool live = i < R;  // every lane takes part in the shuffles
+  const double* src = S + (live ? ridx[i] : 0) * lds;
+  double x[NJ];
 #pragma unroll
-  for (int j = 0; j < TI_MAX; ++j) x[j] = j < nc ? src[j] : 0.0;
+  for (int jj = 0; jj < NJ; ++jj) {
+    const int j = jj * WH_G + g;
+    x[jj] = (live && j < nc) ? src[j] : 0.0;
+  }
 #pragma unroll
   for (int a = TI_MAX - 1; a > 0; --a) {
-    const double ya = x[a];  // final (unit diagonal)
+    const double ya = __shfl_sync(0xffffffffu, x[a / WH_G], (lane & ~(WH_G - 1)) | (a % WH_G), 32);
 #pragma unroll
-    for (int j = 0; j < a; ++j) x[j] = fma(-ya, L1[a][j], x[j]);
+    for (int jj = 0; jj < NJ; ++jj) {
+      const int j = jj * WH_G + g;
+      if (jj * WH_G < a && j < a) x[jj] = fma(-ya, L1[a][j], x[jj]);
+    }
   }
+  if (!live) return;
   double* dst = out + (long long)i * ldo;
 #pragma unroll
-  for (int j = 0; j < TI_MAX; ++j)
-    if (j < nc) dst[j] = x[j];
+  for (int jj = 0; jj < NJ; ++jj) {
+    const int j = jj * WH_G + g;
+    if (j < nc) dst[j] = x[jj];
+  }
 }
 
 int launch_what(const double* S, long long lds, const int64_t* sub, int nc, const int64_t* ridx, int R, double* out,
                 long long ldo, cudaStream_t st) {
   if (nc < 0 || nc > TI_MAX || R < 0 || ldo < nc) return RS_ERR_ARG;
   if (nc == 0 || R == 0) return RS_OK;
-  what_kernel<<<(R + WH_T - 1) / WH_T, WH_T, 0, st>>>(S, lds, sub, nc, ridx, R, out, ldo);
+  what_kernel<<<(unsigned)(((long long)R * WH_G + WH_T - 1) / WH_T), WH_T, 0, st>>>(S, lds, sub, nc, ridx, R, out,
+                                                                                  ldo);
   count_launch(1);
   return cudaGetLastError() == cudaSuccess ? RS_OK : RS_ERR_CUDA;
 }
